@@ -1,0 +1,217 @@
+// TEST INFRASTRUCTURE ONLY. Our driver over the UNMODIFIED reference library (built from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/). It is the reference side of
+// the parity contract and the bench's CPU reference arm; the product never links it.
+//
+//   ref_driver golden <L> <heads> <kv> <dim> <causal> <seed> <out.bin>
+//       single-device oracle, loss = sum(out * R) (mirrors report.cpp:61-85) plus the lse of
+//       attn_block_forward + finalize_piece (attention.cpp:61-165)
+//   ref_driver engine <engine> <sp> <L> <heads> <kv> <dim> <u> <r> <seed> <out.bin>
+//       sharded run gathered to global order (mirrors report.cpp:95-133) + per-rank bytes
+//   ref_driver bench <engine> <sp> <L> <heads> <kv> <dim> <steps>
+//       wall time of fwd+bwd of run_attention_engine, one thread per rank (comm.cpp:197-222)
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "seqpar/attention.hpp"
+#include "seqpar/comm.hpp"
+#include "seqpar/partition.hpp"
+#include "seqpar/report.hpp"
+#include "seqpar/tensor.hpp"
+
+using namespace seqpar;
+
+namespace {
+
+struct Data {
+  std::vector<double> q, k, v, R;
+};
+
+// Same draw order as report.cpp:42-54 (q, k, v, R; uniform(-2, 2)).
+Data make_data(uint64_t seed, int64_t L, int heads, int kv, int dim) {
+  Rng rng(seed);
+  Data d;
+  auto fill = [&](std::vector<double>& x, int64_t n) {
+    x.resize(static_cast<size_t>(n));
+    for (double& e : x) e = rng.uniform_range(-2.0, 2.0);
+  };
+  fill(d.q, L * heads * dim);
+  fill(d.k, L * kv * dim);
+  fill(d.v, L * kv * dim);
+  fill(d.R, L * heads * dim);
+  return d;
+}
+
+void put(FILE* f, const std::vector<double>& x) {
+  const int64_t n = static_cast<int64_t>(x.size());
+  std::fwrite(&n, sizeof(n), 1, f);
+  std::fwrite(x.data(), sizeof(double), x.size(), f);
+}
+
+ShardLayout layout_for(Engine e, int64_t L, int sp, int u, int r) {
+  if (e == Engine::ring) return ShardLayout::make_zigzag(L, sp);
+  if (e == Engine::usp) return ShardLayout::make_usp(L, u, r);
+  return ShardLayout::make_naive(L, sp);
+}
+
+int golden(int argc, char** argv) {
+  if (argc != 9) return 2;
+  const int64_t L = std::atoll(argv[2]);
+  const int heads = std::atoi(argv[3]), kv = std::atoi(argv[4]), dim = std::atoi(argv[5]);
+  const bool causal = std::atoi(argv[6]) != 0;
+  const uint64_t seed = std::strtoull(argv[7], nullptr, 10);
+  Data d = make_data(seed, L, heads, kv, dim);
+  Tensor q = Tensor::from({1, L, heads, dim}, d.q, true);
+  Tensor k = Tensor::from({1, L, kv, dim}, d.k, true);
+  Tensor v = Tensor::from({1, L, kv, dim}, d.v, true);
+  Tensor R = Tensor::from({1, L, heads, dim}, d.R);
+  std::vector<int64_t> pos(static_cast<size_t>(L));
+  std::iota(pos.begin(), pos.end(), int64_t{0});
+  std::vector<double> out;
+  Tape tape;
+  {
+    TapeScope sc(&tape);
+    const int64_t rep = heads / kv;
+    Tensor ke = rep > 1 ? repeat_heads(k, rep) : k;
+    Tensor ve = rep > 1 ? repeat_heads(v, rep) : v;
+    Tensor o = oracle_attention(q, ke, ve, pos, causal);
+    tape.backward(sum_all(mul(o, R)));
+    out.assign(o.values().begin(), o.values().end());
+  }
+  // lse through the block kernel on expanded kv
+  const int64_t rep = heads / kv;
+  std::vector<double> ke(static_cast<size_t>(L * heads * dim)), ve(ke.size());
+  for (int64_t i = 0; i < L; ++i)
+    for (int h = 0; h < heads; ++h)
+      for (int c = 0; c < dim; ++c) {
+        ke[(i * heads + h) * dim + c] = d.k[(i * kv + h / rep) * dim + c];
+        ve[(i * heads + h) * dim + c] = d.v[(i * kv + h / rep) * dim + c];
+      }
+  AttnPiece p = attn_block_forward(1, heads, dim, d.q, pos, ke, ve, pos, causal,
+                                   1.0 / std::sqrt(static_cast<double>(dim)));
+  std::vector<double> out2, lse;
+  finalize_piece(p, out2, lse);
+  FILE* f = std::fopen(argv[8], "wb");
+  if (!f) return 3;
+  put(f, d.q); put(f, d.k); put(f, d.v); put(f, d.R);
+  put(f, out); put(f, lse);
+  put(f, std::vector<double>(q.grad().begin(), q.grad().end()));
+  put(f, std::vector<double>(k.grad().begin(), k.grad().end()));
+  put(f, std::vector<double>(v.grad().begin(), v.grad().end()));
+  std::fclose(f);
+  return 0;
+}
+
+int engine(int argc, char** argv) {
+  if (argc != 12) return 2;
+  const Engine e = engine_from_string(argv[2]);
+  const int sp = std::atoi(argv[3]);
+  const int64_t L = std::atoll(argv[4]);
+  const int heads = std::atoi(argv[5]), kv = std::atoi(argv[6]), dim = std::atoi(argv[7]);
+  const int u = std::atoi(argv[8]), r = std::atoi(argv[9]);
+  const uint64_t seed = std::strtoull(argv[10], nullptr, 10);
+  Data d = make_data(seed, L, heads, kv, dim);
+  const ShardLayout layout = layout_for(e, L, sp, u, r);
+  const int64_t qw = static_cast<int64_t>(heads) * dim, kw = static_cast<int64_t>(kv) * dim;
+  AttentionConfig cfg{.heads = heads, .kv_heads = kv, .head_dim = dim, .causal = true,
+                      .ulysses_degree = u, .ring_degree = r};
+  std::vector<std::vector<double>> outs(sp), dqs(sp), dks(sp), dvs(sp);
+  CommFabric fabric(sp, sp, SchedulerKind::threaded);
+  fabric.run([&](RankCtx& ctx) {
+    const int idx = ctx.sp_group.index_of(ctx.rank);
+    const int64_t l = layout.local_len();
+    Tensor ql = Tensor::from({1, l, heads, dim}, shard_rows(d.q, qw, layout, idx), true);
+    Tensor kl = Tensor::from({1, l, kv, dim}, shard_rows(d.k, kw, layout, idx), true);
+    Tensor vl = Tensor::from({1, l, kv, dim}, shard_rows(d.v, kw, layout, idx), true);
+    Tensor Rl = Tensor::from({1, l, heads, dim}, shard_rows(d.R, qw, layout, idx));
+    Tape tape;
+    TapeScope sc(&tape);
+    Tensor out = run_attention_engine(ctx, e, cfg, layout, ql, kl, vl);
+    tape.backward(sum_all(mul(out, Rl)));
+    outs[idx].assign(out.values().begin(), out.values().end());
+    dqs[idx].assign(ql.grad().begin(), ql.grad().end());
+    dks[idx].assign(kl.grad().begin(), kl.grad().end());
+    dvs[idx].assign(vl.grad().begin(), vl.grad().end());
+  });
+  FILE* f = std::fopen(argv[11], "wb");
+  if (!f) return 3;
+  put(f, gather_rows(outs, qw, layout));
+  put(f, gather_rows(dqs, qw, layout));
+  put(f, gather_rows(dks, kw, layout));
+  put(f, gather_rows(dvs, kw, layout));
+  std::vector<double> bytes, a2a, ag, p2p;
+  for (int rk = 0; rk < sp; ++rk) {
+    bytes.push_back(static_cast<double>(fabric.total_bytes(rk)));
+    a2a.push_back(static_cast<double>(fabric.stats(rk, Primitive::all_to_all).bytes));
+    ag.push_back(static_cast<double>(fabric.stats(rk, Primitive::all_gather).bytes));
+    p2p.push_back(static_cast<double>(fabric.stats(rk, Primitive::p2p).bytes));
+  }
+  put(f, bytes); put(f, a2a); put(f, ag); put(f, p2p);
+  std::fclose(f);
+  return 0;
+}
+
+int bench(int argc, char** argv) {
+  if (argc != 9) return 2;
+  const Engine e = engine_from_string(argv[2]);
+  const int sp = std::atoi(argv[3]);
+  const int64_t L = std::atoll(argv[4]);
+  const int heads = std::atoi(argv[5]), kv = std::atoi(argv[6]), dim = std::atoi(argv[7]);
+  const int steps = std::atoi(argv[8]);
+  Data d = make_data(1, L, heads, kv, dim);
+  const ShardLayout layout = layout_for(e, L, sp, 0, 0);
+  const int64_t qw = static_cast<int64_t>(heads) * dim, kw = static_cast<int64_t>(kv) * dim;
+  AttentionConfig cfg{.heads = heads, .kv_heads = kv, .head_dim = dim, .causal = true};
+  CommFabric fabric(sp, sp, SchedulerKind::threaded);
+  std::vector<double> secs;
+  for (int s = 0; s < steps; ++s) {
+    const auto t0 = std::chrono::steady_clock::now();
+    fabric.run([&](RankCtx& ctx) {
+      const int idx = ctx.sp_group.index_of(ctx.rank);
+      const int64_t l = layout.local_len();
+      Tensor ql = Tensor::from({1, l, heads, dim}, shard_rows(d.q, qw, layout, idx), true);
+      Tensor kl = Tensor::from({1, l, kv, dim}, shard_rows(d.k, kw, layout, idx), true);
+      Tensor vl = Tensor::from({1, l, kv, dim}, shard_rows(d.v, kw, layout, idx), true);
+      Tensor Rl = Tensor::from({1, l, heads, dim}, shard_rows(d.R, qw, layout, idx));
+      Tape tape;
+      TapeScope sc(&tape);
+      Tensor out = run_attention_engine(ctx, e, cfg, layout, ql, kl, vl);
+      tape.backward(sum_all(mul(out, Rl)));
+    });
+    secs.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  }
+  double tot = 0;
+  for (double x : secs) tot += x;
+  const double per = tot / steps;
+  std::printf("{\"engine\": \"%s\", \"sp\": %d, \"L\": %lld, \"heads\": %d, \"kv\": %d, \"dim\": %d, "
+              "\"steps\": %d, \"s_per_step\": %.6f, \"tokens_per_s\": %.6f, \"flops_rank0\": %lld}\n",
+              argv[2], sp, static_cast<long long>(L), heads, kv, dim, steps, per,
+              static_cast<double>(L) / per, static_cast<long long>(fabric.flops(0)));
+  return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::fprintf(stderr, "usage: ref_driver golden|engine|bench ...\n");
+    return 2;
+  }
+  try {
+    const std::string mode = argv[1];
+    int rc = 2;
+    if (mode == "golden") rc = golden(argc, argv);
+    else if (mode == "engine") rc = engine(argc, argv);
+    else if (mode == "bench") rc = bench(argc, argv);
+    if (rc == 2) std::fprintf(stderr, "bad arguments for %s\n", mode.c_str());
+    return rc;
+  } catch (const std::exception& ex) {
+    std::fprintf(stderr, "error: %s\n", ex.what());
+    return 1;
+  }
+}
