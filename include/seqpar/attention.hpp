@@ -1,0 +1,102 @@
+// B200 mirror of the reference attention-engine API
+// (/root/reference/proj/include/seqpar/attention.hpp). Same engine names, AttentionConfig
+// fields and error behaviour; tensors are device views (bf16, [bs, len, heads, dim]
+// contiguous) and the tape node becomes an explicit forward -> SavedState -> backward pair.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "seqpar/comm.hpp"
+#include "seqpar/partition.hpp"
+
+namespace seqpar {
+
+enum class Engine { oracle, ulysses, dummy_head, xtuner, ring, usp };  // attention.hpp:14
+const char* engine_name(Engine e);
+Engine engine_from_string(const std::string& s);
+
+struct AttentionConfig {  // attention.hpp:19-26
+  int heads = 1;
+  int kv_heads = 0;  // 0 = heads
+  int head_dim = 1;
+  bool causal = true;
+  int ulysses_degree = 0;  // usp only
+  int ring_degree = 0;     // usp only
+};
+
+// Non-owning device view of a [bs, len, heads, dim] bf16 tensor, contiguous.
+struct DeviceTensor {
+  void* data = nullptr;
+  int64_t bs = 0, len = 0, heads = 0, dim = 0;
+  int64_t numel() const { return bs * len * heads * dim; }
+};
+
+// Everything the backward needs (the reference's tape closure captures, attention.cpp:236-258).
+// Owns the engine's device workspace; q/k/v/out views must stay valid until backward.
+struct SavedState;
+void saved_state_free(SavedState* s);
+struct SavedDeleter {
+  void operator()(SavedState* s) const { saved_state_free(s); }
+};
+using SavedPtr = std::unique_ptr<SavedState, SavedDeleter>;
+
+// Neat-packed documents (varlen): consecutive global positions [0, L) are cut into documents
+// of these lengths; a query only sees keys of its own document (causal by global index).
+// Empty = one document. The reference has no varlen path; the composed oracle runs
+// oracle_attention per document.
+struct Documents {
+  std::vector<int64_t> lengths;
+};
+
+// attention.hpp:90-92. q [bs, local_len, heads, dim], k/v [bs, local_len, kv_heads, dim];
+// out has q's shape; lse (optional) is [bs, local_len, heads] fp32 natural log.
+SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig& cfg,
+                              const ShardLayout& layout, const DeviceTensor& q,
+                              const DeviceTensor& k, const DeviceTensor& v,
+                              const DeviceTensor& out, float* lse,
+                              const Documents* docs = nullptr);
+
+// The tape node's backward: dq/dk/dv are written (not accumulated) in q/k/v's layouts.
+void run_attention_engine_backward(RankCtx& ctx, SavedState& saved, const DeviceTensor& dout,
+                                   const DeviceTensor& dq, const DeviceTensor& dk,
+                                   const DeviceTensor& dv);
+
+// A view shaped like the forward's q (which=0) or k/v (which=1) over `data`.
+DeviceTensor saved_view(const SavedState& s, int which, void* data);
+
+// ---- kernel-level API (attention.hpp:43-66) on device buffers ----
+// attn_block_forward + merge_piece fused: merges the block's piece into the running fp32
+// accumulator (acc_out [bs, lq, heads, dim], acc_lse [bs, lq, heads]; lse = -inf marks an empty
+// row). finalize_piece is block_finalize. Positions are host int64 lists (run-structured).
+void block_forward_merge(cudaStream_t s, int64_t bs, int heads, int kv_heads, int dim,
+                         const void* q, const std::vector<int64_t>& qpos, const void* k,
+                         const void* v, const std::vector<int64_t>& kpos, bool causal,
+                         double scale, float* acc_out, float* acc_lse, int64_t* pairs = nullptr);
+void block_finalize(cudaStream_t s, int64_t rows, int dim, const float* acc_out, void* out_bf16);
+// attn_block_backward: += into fp32 dq [bs,lq,heads,dim], dk/dv [bs,lk,kv_heads,dim].
+void block_backward(cudaStream_t s, int64_t bs, int heads, int kv_heads, int dim, const void* q,
+                    const std::vector<int64_t>& qpos, const void* k, const void* v,
+                    const std::vector<int64_t>& kpos, bool causal, double scale, const void* out,
+                    const float* lse, const void* dout, float* dq, float* dk, float* dv,
+                    int64_t* pairs = nullptr);
+
+// Reference all_to_all (comm.cpp:357-379) on a [bs, len, heads, dim] tensor of any element
+// size: scatter_dim/gather_dim in {1, 2}. out shape follows the reference.
+void all_to_all(RankCtx& ctx, const CommGroup& group, const void* local, int64_t bs, int64_t len,
+                int64_t heads, int64_t dim, int elem_bytes, int scatter_dim, int gather_dim,
+                void* out);
+
+// Event timing of the attention kernels (bench.py): ms[0]/n[0] forward, ms[1]/n[1] backward.
+void profile_enable(bool on);
+void profile_read(double* ms, int64_t* n);
+
+// Which attention kernel family the engines launch.
+enum class KernelFamily { tcgen05, mma };
+void set_kernel_family(KernelFamily f);
+KernelFamily kernel_family();
+
+}  // namespace seqpar

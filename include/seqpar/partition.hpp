@@ -1,0 +1,65 @@
+// B200 mirror of the reference partition API (/root/reference/proj/include/seqpar/partition.hpp).
+// Pure host integer code: which global positions each SP group index owns, padding quantum,
+// causal pair counts. Same names, argument meaning and ConfigError behaviour.
+#pragma once
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace seqpar {
+
+// tensor.hpp:18-26 (ShapeError / ConfigError / StateError)
+struct ShapeError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StateError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+enum class SplitMode { naive, zigzag, usp };  // partition.hpp:14
+const char* split_mode_name(SplitMode m);
+SplitMode split_mode_from_string(const std::string& s);
+
+// partition.hpp:21-36
+struct ShardLayout {
+  SplitMode mode = SplitMode::naive;
+  int sp = 1;
+  int64_t global_len = 0;
+  int u_degree = 0;
+  int r_degree = 0;
+  std::vector<std::vector<int64_t>> owned;
+
+  static ShardLayout make_naive(int64_t len, int sp);    // partition.cpp:37-51
+  static ShardLayout make_zigzag(int64_t len, int sp);   // partition.cpp:53-73
+  static ShardLayout make_usp(int64_t len, int ulysses_degree, int ring_degree);  // :75-103
+
+  int64_t local_len() const { return global_len / sp; }
+  const std::vector<int64_t>& positions_of(int index) const;
+  bool operator==(const ShardLayout& o) const;
+};
+
+int64_t causal_pair_count(const ShardLayout& layout, int index);  // partition.cpp:118-122
+std::vector<int64_t> make_position_ids(const ShardLayout& layout, int index);  // :160-162
+int64_t pad_length(int64_t len, int sp, int64_t cutoff_len, bool pad_to_cutoff = false);  // :179-200
+int pick_xtuner_insp(int heads, int sp, int head_dim);  // attention.cpp:354-366
+
+// Closed-form per-rank fwd+bwd bytes in the reference's own accounting (f64 elements, KV
+// expanded to q heads): report.cpp:906-941.
+int64_t ulysses_bytes(int64_t bs, int64_t len, int64_t heads, int64_t head_dim, int sp);
+int64_t ring_bytes(int64_t bs, int64_t len, int64_t heads, int64_t head_dim, int sp);
+int64_t dummy_head_bytes(int64_t bs, int64_t len, int64_t heads, int64_t head_dim, int sp);
+int64_t xtuner_bytes(int64_t bs, int64_t len, int64_t heads, int64_t head_dim, int sp);
+int64_t usp_bytes(int64_t bs, int64_t len, int64_t heads, int64_t head_dim, int u, int r);
+
+// Contiguous position runs of a position list: rows [row0, row0+n) hold positions
+// [pos0, pos0+n). The kernels work on runs instead of per-row position arrays.
+struct PosRun {
+  int64_t row0, pos0, n;
+};
+std::vector<PosRun> position_runs(const std::vector<int64_t>& positions);
+
+}  // namespace seqpar

@@ -1,0 +1,149 @@
+/* spattn — C ABI of the B200 sequence-parallel attention layer (libspattn.so).
+ *
+ * Drop-in boundary for the reference's SP attention path
+ * (/root/reference/proj, C++20 library `seqpar`). Every entry point replaces one reference
+ * interface, cited below; INTEGRATION.md shows the binding a maintainer adds on the reference
+ * side. Plain pointers and sizes only: device buffers are bf16 [bs, len, heads, dim]
+ * contiguous (lse fp32 [bs, len, heads], natural log). Exceptions never cross this boundary:
+ * every call returns a status and spattn_last_error() (thread-local) holds the message —
+ * the reference throws ConfigError / ShapeError / StateError (tensor.hpp:18-26) and its
+ * Python module maps them to ValueError (py_module.cpp:320-321).
+ */
+#ifndef SPATTN_H
+#define SPATTN_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SPATTN_OK = 0,
+  SPATTN_ERR_CONFIG = 1, /* seqpar::ConfigError */
+  SPATTN_ERR_SHAPE = 2,  /* seqpar::ShapeError */
+  SPATTN_ERR_STATE = 3,  /* seqpar::StateError, CUDA and NCCL failures */
+  SPATTN_ERR_PEER = 4    /* a peer rank failed (CommFabric PeerAbort, comm.cpp:10-14) */
+};
+
+/* Engine (attention.hpp:14) and SplitMode (partition.hpp:14) enumerations, same order. */
+enum { SPATTN_ORACLE = 0, SPATTN_ULYSSES, SPATTN_DUMMY_HEAD, SPATTN_XTUNER, SPATTN_RING, SPATTN_USP };
+enum { SPATTN_NAIVE = 0, SPATTN_ZIGZAG, SPATTN_SPLIT_USP };
+/* Primitive (comm.hpp:19) */
+enum { SPATTN_ALL_TO_ALL = 0, SPATTN_ALL_GATHER, SPATTN_P2P, SPATTN_ALL_REDUCE, SPATTN_BROADCAST };
+
+/* AttentionConfig (attention.hpp:19-26) */
+typedef struct {
+  int32_t heads, kv_heads, head_dim, causal, ulysses_degree, ring_degree;
+} spattn_config;
+
+/* ShardLayout::make_naive / make_zigzag / make_usp arguments (partition.hpp:29-31) */
+typedef struct {
+  int32_t mode, sp;
+  int64_t global_len;
+  int32_t u_degree, r_degree;
+} spattn_layout;
+
+typedef struct spattn_ctx spattn_ctx;       /* RankCtx (comm.hpp:63-82): one per rank */
+typedef struct spattn_fabric spattn_fabric; /* CommFabric (comm.hpp:86-140): loopback ranks */
+typedef struct spattn_saved spattn_saved;   /* the tape closure's captures (attention.cpp:236-258) */
+
+const char* spattn_last_error(void);
+int spattn_abi_version(void);
+
+/* ---- partition / report host functions (pure integer, no GPU) ---- */
+/* ShardLayout::positions_of (partition.cpp:105-111); out holds global_len/sp entries */
+int spattn_layout_positions(const spattn_layout* layout, int index, int64_t* out);
+/* causal_pair_count (partition.cpp:118-122) */
+int spattn_causal_pairs(const spattn_layout* layout, int index, int64_t* out);
+/* pad_length (partition.cpp:179-200) */
+int spattn_pad_length(int64_t len, int sp, int64_t cutoff_len, int pad_to_cutoff, int64_t* out);
+/* pick_xtuner_insp (attention.cpp:354-366) */
+int spattn_pick_xtuner_insp(int heads, int sp, int head_dim, int* out);
+/* ulysses/ring/dummy_head/xtuner/usp_bytes (report.cpp:906-941), reference accounting */
+int spattn_reference_bytes(int engine, int64_t bs, int64_t len, int64_t heads, int64_t head_dim,
+                           int sp, int u, int r, int64_t* out);
+
+/* ---- contexts ---- */
+/* NCCL backend: one process per GPU. rank 0 creates the id, the launcher broadcasts it. */
+int spattn_nccl_unique_id(uint8_t out[128]);
+int spattn_ctx_create_nccl(int device, int rank, int world, int sp, const uint8_t unique_id[128],
+                           spattn_ctx** out);
+int spattn_ctx_destroy(spattn_ctx* ctx);
+/* Loopback fabric: `world` ranks as threads sharing one device (CommFabric::run analog).
+ * force_messages=1 routes collectives through the pack -> send/recv -> unpack path. */
+int spattn_fabric_create(int device, int world, int sp, int force_messages, spattn_fabric** out);
+int spattn_fabric_destroy(spattn_fabric* f);
+int spattn_fabric_ctx(spattn_fabric* f, int rank, spattn_ctx** out);
+/* Compute stream of a context (cudaStream_t); NULL restores the context's own stream. */
+int spattn_ctx_set_stream(spattn_ctx* ctx, void* stream);
+int spattn_ctx_stream(spattn_ctx* ctx, void** stream);
+/* send-side per-primitive counters (PrimitiveStats, comm.hpp:30-33) and flop counter */
+int spattn_ctx_stats(spattn_ctx* ctx, int primitive, int64_t* calls, int64_t* bytes);
+int spattn_ctx_flops(spattn_ctx* ctx, int64_t* flops);
+int spattn_ctx_reset_stats(spattn_ctx* ctx);
+/* 0 = tcgen05/TMEM kernels (default where supported), 1 = mma.sync kernels */
+int spattn_set_kernel_family(int family);
+int spattn_get_kernel_family(void);
+
+/* Diagnostics for the bench: number of kernels this library has launched, and CUDA-event
+ * timing of the attention kernels (fwd: ms[0], n[0]; bwd: ms[1], n[1]) since enabling. */
+int64_t spattn_launch_count(void);
+int spattn_profile_enable(int on);
+int spattn_profile_read(double ms[2], int64_t n[2]);
+
+/* ---- engine: run_attention_engine (attention.hpp:90-92) + its tape backward ----
+ * Collective over the SP group: every rank calls with its shard. q [bs, local_len, heads, d],
+ * k/v [bs, local_len, kv_heads, d], out like q, lse optional. doc_lens (optional, n_docs>0)
+ * cuts the global sequence into neat-packed documents (varlen). *saved must be released with
+ * spattn_saved_free; q/k/v/out must stay valid until spattn_bwd. Stream-ordered on the
+ * context's compute stream. */
+int spattn_fwd(spattn_ctx* ctx, int engine, const spattn_config* cfg, const spattn_layout* layout,
+               int64_t bs, const void* q, const void* k, const void* v, void* out, float* lse,
+               const int64_t* doc_lens, int n_docs, spattn_saved** saved);
+int spattn_bwd(spattn_ctx* ctx, spattn_saved* saved, const void* dout, void* dq, void* dk,
+               void* dv);
+void spattn_saved_free(spattn_saved* saved);
+
+/* Loopback group drivers: one call runs every rank on its own thread (arrays of world
+ * pointers), returning when all ranks' streams are idle. */
+int spattn_fabric_fwd(spattn_fabric* f, int engine, const spattn_config* cfg,
+                      const spattn_layout* layout, int64_t bs, const void* const* q,
+                      const void* const* k, const void* const* v, void* const* out,
+                      float* const* lse, const int64_t* doc_lens, int n_docs,
+                      spattn_saved** saved);
+int spattn_fabric_bwd(spattn_fabric* f, spattn_saved* const* saved, const void* const* dout,
+                      void* const* dq, void* const* dk, void* const* dv);
+/* all_to_all (comm.cpp:357-379) on [bs, len, heads, dim] tensors of elem_bytes each */
+int spattn_fabric_all_to_all(spattn_fabric* f, const void* const* local, void* const* out,
+                             int64_t bs, int64_t len, int64_t heads, int64_t dim, int elem_bytes,
+                             int scatter_dim, int gather_dim);
+
+/* ---- kernel-level API (attention.hpp:43-66) ---- */
+/* attn_block_forward + merge_piece: merges into acc_out (fp32 [bs,lq,heads,dim]) / acc_lse
+ * (fp32 [bs,lq,heads], -inf = empty row). Positions are host int64 arrays. */
+int spattn_block_fwd(void* stream, int64_t bs, int heads, int kv_heads, int dim, const void* q,
+                     const int64_t* qpos, int64_t lq, const void* k, const void* v,
+                     const int64_t* kpos, int64_t lk, int causal, double scale, float* acc_out,
+                     float* acc_lse, int64_t* pairs);
+/* finalize_piece: bf16 out = acc_out (the accumulator is already normalised) */
+int spattn_block_finalize(void* stream, int64_t rows, int dim, const float* acc_out, void* out);
+/* merge_piece on finished pieces: acc <- LSE-merge(acc, piece) (fp32, warp per row) */
+int spattn_lse_merge(void* stream, float* acc_out, float* acc_lse, const float* out,
+                     const float* lse, int64_t rows, int dim);
+/* attn_block_backward: += into fp32 dq [bs,lq,heads,dim], dk/dv [bs,lk,kv_heads,dim] */
+int spattn_block_bwd(void* stream, int64_t bs, int heads, int kv_heads, int dim, const void* q,
+                     const int64_t* qpos, int64_t lq, const void* k, const void* v,
+                     const int64_t* kpos, int64_t lk, int causal, double scale, const void* out,
+                     const float* lse, const void* dout, float* dq, float* dk, float* dv,
+                     int64_t* pairs);
+/* shard_rows / gather_rows (partition.cpp:124-158) on device rows of row_bytes each,
+ * batched over bs: full [bs, L, row] <-> local [bs, L/sp, row] */
+int spattn_shard_rows(void* stream, const spattn_layout* layout, int index, int64_t bs,
+                      int64_t row_bytes, const void* full, void* local);
+int spattn_gather_rows(void* stream, const spattn_layout* layout, int index, int64_t bs,
+                       int64_t row_bytes, const void* local, void* full);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,376 @@
+// extern "C" boundary (include/spattn.h) over the seqpar:: C++ engines.
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "seqpar/attention.hpp"
+#include "spattn.h"
+#include "spattn_internal.h"
+
+struct spattn_ctx {
+  seqpar::RankCtx* rc = nullptr;
+  std::unique_ptr<seqpar::RankCtx> owned;
+  std::unique_ptr<seqpar::Transport> transport;
+  cudaStream_t own_stream = nullptr;
+};
+struct spattn_fabric {
+  std::unique_ptr<seqpar::LoopbackFabric> f;
+  std::vector<spattn_ctx> ctxs;
+};
+struct spattn_saved {
+  seqpar::SavedPtr s;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SPATTN_OK;
+  } catch (const seqpar::ConfigError& e) {
+    g_err = e.what();
+    return SPATTN_ERR_CONFIG;
+  } catch (const seqpar::ShapeError& e) {
+    g_err = e.what();
+    return SPATTN_ERR_SHAPE;
+  } catch (const seqpar::PeerAbort& e) {
+    g_err = e.what();
+    return SPATTN_ERR_PEER;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SPATTN_ERR_STATE;
+  } catch (...) {
+    g_err = "unknown error";
+    return SPATTN_ERR_STATE;
+  }
+}
+
+seqpar::ShardLayout make_layout(const spattn_layout* l) {
+  if (!l) throw seqpar::ConfigError("layout is null");
+  switch (l->mode) {
+    case SPATTN_NAIVE: return seqpar::ShardLayout::make_naive(l->global_len, l->sp);
+    case SPATTN_ZIGZAG: return seqpar::ShardLayout::make_zigzag(l->global_len, l->sp);
+    case SPATTN_SPLIT_USP: {
+      auto L = seqpar::ShardLayout::make_usp(l->global_len, l->u_degree, l->r_degree);
+      if (L.sp != l->sp) throw seqpar::ConfigError("usp layout: u*r != sp");
+      return L;
+    }
+  }
+  throw seqpar::ConfigError("unknown split mode " + std::to_string(l->mode));
+}
+
+seqpar::AttentionConfig make_cfg(const spattn_config* c) {
+  if (!c) throw seqpar::ConfigError("config is null");
+  seqpar::AttentionConfig a;
+  a.heads = c->heads;
+  a.kv_heads = c->kv_heads;
+  a.head_dim = c->head_dim;
+  a.causal = c->causal != 0;
+  a.ulysses_degree = c->ulysses_degree;
+  a.ring_degree = c->ring_degree;
+  if (a.heads <= 0 || a.head_dim <= 0 || a.kv_heads < 0) throw seqpar::ConfigError("invalid attention config");
+  return a;
+}
+
+seqpar::Engine make_engine(int e) {
+  if (e < SPATTN_ORACLE || e > SPATTN_USP) throw seqpar::ConfigError("unknown engine " + std::to_string(e));
+  return static_cast<seqpar::Engine>(e);
+}
+
+struct Views {
+  seqpar::DeviceTensor q, k, v, o;
+};
+Views views(const seqpar::AttentionConfig& c, const seqpar::ShardLayout& L, int64_t bs, const void* q,
+            const void* k, const void* v, const void* o) {
+  const int64_t n = L.local_len();
+  const int64_t kvh = c.kv_heads > 0 ? c.kv_heads : c.heads;
+  Views w;
+  w.q = {const_cast<void*>(q), bs, n, c.heads, c.head_dim};
+  w.k = {const_cast<void*>(k), bs, n, kvh, c.head_dim};
+  w.v = {const_cast<void*>(v), bs, n, kvh, c.head_dim};
+  w.o = {const_cast<void*>(o), bs, n, c.heads, c.head_dim};
+  if (bs <= 0) throw seqpar::ShapeError("batch size must be positive");
+  if (!q || !k || !v || !o) throw seqpar::ShapeError("null tensor pointer");
+  return w;
+}
+
+std::unique_ptr<seqpar::Documents> docs_of(const int64_t* d, int n) {
+  if (!d || n <= 0) return nullptr;
+  auto D = std::make_unique<seqpar::Documents>();
+  D->lengths.assign(d, d + n);
+  return D;
+}
+
+void row_moves(cudaStream_t s, const spattn_layout* layout, int index, int64_t bs, int64_t row_bytes,
+               const void* src, void* dst, bool shard) {
+  const auto L = make_layout(layout);
+  const auto runs = seqpar::position_runs(L.positions_of(index));
+  const int64_t lloc = L.local_len(), len = L.global_len;
+  std::vector<spattn::CopyTask> t;
+  for (int64_t b = 0; b < bs; ++b)
+    for (const auto& r : runs) {
+      if (shard)
+        t.push_back({src, dst, row_bytes, row_bytes, b * len + r.pos0, b * lloc + r.row0, 0, 0, r.n, row_bytes, 0});
+      else
+        t.push_back({src, dst, row_bytes, row_bytes, b * lloc + r.row0, b * len + r.pos0, 0, 0, r.n, row_bytes, 0});
+    }
+  for (size_t i = 0; i < t.size(); i += spattn::kMaxCopyTasks) {
+    spattn::CopyTaskSet ts{};
+    ts.n = static_cast<int>(std::min<size_t>(spattn::kMaxCopyTasks, t.size() - i));
+    for (int j = 0; j < ts.n; ++j) ts.t[j] = t[i + static_cast<size_t>(j)];
+    spattn::launch_copy_tasks(ts, 1, s);
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw seqpar::StateError(std::string("CUDA: ") + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spattn_last_error(void) { return g_err.c_str(); }
+int spattn_abi_version(void) { return 1; }
+
+int spattn_layout_positions(const spattn_layout* layout, int index, int64_t* out) {
+  return guard([&] {
+    const auto L = make_layout(layout);
+    const auto& p = L.positions_of(index);
+    std::memcpy(out, p.data(), p.size() * sizeof(int64_t));
+  });
+}
+int spattn_causal_pairs(const spattn_layout* layout, int index, int64_t* out) {
+  return guard([&] { *out = seqpar::causal_pair_count(make_layout(layout), index); });
+}
+int spattn_pad_length(int64_t len, int sp, int64_t cutoff, int pad_to_cutoff, int64_t* out) {
+  return guard([&] { *out = seqpar::pad_length(len, sp, cutoff, pad_to_cutoff != 0); });
+}
+int spattn_pick_xtuner_insp(int heads, int sp, int head_dim, int* out) {
+  return guard([&] { *out = seqpar::pick_xtuner_insp(heads, sp, head_dim); });
+}
+int spattn_reference_bytes(int engine, int64_t bs, int64_t len, int64_t heads, int64_t d, int sp,
+                           int u, int r, int64_t* out) {
+  return guard([&] {
+    switch (make_engine(engine)) {
+      case seqpar::Engine::oracle: *out = 0; break;
+      case seqpar::Engine::ulysses: *out = seqpar::ulysses_bytes(bs, len, heads, d, sp); break;
+      case seqpar::Engine::dummy_head: *out = seqpar::dummy_head_bytes(bs, len, heads, d, sp); break;
+      case seqpar::Engine::xtuner: *out = seqpar::xtuner_bytes(bs, len, heads, d, sp); break;
+      case seqpar::Engine::ring: *out = seqpar::ring_bytes(bs, len, heads, d, sp); break;
+      case seqpar::Engine::usp: *out = seqpar::usp_bytes(bs, len, heads, d, u, r); break;
+    }
+  });
+}
+
+int spattn_nccl_unique_id(uint8_t out[128]) {
+  return guard([&] { seqpar::nccl_unique_id(out); });
+}
+
+int spattn_ctx_create_nccl(int device, int rank, int world, int sp, const uint8_t uid[128],
+                           spattn_ctx** out) {
+  return guard([&] {
+    if (sp <= 0 || world % sp) throw seqpar::ConfigError("world must be a multiple of sp");
+    auto c = std::make_unique<spattn_ctx>();
+    c->transport = seqpar::make_nccl_transport(rank, world, uid, device);
+    c->owned = std::make_unique<seqpar::RankCtx>();
+    auto& rc = *c->owned;
+    rc.transport = c->transport.get();
+    rc.rank = rank;
+    rc.device = device;
+    for (int i = 0; i < sp; ++i) rc.sp_group.ranks.push_back(rank / sp * sp + i);
+    if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&rc.comm_stream, cudaStreamNonBlocking) != cudaSuccess)
+      throw seqpar::StateError("cannot create streams");
+    rc.stream = c->own_stream;
+    c->rc = &rc;
+    *out = c.release();
+  });
+}
+
+int spattn_ctx_destroy(spattn_ctx* c) {
+  return guard([&] {
+    if (!c) return;
+    if (c->owned) {
+      cudaStreamSynchronize(c->owned->stream);
+      if (c->own_stream) cudaStreamDestroy(c->own_stream);
+      if (c->owned->comm_stream) cudaStreamDestroy(c->owned->comm_stream);
+    }
+    delete c;
+  });
+}
+
+int spattn_fabric_create(int device, int world, int sp, int force_messages, spattn_fabric** out) {
+  return guard([&] {
+    auto f = std::make_unique<spattn_fabric>();
+    f->f = std::make_unique<seqpar::LoopbackFabric>(world, sp, device, force_messages != 0);
+    f->ctxs.resize(static_cast<size_t>(world));
+    for (int r = 0; r < world; ++r) {
+      f->ctxs[static_cast<size_t>(r)].rc = &f->f->ctx(r);
+      f->ctxs[static_cast<size_t>(r)].own_stream = f->f->ctx(r).stream;
+    }
+    *out = f.release();
+  });
+}
+int spattn_fabric_destroy(spattn_fabric* f) {
+  return guard([&] { delete f; });
+}
+int spattn_fabric_ctx(spattn_fabric* f, int rank, spattn_ctx** out) {
+  return guard([&] {
+    if (rank < 0 || rank >= static_cast<int>(f->ctxs.size())) throw seqpar::ConfigError("rank out of range");
+    *out = &f->ctxs[static_cast<size_t>(rank)];
+  });
+}
+
+int spattn_ctx_set_stream(spattn_ctx* c, void* stream) {
+  return guard([&] { c->rc->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream; });
+}
+int spattn_ctx_stream(spattn_ctx* c, void** stream) {
+  return guard([&] { *stream = c->rc->stream; });
+}
+int spattn_ctx_stats(spattn_ctx* c, int primitive, int64_t* calls, int64_t* bytes) {
+  return guard([&] {
+    if (primitive < 0 || primitive >= seqpar::kPrimitiveCount) throw seqpar::ConfigError("bad primitive");
+    *calls = c->rc->stats[static_cast<size_t>(primitive)].calls;
+    *bytes = c->rc->stats[static_cast<size_t>(primitive)].bytes;
+  });
+}
+int spattn_ctx_flops(spattn_ctx* c, int64_t* flops) {
+  return guard([&] { *flops = c->rc->flops; });
+}
+int spattn_ctx_reset_stats(spattn_ctx* c) {
+  return guard([&] { c->rc->reset_stats(); });
+}
+int spattn_set_kernel_family(int family) {
+  return guard([&] {
+    seqpar::set_kernel_family(family == 0 ? seqpar::KernelFamily::tcgen05 : seqpar::KernelFamily::mma);
+  });
+}
+int spattn_get_kernel_family(void) { return seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 ? 0 : 1; }
+
+int64_t spattn_launch_count(void) { return spattn::launch_count(); }
+int spattn_profile_enable(int on) {
+  return guard([&] { seqpar::profile_enable(on != 0); });
+}
+int spattn_profile_read(double ms[2], int64_t n[2]) {
+  return guard([&] { seqpar::profile_read(ms, n); });
+}
+
+int spattn_fwd(spattn_ctx* ctx, int engine, const spattn_config* cfg, const spattn_layout* layout,
+               int64_t bs, const void* q, const void* k, const void* v, void* out, float* lse,
+               const int64_t* doc_lens, int n_docs, spattn_saved** saved) {
+  return guard([&] {
+    const auto c = make_cfg(cfg);
+    const auto L = make_layout(layout);
+    const auto w = views(c, L, bs, q, k, v, out);
+    const auto D = docs_of(doc_lens, n_docs);
+    auto s = seqpar::run_attention_engine(*ctx->rc, make_engine(engine), c, L, w.q, w.k, w.v, w.o,
+                                          lse, D.get());
+    if (saved) {
+      *saved = new spattn_saved{std::move(s)};
+    }
+  });
+}
+
+int spattn_bwd(spattn_ctx* ctx, spattn_saved* saved, const void* dout, void* dq, void* dk, void* dv) {
+  return guard([&] {
+    if (!saved || !saved->s) throw seqpar::StateError("backward without a saved forward");
+    auto& S = *saved->s;
+    // views take the forward's shapes
+    seqpar::run_attention_engine_backward(*ctx->rc, S, seqpar::saved_view(S, 0, const_cast<void*>(dout)),
+                                          seqpar::saved_view(S, 0, dq), seqpar::saved_view(S, 1, dk),
+                                          seqpar::saved_view(S, 1, dv));
+  });
+}
+
+void spattn_saved_free(spattn_saved* s) { delete s; }
+
+int spattn_fabric_fwd(spattn_fabric* f, int engine, const spattn_config* cfg,
+                      const spattn_layout* layout, int64_t bs, const void* const* q,
+                      const void* const* k, const void* const* v, void* const* out,
+                      float* const* lse, const int64_t* doc_lens, int n_docs, spattn_saved** saved) {
+  return guard([&] {
+    const auto c = make_cfg(cfg);
+    const auto L = make_layout(layout);
+    const auto D = docs_of(doc_lens, n_docs);
+    const auto e = make_engine(engine);
+    std::vector<seqpar::SavedPtr> res(static_cast<size_t>(f->f->world_size()));
+    f->f->run([&](seqpar::RankCtx& rc) {
+      const size_t r = static_cast<size_t>(rc.rank);
+      const auto w = views(c, L, bs, q[r], k[r], v[r], out[r]);
+      res[r] = seqpar::run_attention_engine(rc, e, c, L, w.q, w.k, w.v, w.o, lse ? lse[r] : nullptr, D.get());
+    });
+    for (size_t r = 0; r < res.size(); ++r)
+      if (saved) saved[r] = new spattn_saved{std::move(res[r])};
+  });
+}
+
+int spattn_fabric_bwd(spattn_fabric* f, spattn_saved* const* saved, const void* const* dout,
+                      void* const* dq, void* const* dk, void* const* dv) {
+  return guard([&] {
+    f->f->run([&](seqpar::RankCtx& rc) {
+      const size_t r = static_cast<size_t>(rc.rank);
+      auto& S = *saved[r]->s;
+      seqpar::run_attention_engine_backward(rc, S, seqpar::saved_view(S, 0, const_cast<void*>(dout[r])),
+                                            seqpar::saved_view(S, 0, dq[r]), seqpar::saved_view(S, 1, dk[r]),
+                                            seqpar::saved_view(S, 1, dv[r]));
+    });
+  });
+}
+
+int spattn_fabric_all_to_all(spattn_fabric* f, const void* const* local, void* const* out,
+                             int64_t bs, int64_t len, int64_t heads, int64_t dim, int elem_bytes,
+                             int scatter_dim, int gather_dim) {
+  return guard([&] {
+    f->f->run([&](seqpar::RankCtx& rc) {
+      const size_t r = static_cast<size_t>(rc.rank);
+      seqpar::all_to_all(rc, rc.sp_group, local[r], bs, len, heads, dim, elem_bytes, scatter_dim,
+                         gather_dim, out[r]);
+    });
+  });
+}
+
+int spattn_block_fwd(void* stream, int64_t bs, int heads, int kv_heads, int dim, const void* q,
+                     const int64_t* qpos, int64_t lq, const void* k, const void* v,
+                     const int64_t* kpos, int64_t lk, int causal, double scale, float* acc_out,
+                     float* acc_lse, int64_t* pairs) {
+  return guard([&] {
+    std::vector<int64_t> qp(qpos, qpos + lq), kp(kpos, kpos + lk);
+    seqpar::block_forward_merge(static_cast<cudaStream_t>(stream), bs, heads, kv_heads, dim, q, qp,
+                                k, v, kp, causal != 0, scale, acc_out, acc_lse, pairs);
+  });
+}
+int spattn_block_finalize(void* stream, int64_t rows, int dim, const float* acc_out, void* out) {
+  return guard([&] { seqpar::block_finalize(static_cast<cudaStream_t>(stream), rows, dim, acc_out, out); });
+}
+int spattn_lse_merge(void* stream, float* acc_out, float* acc_lse, const float* out,
+                     const float* lse, int64_t rows, int dim) {
+  return guard([&] {
+    spattn::launch_lse_merge(acc_out, acc_lse, out, lse, rows, dim, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw seqpar::StateError(std::string("CUDA: ") + cudaGetErrorString(e));
+  });
+}
+int spattn_block_bwd(void* stream, int64_t bs, int heads, int kv_heads, int dim, const void* q,
+                     const int64_t* qpos, int64_t lq, const void* k, const void* v,
+                     const int64_t* kpos, int64_t lk, int causal, double scale, const void* out,
+                     const float* lse, const void* dout, float* dq, float* dk, float* dv,
+                     int64_t* pairs) {
+  return guard([&] {
+    std::vector<int64_t> qp(qpos, qpos + lq), kp(kpos, kpos + lk);
+    seqpar::block_backward(static_cast<cudaStream_t>(stream), bs, heads, kv_heads, dim, q, qp, k, v,
+                           kp, causal != 0, scale, out, lse, dout, dq, dk, dv, pairs);
+  });
+}
+int spattn_shard_rows(void* stream, const spattn_layout* layout, int index, int64_t bs,
+                      int64_t row_bytes, const void* full, void* local) {
+  return guard([&] { row_moves(static_cast<cudaStream_t>(stream), layout, index, bs, row_bytes, full, local, true); });
+}
+int spattn_gather_rows(void* stream, const spattn_layout* layout, int index, int64_t bs,
+                       int64_t row_bytes, const void* local, void* full) {
+  return guard([&] { row_moves(static_cast<cudaStream_t>(stream), layout, index, bs, row_bytes, local, full, false); });
+}
+
+}  // extern "C"

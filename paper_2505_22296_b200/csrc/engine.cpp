@@ -1,0 +1,1297 @@
+// SP attention engines on B200: Ulysses, Dummy-Head Ulysses, XTuner hidden-split (comparator),
+// zigzag Ring, USP, and the single-device oracle engine — per-rank programs over a Transport.
+//
+// Reference semantics (paths under /root/reference/proj/src):
+//   run_attention_engine  attention.cpp:526-574   (validation, dispatch)
+//   ulysses_core/engine   attention.cpp:391-410
+//   dummy_head_engine     attention.cpp:412-425   (pad heads to a multiple of sp, slice back)
+//   xtuner_engine         attention.cpp:427-464
+//   ring_attention/engine attention.cpp:262-352, :466-472
+//   usp_engine            attention.cpp:474-522
+// B200 design differences (results identical up to bf16/fp32 rounding):
+//   * GQA is never expanded (repeat_heads): each rank receives only the kv heads its query
+//     heads read (a "kv window") and the kernels index kv head h/rep.
+//   * Dummy heads are virtual: no zero head is sent or computed; a rank whose window is all
+//     padding simply has zero local heads.
+//   * all_to_all + pad/unpad + the layout permutation are one copy-task pass per direction
+//     (peer reads on a shared-memory transport; pack -> NCCL send/recv -> unpack otherwise).
+//   * Ulysses writes the gathered rows in natural position order, so the attention kernel sees
+//     contiguous causal runs for any layout.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "seqpar/attention.hpp"
+#include "spattn_internal.h"
+
+namespace seqpar {
+using spattn::AttnProblem;
+using spattn::CopyTask;
+using spattn::HeadMap;
+
+#define SP_CUDA(x)                                                                              \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      throw StateError(std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #x);            \
+  } while (0)
+
+namespace {
+KernelFamily g_family = KernelFamily::mma;
+}
+void set_kernel_family(KernelFamily f) { g_family = f; }
+KernelFamily kernel_family() { return g_family; }
+
+const char* engine_name(Engine e) {
+  static const char* n[] = {"oracle", "ulysses", "dummy_head", "xtuner", "ring", "usp"};
+  return n[static_cast<int>(e)];
+}
+Engine engine_from_string(const std::string& s) {  // attention.cpp:10-28
+  for (int i = 0; i < 6; ++i)
+    if (s == engine_name(static_cast<Engine>(i))) return static_cast<Engine>(i);
+  throw ConfigError("unknown engine '" + s + "'");
+}
+
+// ------------------------------------------------------------------------- device buffers
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t n, cudaStream_t st) : bytes(n), s(st) {
+    if (n) SP_CUDA(cudaMallocAsync(&p, n, st));
+  }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(bytes, o.bytes);
+    std::swap(s, o.s);
+    return *this;
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  void zero() {
+    if (bytes) SP_CUDA(cudaMemsetAsync(p, 0, bytes, s));
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+void check_launch() { SP_CUDA(cudaGetLastError()); }
+
+// --------------------------------------------------------------------------- problem lists
+int64_t admitted_pairs(const AttnProblem& p) {
+  if (!p.causal) return static_cast<int64_t>(p.nq) * p.nk;
+  // sum_{a=0}^{nq-1} clamp(a + off + 1, 0, nk)
+  int64_t total = 0;
+  const int64_t a0 = std::max<int64_t>(0, -static_cast<int64_t>(p.off));  // first a with >=1 key
+  const int64_t a_full = std::max<int64_t>(a0, static_cast<int64_t>(p.nk) - 1 - p.off);  // a + off + 1 >= nk
+  const int64_t a_mid_end = std::min<int64_t>(p.nq, a_full);
+  if (a_mid_end > a0) {
+    const int64_t lo = a0 + p.off + 1, hi = a_mid_end - 1 + p.off + 1;
+    total += (lo + hi) * (a_mid_end - a0) / 2;
+  }
+  if (p.nq > a_full) total += (p.nq - std::max(a_full, a0)) * static_cast<int64_t>(p.nk);
+  return total;
+}
+
+struct SubRun {
+  int64_t row0, pos0, n;
+  int64_t doc;
+};
+
+std::vector<SubRun> split_by_docs(const std::vector<PosRun>& runs, const Documents* docs) {
+  std::vector<SubRun> out;
+  if (!docs || docs->lengths.empty()) {
+    for (const auto& r : runs) out.push_back({r.row0, r.pos0, r.n, 0});
+    return out;
+  }
+  std::vector<int64_t> bounds{0};
+  for (int64_t l : docs->lengths) bounds.push_back(bounds.back() + l);
+  for (const auto& r : runs) {
+    int64_t p = r.pos0, row = r.row0;
+    const int64_t end = r.pos0 + r.n;
+    while (p < end) {
+      const auto it = std::upper_bound(bounds.begin(), bounds.end(), p);
+      const int64_t doc = (it - bounds.begin()) - 1;
+      const int64_t stop = std::min(end, it == bounds.end() ? end : *it);
+      out.push_back({row, p, stop - p, doc});
+      row += stop - p;
+      p = stop;
+    }
+  }
+  return out;
+}
+
+// Pairs every query run with every key run of the same document. A pair is skipped when no
+// key is admitted, marked full when every key is admitted, else causal with c <= a + off.
+// Consecutive key runs of one query run are fused when the earlier one is fully admitted
+// (zigzag ring steps and Ulysses both collapse to one problem per query run this way).
+std::vector<AttnProblem> make_problems(const std::vector<PosRun>& qruns,
+                                       const std::vector<PosRun>& kruns, bool causal, int64_t bs,
+                                       int64_t q_rows_b, int64_t k_rows_b, const Documents* docs,
+                                       int64_t* pairs) {
+  const auto qs = split_by_docs(qruns, docs), ks = split_by_docs(kruns, docs);
+  std::vector<AttnProblem> one;
+  for (const auto& Q : qs) {
+    std::vector<AttnProblem> row;
+    for (const auto& K : ks) {
+      if (K.doc != Q.doc) continue;
+      AttnProblem p{static_cast<int>(Q.row0), static_cast<int>(Q.n), static_cast<int>(K.row0),
+                    static_cast<int>(K.n), 0, 0};
+      if (causal) {
+        const int64_t off = Q.pos0 - K.pos0;
+        if (off + Q.n - 1 < 0) continue;
+        if (off < K.n - 1) {
+          p.causal = 1;
+          p.off = static_cast<int>(off);
+        }
+      }
+      row.push_back(p);
+    }
+    std::sort(row.begin(), row.end(),
+              [](const AttnProblem& a, const AttnProblem& b) { return a.k_row0 < b.k_row0; });
+    std::vector<AttnProblem> fused;
+    for (const auto& p : row) {
+      if (!fused.empty()) {
+        AttnProblem& f = fused.back();
+        const bool adjacent = f.k_row0 + f.nk == p.k_row0;
+        if (adjacent && !f.causal && (!p.causal || p.off >= -1)) {
+          const int shift = f.nk;
+          f.nk += p.nk;
+          if (p.causal) {
+            f.causal = 1;
+            f.off = p.off + shift;
+          }
+          continue;
+        }
+      }
+      fused.push_back(p);
+    }
+    one.insert(one.end(), fused.begin(), fused.end());
+  }
+  std::vector<AttnProblem> all;
+  int64_t total = 0;
+  for (int64_t b = 0; b < bs; ++b)
+    for (auto p : one) {
+      p.q_row0 += static_cast<int>(b * q_rows_b);
+      p.k_row0 += static_cast<int>(b * k_rows_b);
+      total += admitted_pairs(p);
+      all.push_back(p);
+    }
+  if (pairs) *pairs = total;
+  return all;
+}
+
+// Launch groups whose query rows are disjoint (each launch writes or merges a row once).
+std::vector<std::vector<AttnProblem>> q_disjoint_waves(const std::vector<AttnProblem>& probs) {
+  std::vector<std::vector<AttnProblem>> waves;
+  for (const auto& p : probs) {
+    bool placed = false;
+    for (auto& w : waves) {
+      if (static_cast<int>(w.size()) >= spattn::kMaxProblems) continue;
+      bool clash = false;
+      for (const auto& o : w)
+        clash |= !(p.q_row0 + p.nq <= o.q_row0 || o.q_row0 + o.nq <= p.q_row0);
+      if (!clash) {
+        w.push_back(p);
+        placed = true;
+        break;
+      }
+    }
+    if (!placed) waves.push_back({p});
+  }
+  return waves;
+}
+
+spattn::ProblemSet to_set(const std::vector<AttnProblem>& v, size_t from, size_t n) {
+  spattn::ProblemSet ps{};
+  ps.n = static_cast<int>(n);
+  for (size_t i = 0; i < n; ++i) ps.p[i] = v[from + i];
+  return ps;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------- attention drivers
+// Declared by the kernel translation units.
+}  // namespace seqpar
+namespace spattn {
+void launch_attn_fwd_mma(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s);
+void launch_attn_bwd_mma(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
+bool tc_fwd_supported(const FwdArgs& a);
+void launch_attn_fwd_tc(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s);
+bool tc_bwd_supported(const BwdArgs& a);
+void launch_attn_bwd_tc(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
+void launch_add_tasks_f32(const CopyTaskSet& ts, cudaStream_t s);
+
+void launch_attn_fwd(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
+  if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && tc_fwd_supported(a))
+    launch_attn_fwd_tc(a, ps, s);
+  else
+    launch_attn_fwd_mma(a, ps, s);
+}
+void launch_attn_bwd(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
+  if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && tc_bwd_supported(a))
+    launch_attn_bwd_tc(a, ps, s);
+  else
+    launch_attn_bwd_mma(a, ps, s);
+}
+}  // namespace spattn
+namespace seqpar {
+namespace {
+
+// Kernel timing for bench.py's roofline: CUDA events recorded on the launching stream around
+// every attention forward / backward launch group while profiling is on.
+struct KernelProfiler {
+  std::mutex mu;
+  bool on = false;
+  struct Rec {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+} g_prof;
+
+struct ProfScope {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  int kind;
+  ProfScope(cudaStream_t st, int k) : s(st), kind(k) {
+    if (!g_prof.on) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.recs.push_back({kind, a, b});
+  }
+};
+
+void require_dim(int d) {
+  if (d != 64 && d != 128) throw ConfigError("attention kernels support head_dim 64 or 128, got " + std::to_string(d));
+}
+
+// Plain (single wave) or merging (any number of waves) forward over a problem list.
+void attention_forward(cudaStream_t s, const spattn::FwdArgs& base,
+                       const std::vector<AttnProblem>& probs, bool merge) {
+  require_dim(base.d);
+  auto waves = q_disjoint_waves(probs);
+  if (!merge && waves.size() > 1) throw StateError("attention_forward: overlapping problems need merge mode");
+  ProfScope prof(s, 0);
+  for (const auto& w : waves) {
+    spattn::launch_attn_fwd(base, to_set(w, 0, w.size()), s);
+    check_launch();
+  }
+}
+
+void attention_backward(cudaStream_t s, const spattn::BwdArgs& base,
+                        const std::vector<AttnProblem>& probs) {
+  require_dim(base.d);
+  ProfScope prof(s, 1);
+  for (size_t i = 0; i < probs.size(); i += spattn::kMaxProblems) {
+    const size_t n = std::min<size_t>(spattn::kMaxProblems, probs.size() - i);
+    spattn::launch_attn_bwd(base, to_set(probs, i, n), s);
+    check_launch();
+  }
+}
+
+void run_tasks(const std::vector<CopyTask>& tasks, int elem, bool add, cudaStream_t s) {
+  for (size_t i = 0; i < tasks.size(); i += spattn::kMaxCopyTasks) {
+    spattn::CopyTaskSet ts{};
+    ts.n = static_cast<int>(std::min<size_t>(spattn::kMaxCopyTasks, tasks.size() - i));
+    for (int j = 0; j < ts.n; ++j) ts.t[j] = tasks[i + static_cast<size_t>(j)];
+    if (add)
+      spattn::launch_add_tasks_f32(ts, s);
+    else
+      spattn::launch_copy_tasks(ts, elem, s);
+    check_launch();
+  }
+}
+
+// ------------------------------------------------------------------ sequence <-> head moves
+// X_i: member i's sequence shard, rows [bs * lloc], row width xw elements.
+// Y_j: member j's head shard, rows [bs * lg], row width yw[j] elements.
+// Forward (scatter heads, gather sequence): Y_j[b*lg + dst(i, r)] cols [ycol_j, +n_j) <-
+//   X_i[b*lloc + r] cols [xcol_j, +n_j); then pad_j zero columns follow in Y_j.
+// Reverse: X_i[b*lloc + r] cols [xcol_j, +n_j) (+)= Y_j[b*lg + dst(i, r)] cols [ycol_j, +n_j).
+// dst(i, r) is given by runs[i] (row0 = local row, pos0 = destination row within a batch).
+struct Window {
+  int64_t xcol = 0, ycol = 0, n = 0, pad = 0;
+};
+struct MoveSpec {
+  int64_t bs = 1, lloc = 0, lg = 0;
+  int64_t xw = 0;
+  std::vector<int64_t> yw;
+  std::vector<Window> win;
+  std::vector<std::vector<PosRun>> runs;
+  int elem = 2;
+};
+
+void move_forward(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const void* x, void* y,
+                  cudaStream_t s) {
+  const int G = g.size(), me = g.index_of(ctx.rank);
+  int64_t sent = 0;
+  for (int j = 0; j < G; ++j)
+    if (j != me) sent += m.bs * m.lloc * m.win[static_cast<size_t>(j)].n * m.elem;
+  ctx.count(Primitive::all_to_all, sent);
+  const Window& w = m.win[static_cast<size_t>(me)];
+  const int64_t yw = m.yw[static_cast<size_t>(me)];
+  auto unpack = [&](int i, const void* src, int64_t src_stride, int64_t src_col0) {
+    std::vector<CopyTask> t;
+    for (int64_t b = 0; b < m.bs; ++b)
+      for (const auto& r : m.runs[static_cast<size_t>(i)])
+        t.push_back({src, y, src_stride, yw, b * m.lloc + r.row0, b * m.lg + r.pos0, src_col0,
+                     w.ycol, r.n, w.n, w.pad});
+    return t;
+  };
+  if (G == 1 || ctx.transport->peer_access()) {
+    std::vector<void*> ptrs{const_cast<void*>(x)};
+    if (G > 1) ptrs = ctx.transport->exchange_ptrs(g, ctx.rank, const_cast<void*>(x), s);
+    std::vector<CopyTask> tasks;
+    for (int i = 0; i < G; ++i) {
+      auto t = unpack(i, ptrs[static_cast<size_t>(i)], m.xw, w.xcol);
+      tasks.insert(tasks.end(), t.begin(), t.end());
+    }
+    run_tasks(tasks, m.elem, false, s);
+    if (G > 1) ctx.transport->release(g, ctx.rank, s);
+    return;
+  }
+  // message path: pack per destination -> grouped send/recv -> unpack per source
+  const int64_t rows = m.bs * m.lloc;
+  std::vector<int64_t> soff(G + 1, 0), roff(G + 1, 0);
+  for (int j = 0; j < G; ++j) soff[j + 1] = soff[j] + rows * m.win[static_cast<size_t>(j)].n;
+  for (int i = 0; i < G; ++i) roff[i + 1] = roff[i] + rows * w.n;
+  DevBuf sbuf(static_cast<size_t>(soff[G] * m.elem), s), rbuf(static_cast<size_t>(roff[G] * m.elem), s);
+  std::vector<CopyTask> pack;
+  for (int j = 0; j < G; ++j) {
+    const Window& wj = m.win[static_cast<size_t>(j)];
+    if (wj.n == 0) continue;
+    pack.push_back({x, static_cast<char*>(sbuf.p) + soff[j] * m.elem, m.xw, wj.n, 0, 0, wj.xcol, 0,
+                    rows, wj.n, 0});
+  }
+  run_tasks(pack, m.elem, false, s);
+  std::vector<Msg> sends, recvs;
+  for (int j = 0; j < G; ++j) {
+    sends.push_back({j, static_cast<char*>(sbuf.p) + soff[j] * m.elem,
+                     static_cast<size_t>((soff[j + 1] - soff[j]) * m.elem)});
+    recvs.push_back({j, static_cast<char*>(rbuf.p) + roff[j] * m.elem,
+                     static_cast<size_t>((roff[j + 1] - roff[j]) * m.elem)});
+  }
+  ctx.transport->send_recv(g, ctx.rank, sends, recvs, s);
+  std::vector<CopyTask> tasks;
+  for (int i = 0; i < G; ++i) {
+    if (w.n == 0 && w.pad == 0) continue;
+    auto t = unpack(i, static_cast<char*>(rbuf.p) + roff[i] * m.elem, w.n, 0);
+    tasks.insert(tasks.end(), t.begin(), t.end());
+  }
+  run_tasks(tasks, m.elem, false, s);
+}
+
+void move_reverse(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const void* y, void* x,
+                  bool add, cudaStream_t s) {
+  const int G = g.size(), me = g.index_of(ctx.rank);
+  const Window& wm = m.win[static_cast<size_t>(me)];
+  ctx.count(Primitive::all_to_all, (G - 1) * m.bs * m.lloc * wm.n * m.elem);
+  auto gather_from = [&](int j, const void* src, int64_t src_stride, int64_t src_col0,
+                         bool packed_rows) {
+    const Window& wj = m.win[static_cast<size_t>(j)];
+    std::vector<CopyTask> t;
+    if (wj.n == 0) return t;
+    if (packed_rows) {
+      t.push_back({src, x, src_stride, m.xw, 0, 0, src_col0, wj.xcol, m.bs * m.lloc, wj.n, 0});
+      return t;
+    }
+    for (int64_t b = 0; b < m.bs; ++b)
+      for (const auto& r : m.runs[static_cast<size_t>(me)])
+        t.push_back({src, x, src_stride, m.xw, b * m.lg + r.pos0, b * m.lloc + r.row0, src_col0,
+                     wj.xcol, r.n, wj.n, 0});
+    return t;
+  };
+  if (G == 1 || ctx.transport->peer_access()) {
+    std::vector<void*> ptrs{const_cast<void*>(y)};
+    if (G > 1) ptrs = ctx.transport->exchange_ptrs(g, ctx.rank, const_cast<void*>(y), s);
+    std::vector<CopyTask> tasks;
+    for (int j = 0; j < G; ++j) {
+      auto t = gather_from(j, ptrs[static_cast<size_t>(j)], m.yw[static_cast<size_t>(j)],
+                           m.win[static_cast<size_t>(j)].ycol, false);
+      tasks.insert(tasks.end(), t.begin(), t.end());
+    }
+    run_tasks(tasks, m.elem, add, s);
+    if (G > 1) ctx.transport->release(g, ctx.rank, s);
+    return;
+  }
+  // message path: member me packs, for every destination i, its rows of i in i's local order
+  const int64_t rows = m.bs * m.lloc;
+  DevBuf sbuf(static_cast<size_t>(G * rows * wm.n * m.elem), s);
+  std::vector<int64_t> roff(G + 1, 0);
+  for (int j = 0; j < G; ++j) roff[j + 1] = roff[j] + rows * m.win[static_cast<size_t>(j)].n;
+  DevBuf rbuf(static_cast<size_t>(roff[G] * m.elem), s);
+  std::vector<CopyTask> pack;
+  if (wm.n > 0)
+    for (int i = 0; i < G; ++i) {
+      char* dst = static_cast<char*>(sbuf.p) + i * rows * wm.n * m.elem;
+      for (int64_t b = 0; b < m.bs; ++b)
+        for (const auto& r : m.runs[static_cast<size_t>(i)])
+          pack.push_back({y, dst, m.yw[static_cast<size_t>(me)], wm.n, b * m.lg + r.pos0,
+                          b * m.lloc + r.row0, wm.ycol, 0, r.n, wm.n, 0});
+    }
+  run_tasks(pack, m.elem, false, s);
+  std::vector<Msg> sends, recvs;
+  for (int i = 0; i < G; ++i) {
+    sends.push_back({i, static_cast<char*>(sbuf.p) + i * rows * wm.n * m.elem,
+                     static_cast<size_t>(rows * wm.n * m.elem)});
+    recvs.push_back({i, static_cast<char*>(rbuf.p) + roff[i] * m.elem,
+                     static_cast<size_t>((roff[i + 1] - roff[i]) * m.elem)});
+  }
+  ctx.transport->send_recv(g, ctx.rank, sends, recvs, s);
+  std::vector<CopyTask> tasks;
+  for (int j = 0; j < G; ++j) {
+    auto t = gather_from(j, static_cast<char*>(rbuf.p) + roff[j] * m.elem,
+                         m.win[static_cast<size_t>(j)].n, 0, true);
+    tasks.insert(tasks.end(), t.begin(), t.end());
+  }
+  run_tasks(tasks, m.elem, add, s);
+}
+
+bool windows_overlap(const std::vector<Window>& w) {
+  for (size_t a = 0; a < w.size(); ++a)
+    for (size_t b = a + 1; b < w.size(); ++b)
+      if (w[a].n && w[b].n && w[a].xcol < w[b].xcol + w[b].n && w[b].xcol < w[a].xcol + w[a].n)
+        return true;
+  return false;
+}
+
+// ---------------------------------------------------------------- head windows (Ulysses)
+struct HeadPlan {
+  int G = 1;
+  int hp = 0;  // padded heads per member
+  std::vector<int> qlo, qn, kvlo, kvn;
+};
+
+HeadPlan plan_heads(int H, int Hkv, int G) {
+  HeadPlan p;
+  p.G = G;
+  p.hp = (H + G - 1) / G;
+  const int rep = H / Hkv;
+  for (int j = 0; j < G; ++j) {
+    const int lo = j * p.hp;
+    const int n = std::max(0, std::min(H, lo + p.hp) - lo);
+    p.qlo.push_back(lo);
+    p.qn.push_back(n);
+    const int klo = n ? lo / rep : 0;
+    p.kvlo.push_back(klo);
+    p.kvn.push_back(n ? (lo + n - 1) / rep + 1 - klo : 0);
+  }
+  return p;
+}
+
+MoveSpec head_move(const HeadPlan& hp, bool kv, int64_t bs, int64_t lloc, int64_t heads_x, int d,
+                   const std::vector<std::vector<PosRun>>& runs, int elem, int64_t unit = -1) {
+  // unit: columns per head (d for tensors, 1 for lse)
+  const int64_t u = unit < 0 ? d : unit;
+  MoveSpec m;
+  m.bs = bs;
+  m.lloc = lloc;
+  m.lg = lloc * hp.G;
+  m.xw = heads_x * u;
+  m.elem = elem;
+  m.runs = runs;
+  for (int j = 0; j < hp.G; ++j) {
+    const int lo = kv ? hp.kvlo[static_cast<size_t>(j)] : hp.qlo[static_cast<size_t>(j)];
+    const int n = kv ? hp.kvn[static_cast<size_t>(j)] : hp.qn[static_cast<size_t>(j)];
+    m.win.push_back({lo * u, 0, n * u, 0});
+    m.yw.push_back(n * u);
+  }
+  return m;
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------------- saved state
+struct SavedState {
+  Engine engine = Engine::oracle;
+  AttentionConfig cfg;
+  ShardLayout layout;
+  Documents docs;
+  bool has_docs = false;
+  int64_t bs = 0, lloc = 0;
+  cudaStream_t stream = nullptr;
+  // local (sequence-sharded) views captured at forward
+  DeviceTensor q, k, v, out;
+  // engine workspaces
+  std::vector<DevBuf> bufs;
+  // ulysses/usp inner: gathered tensors and plan
+  HeadPlan hplan;
+  int inner_G = 1;
+  std::vector<std::vector<PosRun>> inner_runs;
+  // ring: local q/k/v/out (either the user views or inner-gathered), lse
+  float* lse = nullptr;
+  const void* rq = nullptr;
+  const void* rk = nullptr;
+  const void* rv = nullptr;
+  const void* ro = nullptr;
+  int64_t rrows = 0;
+  HeadMap hm{};
+  int64_t q_stride = 0, kv_stride = 0;
+  std::vector<AttnProblem> plain_probs;  // single-block attention problems
+  // ring
+  bool ring = false;
+  CommGroup ring_group;
+  std::vector<std::vector<PosRun>> ring_runs;  // per ring member: local row -> position
+  // xtuner
+  int insp = 1;
+};
+
+void saved_state_free(SavedState* s) { delete s; }
+
+void profile_enable(bool on) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_prof.on = on;
+}
+
+void profile_read(double* ms, int64_t* n) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  ms[0] = ms[1] = 0;
+  n[0] = n[1] = 0;
+  for (auto& r : g_prof.recs) {
+    float t = 0;
+    SP_CUDA(cudaEventSynchronize(r.b));
+    SP_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.kind] += t;
+    n[r.kind] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.recs.clear();
+}
+
+DeviceTensor saved_view(const SavedState& s, int which, void* data) {
+  DeviceTensor t = which == 0 ? s.q : s.k;
+  t.data = data;
+  return t;
+}
+
+namespace {
+
+struct Local {
+  const void* q;
+  const void* k;
+  const void* v;
+  int64_t rows;  // bs * local rows
+  int64_t q_stride, kv_stride;
+  HeadMap hm;
+};
+
+// Single-block attention (oracle_attention, attention.cpp:218-260) on local rows.
+void plain_forward(RankCtx& ctx, const Local& L, int d, const std::vector<AttnProblem>& probs,
+                   void* out, float* lse) {
+  spattn::FwdArgs a{};
+  a.q = L.q;
+  a.k = L.k;
+  a.v = L.v;
+  a.o = out;
+  a.lse = lse;
+  a.acc_o = nullptr;
+  a.q_row_stride = L.q_stride;
+  a.kv_row_stride = L.kv_stride;
+  a.o_row_stride = L.q_stride;
+  a.lse_row_stride = L.hm.hq;
+  a.d = d;
+  a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+  a.hm = L.hm;
+  if (L.hm.hq == 0) return;
+  // rows no problem covers (empty attention) carry out=0, lse=-inf (finalize_piece, :151-165)
+  SP_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(L.rows * L.q_stride * 2), ctx.stream));
+  spattn::launch_fill_f32(lse, -INFINITY, L.rows * L.hm.hq, ctx.stream);
+  attention_forward(ctx.stream, a, probs, false);
+}
+
+void plain_backward(RankCtx& ctx, const Local& L, int d, const std::vector<AttnProblem>& probs,
+                    const void* out, const float* lse, const void* dout, float* dq, float* dk,
+                    float* dv) {
+  if (L.hm.hq == 0) return;
+  spattn::BwdArgs a{};
+  a.q = L.q;
+  a.k = L.k;
+  a.v = L.v;
+  a.o = out;
+  a.dout = dout;
+  a.lse = lse;
+  DevBuf delta(static_cast<size_t>(L.rows * L.hm.hq * 4), ctx.stream);
+  a.delta = delta.as<float>();
+  a.dq_acc = dq;
+  a.dk_acc = dk;
+  a.dv_acc = dv;
+  a.q_row_stride = L.q_stride;
+  a.kv_row_stride = L.kv_stride;
+  a.o_row_stride = L.q_stride;
+  a.dq_row_stride = L.q_stride;
+  a.dkv_row_stride = L.kv_stride;
+  a.lse_row_stride = L.hm.hq;
+  a.d = d;
+  a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+  a.hm = L.hm;
+  spattn::launch_attn_bwd_pre(a, static_cast<int>(L.rows), ctx.stream);
+  check_launch();
+  attention_backward(ctx.stream, a, probs);
+}
+
+// ------------------------------------------------------------------------ ring attention
+// ring_attention (attention.cpp:262-352): k|v circulate sp-1 times forward (rank i receives
+// from i-1), merged with the online softmax; backward circulates k|v|dk|dv sp times.
+// The rotation for step s+1 runs on the comm stream while step s computes.
+void ring_forward(RankCtx& ctx, const CommGroup& grp, const std::vector<std::vector<PosRun>>& runs,
+                  const Local& L, int d, bool causal, int64_t bs, int64_t lrows,
+                  const Documents* docs, void* out, float* lse) {
+  const int G = grp.size(), me = grp.index_of(ctx.rank);
+  const int64_t kv_elems = L.rows * L.kv_stride;
+  const size_t kvb = static_cast<size_t>(kv_elems * 2);
+  cudaStream_t s = ctx.stream, cs = ctx.comm_stream;
+  DevBuf acc(static_cast<size_t>(L.rows * L.q_stride * 4), s);
+  acc.zero();
+  spattn::launch_fill_f32(lse, -INFINITY, L.rows * L.hm.hq, s);
+  DevBuf buf[2] = {DevBuf(2 * kvb, s), DevBuf(2 * kvb, s)};
+  SP_CUDA(cudaMemcpyAsync(buf[0].p, L.k, kvb, cudaMemcpyDeviceToDevice, s));
+  SP_CUDA(cudaMemcpyAsync(static_cast<char*>(buf[0].p) + kvb, L.v, kvb, cudaMemcpyDeviceToDevice, s));
+  cudaEvent_t ev_main, ev_comm;
+  SP_CUDA(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
+  SP_CUDA(cudaEventCreateWithFlags(&ev_comm, cudaEventDisableTiming));
+  spattn::FwdArgs a{};
+  a.q = L.q;
+  a.o = nullptr;
+  a.acc_o = acc.as<float>();
+  a.lse = lse;
+  a.q_row_stride = L.q_stride;
+  a.kv_row_stride = L.kv_stride;
+  a.o_row_stride = L.q_stride;
+  a.lse_row_stride = L.hm.hq;
+  a.d = d;
+  a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+  a.hm = L.hm;
+  int64_t pairs_total = 0;
+  for (int step = 0; step < G; ++step) {
+    DevBuf& cur = buf[step & 1];
+    DevBuf& nxt = buf[(step + 1) & 1];
+    if (step + 1 < G) {
+      // comm stream: wait for cur to be complete and for nxt's previous readers (step-1)
+      SP_CUDA(cudaEventRecord(ev_main, s));
+      SP_CUDA(cudaStreamWaitEvent(cs, ev_main, 0));
+      ctx.count(Primitive::p2p, static_cast<int64_t>(2 * kvb));
+      const int next = (me + 1) % G, prev = (me - 1 + G) % G;
+      if (ctx.transport->peer_access()) {
+        auto ptrs = ctx.transport->exchange_ptrs(grp, ctx.rank, cur.p, cs);
+        SP_CUDA(cudaMemcpyAsync(nxt.p, ptrs[static_cast<size_t>(prev)], 2 * kvb,
+                                cudaMemcpyDeviceToDevice, cs));
+        ctx.transport->release(grp, ctx.rank, cs);
+      } else {
+        ctx.transport->send_recv(grp, ctx.rank, {{next, cur.p, 2 * kvb}}, {{prev, nxt.p, 2 * kvb}}, cs);
+      }
+      SP_CUDA(cudaEventRecord(ev_comm, cs));
+    }
+    const int owner = (me - step + G) % G;
+    int64_t pairs = 0;
+    auto probs = make_problems(runs[static_cast<size_t>(me)], runs[static_cast<size_t>(owner)],
+                               causal, bs, lrows, lrows, docs, &pairs);
+    pairs_total += pairs;
+    a.k = cur.p;
+    a.v = static_cast<char*>(cur.p) + kvb;
+    if (L.hm.hq > 0 && !probs.empty()) attention_forward(s, a, probs, true);
+    if (step + 1 < G) SP_CUDA(cudaStreamWaitEvent(s, ev_comm, 0));
+  }
+  ctx.add_flops(4 * d * pairs_total * L.hm.hq);
+  spattn::launch_f32_to_bf16(out, acc.as<float>(), 1.f, L.rows * L.q_stride, s);
+  check_launch();
+  SP_CUDA(cudaStreamWaitEvent(s, ev_comm, 0));
+  cudaEventDestroy(ev_main);
+  cudaEventDestroy(ev_comm);
+}
+
+void ring_backward(RankCtx& ctx, const CommGroup& grp, const std::vector<std::vector<PosRun>>& runs,
+                   const Local& L, int d, bool causal, int64_t bs, int64_t lrows,
+                   const Documents* docs, const void* out, const float* lse, const void* dout,
+                   float* dq, void* dk_bf16, void* dv_bf16, float* dk_f32, float* dv_f32) {
+  const int G = grp.size(), me = grp.index_of(ctx.rank);
+  const int64_t kv_elems = L.rows * L.kv_stride;
+  const size_t kvb = static_cast<size_t>(kv_elems * 2), gb = static_cast<size_t>(kv_elems * 4);
+  const size_t total = 2 * kvb + 2 * gb;
+  cudaStream_t s = ctx.stream;
+  DevBuf buf[2] = {DevBuf(total, s), DevBuf(total, s)};
+  SP_CUDA(cudaMemcpyAsync(buf[0].p, L.k, kvb, cudaMemcpyDeviceToDevice, s));
+  SP_CUDA(cudaMemcpyAsync(static_cast<char*>(buf[0].p) + kvb, L.v, kvb, cudaMemcpyDeviceToDevice, s));
+  SP_CUDA(cudaMemsetAsync(static_cast<char*>(buf[0].p) + 2 * kvb, 0, 2 * gb, s));
+  DevBuf delta(static_cast<size_t>(L.rows * L.hm.hq * 4), s);
+  spattn::BwdArgs a{};
+  a.q = L.q;
+  a.o = out;
+  a.dout = dout;
+  a.lse = lse;
+  a.delta = delta.as<float>();
+  a.dq_acc = dq;
+  a.q_row_stride = L.q_stride;
+  a.kv_row_stride = L.kv_stride;
+  a.o_row_stride = L.q_stride;
+  a.dq_row_stride = L.q_stride;
+  a.dkv_row_stride = L.kv_stride;
+  a.lse_row_stride = L.hm.hq;
+  a.d = d;
+  a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+  a.hm = L.hm;
+  if (L.hm.hq > 0) {
+    spattn::launch_attn_bwd_pre(a, static_cast<int>(L.rows), s);
+    check_launch();
+  }
+  int64_t pairs_total = 0;
+  for (int step = 0; step < G; ++step) {
+    DevBuf& cur = buf[step & 1];
+    DevBuf& nxt = buf[(step + 1) & 1];
+    const int owner = (me - step + G) % G;
+    int64_t pairs = 0;
+    auto probs = make_problems(runs[static_cast<size_t>(me)], runs[static_cast<size_t>(owner)],
+                               causal, bs, lrows, lrows, docs, &pairs);
+    pairs_total += pairs;
+    char* base = static_cast<char*>(cur.p);
+    a.k = base;
+    a.v = base + kvb;
+    a.dk_acc = reinterpret_cast<float*>(base + 2 * kvb);
+    a.dv_acc = reinterpret_cast<float*>(base + 2 * kvb + gb);
+    if (L.hm.hq > 0 && !probs.empty()) attention_backward(s, a, probs);
+    if (G > 1) {
+      ctx.count(Primitive::p2p, static_cast<int64_t>(total));
+      const int next = (me + 1) % G, prev = (me - 1 + G) % G;
+      if (ctx.transport->peer_access()) {
+        auto ptrs = ctx.transport->exchange_ptrs(grp, ctx.rank, cur.p, s);
+        SP_CUDA(cudaMemcpyAsync(nxt.p, ptrs[static_cast<size_t>(prev)], total,
+                                cudaMemcpyDeviceToDevice, s));
+        ctx.transport->release(grp, ctx.rank, s);
+      } else {
+        ctx.transport->send_recv(grp, ctx.rank, {{next, cur.p, total}}, {{prev, nxt.p, total}}, s);
+      }
+    }
+  }
+  ctx.add_flops(10 * d * pairs_total * L.hm.hq);
+  // after G shifts the block is home carrying every rank's dk/dv (attention.cpp:323-324)
+  const char* home = static_cast<const char*>(buf[G & 1].p);
+  if (G == 1) home = static_cast<const char*>(buf[0].p);
+  const float* hdk = reinterpret_cast<const float*>(home + 2 * kvb);
+  const float* hdv = reinterpret_cast<const float*>(home + 2 * kvb + gb);
+  if (dk_f32) {
+    SP_CUDA(cudaMemcpyAsync(dk_f32, hdk, gb, cudaMemcpyDeviceToDevice, s));
+    SP_CUDA(cudaMemcpyAsync(dv_f32, hdv, gb, cudaMemcpyDeviceToDevice, s));
+  } else {
+    spattn::launch_f32_to_bf16(dk_bf16, hdk, 1.f, kv_elems, s);
+    spattn::launch_f32_to_bf16(dv_bf16, hdv, 1.f, kv_elems, s);
+    check_launch();
+  }
+}
+
+void validate(RankCtx& ctx, const AttentionConfig& cfg, const ShardLayout& layout,
+              const DeviceTensor& q, const DeviceTensor& k, const DeviceTensor& v) {
+  // attention.cpp:529-549
+  const int kvh = cfg.kv_heads > 0 ? cfg.kv_heads : cfg.heads;
+  if (q.heads != cfg.heads || q.dim != cfg.head_dim)
+    throw ShapeError("attention: q shape disagrees with the config");
+  if (k.bs != q.bs || k.len != q.len || k.heads != kvh || k.dim != q.dim ||
+      v.bs != k.bs || v.len != k.len || v.heads != k.heads || v.dim != k.dim)
+    throw ShapeError("attention: kv shape disagrees with the config");
+  if (cfg.heads % kvh != 0)
+    throw ConfigError("attention: heads=" + std::to_string(cfg.heads) +
+                      " not a multiple of kv_heads=" + std::to_string(kvh));
+  if (layout.sp != ctx.sp_group.size())
+    throw ConfigError("attention: layout sp does not match the communicator size");
+  if (q.len != layout.local_len())
+    throw ShapeError("attention: local length " + std::to_string(q.len) +
+                     " does not match layout shard length " + std::to_string(layout.local_len()));
+  require_dim(cfg.head_dim);
+}
+
+std::vector<std::vector<PosRun>> runs_of(const ShardLayout& L, int from, int count) {
+  std::vector<std::vector<PosRun>> r;
+  for (int i = from; i < from + count; ++i) r.push_back(position_runs(L.positions_of(i)));
+  return r;
+}
+
+std::vector<PosRun> concat_runs(const ShardLayout& L, int from, int count) {
+  std::vector<int64_t> pos;
+  for (int i = from; i < from + count; ++i) {
+    const auto& o = L.positions_of(i);
+    pos.insert(pos.end(), o.begin(), o.end());
+  }
+  return position_runs(pos);
+}
+
+CommGroup subgroup(const CommGroup& parent, int from, int count, int stride) {
+  CommGroup g;
+  for (int t = 0; t < count; ++t) g.ranks.push_back(parent.ranks[static_cast<size_t>(from + t * stride)]);
+  return g;
+}
+
+}  // namespace
+
+// =============================================================================== forward
+SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig& cfg,
+                              const ShardLayout& layout, const DeviceTensor& q,
+                              const DeviceTensor& k, const DeviceTensor& v,
+                              const DeviceTensor& out, float* lse, const Documents* docs) {
+  validate(ctx, cfg, layout, q, k, v);
+  if (docs && !docs->lengths.empty()) {
+    int64_t t = 0;
+    for (int64_t l : docs->lengths) {
+      if (l <= 0) throw ConfigError("documents: lengths must be positive");
+      t += l;
+    }
+    if (t != layout.global_len) throw ConfigError("documents: lengths must sum to the sequence length");
+  }
+  SavedPtr S(new SavedState);
+  S->engine = engine;
+  S->cfg = cfg;
+  S->layout = layout;
+  S->has_docs = docs && !docs->lengths.empty();
+  if (S->has_docs) S->docs = *docs;
+  const Documents* D = S->has_docs ? &S->docs : nullptr;
+  S->bs = q.bs;
+  S->lloc = q.len;
+  S->stream = ctx.stream;
+  S->q = q;
+  S->k = k;
+  S->v = v;
+  S->out = out;
+  const int H = cfg.heads, Hkv = cfg.kv_heads > 0 ? cfg.kv_heads : cfg.heads, d = cfg.head_dim;
+  const int rep = H / Hkv;
+  const int G = layout.sp;
+  const int me = ctx.sp_group.index_of(ctx.rank);
+  const int64_t bs = q.bs, lloc = q.len, L = layout.global_len;
+  cudaStream_t s = ctx.stream;
+  auto keep = [&](size_t bytes) -> void* {
+    S->bufs.emplace_back(bytes, s);
+    return S->bufs.back().p;
+  };
+
+  switch (engine) {
+    case Engine::oracle: {
+      if (G != 1) throw ConfigError("oracle engine runs only at sp=1");
+      break;
+    }
+    case Engine::ulysses:
+      if (H % G != 0)
+        throw ConfigError("ulysses: heads=" + std::to_string(H) + " not divisible by sp=" +
+                          std::to_string(G) + "; use dummy_head or xtuner");
+      break;
+    case Engine::ring:
+      if (layout.mode != SplitMode::zigzag) throw ConfigError("ring engine requires the zigzag layout");
+      break;
+    case Engine::usp: {
+      const int u = cfg.ulysses_degree, r = cfg.ring_degree;
+      if (u <= 0 || r <= 0) throw ConfigError("usp: ulysses_degree and ring_degree must be positive");
+      if (u * r != G)
+        throw ConfigError("usp: ulysses_degree " + std::to_string(u) + " * ring_degree " +
+                          std::to_string(r) + " != sp " + std::to_string(G));
+      if (layout.mode != SplitMode::usp || layout.u_degree != u || layout.r_degree != r)
+        throw ConfigError("usp: layout was not built for these degrees");
+      break;
+    }
+    case Engine::xtuner:
+    case Engine::dummy_head:
+      break;
+  }
+  float* lse_local = lse;
+  if (!lse_local) lse_local = static_cast<float*>(keep(static_cast<size_t>(bs * lloc * H * 4)));
+  S->lse = lse_local;
+
+  if (engine == Engine::oracle || (engine != Engine::usp && engine != Engine::xtuner &&
+                                   engine != Engine::ring && G == 1)) {
+    // single device: one block over the full sequence (attention.cpp:559-561)
+    Local Lc{q.data, k.data, v.data, bs * lloc, H * d, Hkv * d, {H, Hkv, 0, 0, rep}};
+    auto runs = concat_runs(layout, 0, G);
+    int64_t pairs = 0;
+    S->plain_probs = make_problems(runs, runs, cfg.causal, bs, lloc, lloc, D, &pairs);
+    ctx.add_flops(4 * d * pairs * H);
+    plain_forward(ctx, Lc, d, S->plain_probs, out.data, lse_local);
+    S->rq = q.data, S->rk = k.data, S->rv = v.data, S->ro = out.data;
+    S->rrows = bs * lloc;
+    S->hm = Lc.hm;
+    S->q_stride = H * d, S->kv_stride = Hkv * d;
+    S->engine = Engine::oracle;
+    return S;
+  }
+
+  if (engine == Engine::ring) {
+    Local Lc{q.data, k.data, v.data, bs * lloc, H * d, Hkv * d, {H, Hkv, 0, 0, rep}};
+    S->ring = true;
+    S->ring_group = ctx.sp_group;
+    S->ring_runs = runs_of(layout, 0, G);
+    ring_forward(ctx, ctx.sp_group, S->ring_runs, Lc, d, cfg.causal, bs, lloc, D, out.data, lse_local);
+    S->rq = q.data, S->rk = k.data, S->rv = v.data, S->ro = out.data;
+    S->rrows = bs * lloc;
+    S->hm = Lc.hm;
+    S->q_stride = H * d, S->kv_stride = Hkv * d;
+    return S;
+  }
+
+  if (engine == Engine::xtuner) {
+    // attention.cpp:427-464 — virtual heads of d/insp, a2a, all-gather of insp fragments into
+    // hv_local full heads per rank, attention replicated insp times, virtual slice back.
+    const int insp = pick_xtuner_insp(H, G, d);
+    const int hv_local = H * insp / G;
+    const int grp = me / insp;
+    S->insp = insp;
+    const int64_t lg = lloc * G;
+    auto runs = runs_of(layout, 0, G);
+    auto gather_spec = [&](bool kv, int elem, int64_t unit) {
+      MoveSpec m;
+      m.bs = bs, m.lloc = lloc, m.lg = lg, m.elem = elem, m.runs = runs;
+      m.xw = (kv ? Hkv : H) * unit;
+      for (int j = 0; j < G; ++j) {
+        const int g = j / insp;
+        int lo = g * hv_local, n = hv_local;
+        if (kv) {
+          const int klo = lo / rep;
+          n = (lo + n - 1) / rep + 1 - klo;
+          lo = klo;
+        }
+        m.win.push_back({lo * unit, 0, n * unit, 0});
+        m.yw.push_back(n * unit);
+      }
+      return m;
+    };
+    MoveSpec mq = gather_spec(false, 2, d), mkv = gather_spec(true, 2, d);
+    const int nkv = static_cast<int>(mkv.yw[static_cast<size_t>(me)] / d);
+    void* qg = keep(static_cast<size_t>(bs * lg * hv_local * d * 2));
+    void* kg = keep(static_cast<size_t>(bs * lg * nkv * d * 2));
+    void* vg = keep(static_cast<size_t>(bs * lg * nkv * d * 2));
+    void* og = keep(static_cast<size_t>(bs * lg * hv_local * d * 2));
+    float* lg_lse = static_cast<float*>(keep(static_cast<size_t>(bs * lg * hv_local * 4)));
+    move_forward(ctx, ctx.sp_group, mq, q.data, qg, s);
+    move_forward(ctx, ctx.sp_group, mkv, k.data, kg, s);
+    move_forward(ctx, ctx.sp_group, mkv, v.data, vg, s);
+    Local Lc{qg, kg, vg, bs * lg, hv_local * d, nkv * d,
+             {hv_local, nkv, grp * hv_local, static_cast<int>(mkv.win[static_cast<size_t>(me)].xcol / d), rep}};
+    const std::vector<PosRun> full{{0, 0, lg}};
+    int64_t pairs = 0;
+    S->plain_probs = make_problems(full, full, cfg.causal, bs, lg, lg, D, &pairs);
+    ctx.add_flops(4 * d * pairs * hv_local);
+    plain_forward(ctx, Lc, d, S->plain_probs, og, lg_lse);
+    // virtual slice of this member -> out (contiguous columns of the group's head block)
+    MoveSpec mo;
+    mo.bs = bs, mo.lloc = lloc, mo.lg = lg, mo.elem = 2, mo.runs = runs, mo.xw = H * d;
+    MoveSpec ml = mo;
+    ml.elem = 4, ml.xw = H;
+    const int64_t frag = static_cast<int64_t>(hv_local) * d / insp;
+    for (int j = 0; j < G; ++j) {
+      const int g = j / insp, f = j - g * insp;
+      mo.win.push_back({g * hv_local * d + f * frag, f * frag, frag, 0});
+      mo.yw.push_back(hv_local * d);
+      ml.win.push_back({g * hv_local, 0, f == 0 ? hv_local : 0, 0});
+      ml.yw.push_back(hv_local);
+    }
+    move_reverse(ctx, ctx.sp_group, mo, og, out.data, false, s);
+    move_reverse(ctx, ctx.sp_group, ml, lg_lse, lse_local, false, s);
+    S->rq = qg, S->rk = kg, S->rv = vg, S->ro = og;
+    S->lse = lg_lse;
+    S->rrows = bs * lg;
+    S->hm = Lc.hm;
+    S->q_stride = hv_local * d, S->kv_stride = nkv * d;
+    return S;
+  }
+
+  // ---- ulysses / dummy_head (all G members) and usp (inner u members, then ring over r)
+  int u = G, r = 1, inner_from = 0, rho = 0, iota = me;
+  if (engine == Engine::usp) {
+    u = cfg.ulysses_degree, r = cfg.ring_degree;
+    rho = me / u, iota = me % u;
+    inner_from = rho * u;
+  }
+  const CommGroup inner = subgroup(ctx.sp_group, inner_from, u, 1);
+  HeadPlan hp = plan_heads(H, Hkv, u);
+  S->hplan = hp;
+  S->inner_G = u;
+  const int64_t lg = lloc * u;
+  // destination rows: natural positions for ulysses/dummy (rows == positions); source order
+  // for usp (rows follow the ring layout's positions, attention.cpp:370-378)
+  std::vector<std::vector<PosRun>> runs;
+  if (engine == Engine::usp) {
+    for (int t = 0; t < u; ++t) runs.push_back({{0, t * lloc, lloc}});
+  } else {
+    runs = runs_of(layout, 0, G);
+  }
+  S->inner_runs = runs;
+  const int nq = hp.qn[static_cast<size_t>(iota)], nkv = hp.kvn[static_cast<size_t>(iota)];
+  MoveSpec mq = head_move(hp, false, bs, lloc, H, d, runs, 2);
+  MoveSpec mkv = head_move(hp, true, bs, lloc, Hkv, d, runs, 2);
+  void* qg = keep(static_cast<size_t>(bs * lg * nq * d * 2));
+  void* kg = keep(static_cast<size_t>(bs * lg * nkv * d * 2));
+  void* vg = keep(static_cast<size_t>(bs * lg * nkv * d * 2));
+  void* og = keep(static_cast<size_t>(bs * lg * nq * d * 2));
+  float* glse = static_cast<float*>(keep(static_cast<size_t>(bs * lg * nq * 4)));
+  move_forward(ctx, inner, mq, q.data, qg, s);
+  move_forward(ctx, inner, mkv, k.data, kg, s);
+  move_forward(ctx, inner, mkv, v.data, vg, s);
+  Local Lc{qg, kg, vg, bs * lg, nq * d, nkv * d,
+           {nq, nkv, hp.qlo[static_cast<size_t>(iota)], hp.kvlo[static_cast<size_t>(iota)], rep}};
+  if (engine == Engine::usp && r > 1) {
+    const CommGroup outer = subgroup(ctx.sp_group, iota, r, u);
+    const ShardLayout ring_layout = ShardLayout::make_zigzag(L, r);
+    S->ring = true;
+    S->ring_group = outer;
+    S->ring_runs = runs_of(ring_layout, 0, r);
+    ring_forward(ctx, outer, S->ring_runs, Lc, d, cfg.causal, bs, lg, D, og, glse);
+  } else {
+    const auto pr = engine == Engine::usp ? concat_runs(layout, rho * u, u)
+                                          : std::vector<PosRun>{{0, 0, lg}};
+    int64_t pairs = 0;
+    S->plain_probs = make_problems(pr, pr, cfg.causal, bs, lg, lg, D, &pairs);
+    ctx.add_flops(4 * d * pairs * nq);
+    plain_forward(ctx, Lc, d, S->plain_probs, og, glse);
+  }
+  move_reverse(ctx, inner, mq, og, out.data, false, s);
+  MoveSpec ml = head_move(hp, false, bs, lloc, H, d, runs, 4, 1);
+  move_reverse(ctx, inner, ml, glse, lse_local, false, s);
+  S->rq = qg, S->rk = kg, S->rv = vg, S->ro = og;
+  S->lse = glse;
+  S->rrows = bs * lg;
+  S->hm = Lc.hm;
+  S->q_stride = nq * d, S->kv_stride = nkv * d;
+  return S;
+}
+
+// ============================================================================== backward
+void run_attention_engine_backward(RankCtx& ctx, SavedState& S, const DeviceTensor& dout,
+                                   const DeviceTensor& dq, const DeviceTensor& dk,
+                                   const DeviceTensor& dv) {
+  const AttentionConfig& cfg = S.cfg;
+  const int H = cfg.heads, Hkv = cfg.kv_heads > 0 ? cfg.kv_heads : cfg.heads, d = cfg.head_dim;
+  const int G = S.layout.sp;
+  const int me = ctx.sp_group.index_of(ctx.rank);
+  const int64_t bs = S.bs, lloc = S.lloc;
+  const Documents* D = S.has_docs ? &S.docs : nullptr;
+  cudaStream_t s = ctx.stream;
+  if (dout.bs != bs || dout.len != lloc || dout.heads != H || dout.dim != d)
+    throw ShapeError("backward: dout shape disagrees with the forward output");
+  Local Lc{S.rq, S.rk, S.rv, S.rrows, S.q_stride, S.kv_stride, S.hm};
+
+  if (S.engine == Engine::oracle || (S.engine == Engine::ring)) {
+    const int64_t rows = bs * lloc;
+    DevBuf dqa(static_cast<size_t>(rows * H * d * 4), s);
+    dqa.zero();
+    if (S.engine == Engine::oracle) {
+      DevBuf dka(static_cast<size_t>(rows * Hkv * d * 4), s), dva(static_cast<size_t>(rows * Hkv * d * 4), s);
+      dka.zero();
+      dva.zero();
+      int64_t pairs = 0;
+      for (const auto& p : S.plain_probs) pairs += admitted_pairs(p);
+      ctx.add_flops(10 * d * pairs * H);
+      plain_backward(ctx, Lc, d, S.plain_probs, S.ro, S.lse, dout.data, dqa.as<float>(),
+                     dka.as<float>(), dva.as<float>());
+      spattn::launch_f32_to_bf16(dk.data, dka.as<float>(), 1.f, rows * Hkv * d, s);
+      spattn::launch_f32_to_bf16(dv.data, dva.as<float>(), 1.f, rows * Hkv * d, s);
+    } else {
+      ring_backward(ctx, S.ring_group, S.ring_runs, Lc, d, cfg.causal, bs, lloc, D, S.ro, S.lse,
+                    dout.data, dqa.as<float>(), dk.data, dv.data, nullptr, nullptr);
+    }
+    spattn::launch_f32_to_bf16(dq.data, dqa.as<float>(), 1.f, rows * H * d, s);
+    check_launch();
+    return;
+  }
+
+  if (S.engine == Engine::xtuner) {
+    const int insp = S.insp, hv_local = H * insp / G, grp = me / insp;
+    const int rep = H / Hkv;
+    const int64_t lg = lloc * G;
+    auto runs = runs_of(S.layout, 0, G);
+    // full group dout (all fragments of the group's heads): same pattern as the q gather
+    MoveSpec mq;
+    mq.bs = bs, mq.lloc = lloc, mq.lg = lg, mq.elem = 2, mq.runs = runs, mq.xw = H * d;
+    for (int j = 0; j < G; ++j) {
+      mq.win.push_back({(j / insp) * hv_local * d, 0, static_cast<int64_t>(hv_local) * d, 0});
+      mq.yw.push_back(hv_local * d);
+    }
+    const int nkv = S.hm.hkv;
+    DevBuf dog(static_cast<size_t>(bs * lg * hv_local * d * 2), s);
+    move_forward(ctx, ctx.sp_group, mq, dout.data, dog.p, s);
+    DevBuf dqa(static_cast<size_t>(bs * lg * hv_local * d * 4), s), dka(static_cast<size_t>(bs * lg * nkv * d * 4), s),
+        dva(static_cast<size_t>(bs * lg * nkv * d * 4), s);
+    dqa.zero(), dka.zero(), dva.zero();
+    int64_t pairs = 0;
+    for (const auto& p : S.plain_probs) pairs += admitted_pairs(p);
+    ctx.add_flops(10 * d * pairs * hv_local);
+    plain_backward(ctx, Lc, d, S.plain_probs, S.ro, S.lse, dog.p, dqa.as<float>(), dka.as<float>(),
+                   dva.as<float>());
+    DevBuf dqg(static_cast<size_t>(bs * lg * hv_local * d * 2), s);
+    spattn::launch_f32_to_bf16(dqg.p, dqa.as<float>(), 1.f, bs * lg * hv_local * d, s);
+    MoveSpec mo;
+    mo.bs = bs, mo.lloc = lloc, mo.lg = lg, mo.elem = 2, mo.runs = runs, mo.xw = H * d;
+    const int64_t frag = static_cast<int64_t>(hv_local) * d / insp;
+    for (int j = 0; j < G; ++j) {
+      const int g = j / insp, f = j - g * insp;
+      mo.win.push_back({g * hv_local * d + f * frag, f * frag, frag, 0});
+      mo.yw.push_back(hv_local * d);
+    }
+    move_reverse(ctx, ctx.sp_group, mo, dqg.p, dq.data, false, s);
+    // kv grads: member j returns fragment f of its group's kv block; groups sharing a kv head
+    // add up (the repeat_heads backward sum, tensor.cpp:437-447)
+    MoveSpec mk;
+    mk.bs = bs, mk.lloc = lloc, mk.lg = lg, mk.elem = 4, mk.runs = runs, mk.xw = Hkv * d;
+    for (int j = 0; j < G; ++j) {
+      const int g = j / insp, f = j - g * insp;
+      const int lo = g * hv_local, klo = lo / rep, kn = (lo + hv_local - 1) / rep + 1 - klo;
+      const int64_t kfrag = static_cast<int64_t>(kn) * d / insp;
+      mk.win.push_back({klo * d + f * kfrag, f * kfrag, kfrag, 0});
+      mk.yw.push_back(kn * d);
+    }
+    (void)grp;
+    const int64_t rows = bs * lloc;
+    DevBuf dkf(static_cast<size_t>(rows * Hkv * d * 4), s), dvf(static_cast<size_t>(rows * Hkv * d * 4), s);
+    dkf.zero(), dvf.zero();
+    move_reverse(ctx, ctx.sp_group, mk, dka.p, dkf.p, true, s);
+    move_reverse(ctx, ctx.sp_group, mk, dva.p, dvf.p, true, s);
+    spattn::launch_f32_to_bf16(dk.data, dkf.as<float>(), 1.f, rows * Hkv * d, s);
+    spattn::launch_f32_to_bf16(dv.data, dvf.as<float>(), 1.f, rows * Hkv * d, s);
+    check_launch();
+    return;
+  }
+
+  // ---- ulysses / dummy_head / usp
+  const HeadPlan& hp = S.hplan;
+  const int u = S.inner_G;
+  const int inner_from = S.engine == Engine::usp ? (me / u) * u : 0;
+  const int iota = S.engine == Engine::usp ? me % u : me;
+  const CommGroup inner = subgroup(ctx.sp_group, inner_from, u, 1);
+  const int64_t lg = lloc * u;
+  const int nq = hp.qn[static_cast<size_t>(iota)], nkv = hp.kvn[static_cast<size_t>(iota)];
+  MoveSpec mq = head_move(hp, false, bs, lloc, H, d, S.inner_runs, 2);
+  DevBuf dog(static_cast<size_t>(bs * lg * nq * d * 2), s);
+  move_forward(ctx, inner, mq, dout.data, dog.p, s);
+  DevBuf dqa(static_cast<size_t>(bs * lg * nq * d * 4), s), dka(static_cast<size_t>(bs * lg * nkv * d * 4), s),
+      dva(static_cast<size_t>(bs * lg * nkv * d * 4), s);
+  dqa.zero(), dka.zero(), dva.zero();
+  if (S.ring) {
+    ring_backward(ctx, S.ring_group, S.ring_runs, Lc, d, cfg.causal, bs, lg, D, S.ro, S.lse, dog.p,
+                  dqa.as<float>(), nullptr, nullptr, dka.as<float>(), dva.as<float>());
+  } else {
+    int64_t pairs = 0;
+    for (const auto& p : S.plain_probs) pairs += admitted_pairs(p);
+    ctx.add_flops(10 * d * pairs * nq);
+    plain_backward(ctx, Lc, d, S.plain_probs, S.ro, S.lse, dog.p, dqa.as<float>(), dka.as<float>(),
+                   dva.as<float>());
+  }
+  DevBuf dqg(static_cast<size_t>(bs * lg * nq * d * 2), s);
+  spattn::launch_f32_to_bf16(dqg.p, dqa.as<float>(), 1.f, bs * lg * nq * d, s);
+  move_reverse(ctx, inner, mq, dqg.p, dq.data, false, s);
+  MoveSpec mkv = head_move(hp, true, bs, lloc, Hkv, d, S.inner_runs, 2);
+  const int64_t rows = bs * lloc;
+  if (!windows_overlap(mkv.win)) {
+    DevBuf dkg(static_cast<size_t>(bs * lg * nkv * d * 2), s), dvg(static_cast<size_t>(bs * lg * nkv * d * 2), s);
+    spattn::launch_f32_to_bf16(dkg.p, dka.as<float>(), 1.f, bs * lg * nkv * d, s);
+    spattn::launch_f32_to_bf16(dvg.p, dva.as<float>(), 1.f, bs * lg * nkv * d, s);
+    move_reverse(ctx, inner, mkv, dkg.p, dk.data, false, s);
+    move_reverse(ctx, inner, mkv, dvg.p, dv.data, false, s);
+  } else {
+    // kv heads shared by members (Hkv % u != 0): sum fp32 partials (repeat_heads backward)
+    MoveSpec mk4 = head_move(hp, true, bs, lloc, Hkv, d, S.inner_runs, 4);
+    DevBuf dkf(static_cast<size_t>(rows * Hkv * d * 4), s), dvf(static_cast<size_t>(rows * Hkv * d * 4), s);
+    dkf.zero(), dvf.zero();
+    move_reverse(ctx, inner, mk4, dka.p, dkf.p, true, s);
+    move_reverse(ctx, inner, mk4, dva.p, dvf.p, true, s);
+    spattn::launch_f32_to_bf16(dk.data, dkf.as<float>(), 1.f, rows * Hkv * d, s);
+    spattn::launch_f32_to_bf16(dv.data, dvf.as<float>(), 1.f, rows * Hkv * d, s);
+  }
+  check_launch();
+}
+
+// ========================================================================= kernel-level API
+void block_forward_merge(cudaStream_t s, int64_t bs, int heads, int kv_heads, int dim,
+                         const void* q, const std::vector<int64_t>& qpos, const void* k,
+                         const void* v, const std::vector<int64_t>& kpos, bool causal,
+                         double scale, float* acc_out, float* acc_lse, int64_t* pairs) {
+  if (heads % kv_heads) throw ConfigError("block_forward: heads not a multiple of kv_heads");
+  const int64_t lq = static_cast<int64_t>(qpos.size()), lk = static_cast<int64_t>(kpos.size());
+  auto probs = make_problems(position_runs(qpos), position_runs(kpos), causal, bs, lq, lk, nullptr, pairs);
+  if (pairs) *pairs *= heads;
+  spattn::FwdArgs a{};
+  a.q = q, a.k = k, a.v = v, a.o = nullptr, a.acc_o = acc_out, a.lse = acc_lse;
+  a.q_row_stride = static_cast<int64_t>(heads) * dim;
+  a.kv_row_stride = static_cast<int64_t>(kv_heads) * dim;
+  a.o_row_stride = a.q_row_stride;
+  a.lse_row_stride = heads;
+  a.d = dim;
+  a.scale = static_cast<float>(scale);
+  a.hm = {heads, kv_heads, 0, 0, heads / kv_heads};
+  if (!probs.empty()) attention_forward(s, a, probs, true);
+}
+
+void block_finalize(cudaStream_t s, int64_t rows, int dim, const float* acc_out, void* out_bf16) {
+  spattn::launch_f32_to_bf16(out_bf16, acc_out, 1.f, rows * dim, s);
+  check_launch();
+}
+
+void block_backward(cudaStream_t s, int64_t bs, int heads, int kv_heads, int dim, const void* q,
+                    const std::vector<int64_t>& qpos, const void* k, const void* v,
+                    const std::vector<int64_t>& kpos, bool causal, double scale, const void* out,
+                    const float* lse, const void* dout, float* dq, float* dk, float* dv,
+                    int64_t* pairs) {
+  if (heads % kv_heads) throw ConfigError("block_backward: heads not a multiple of kv_heads");
+  const int64_t lq = static_cast<int64_t>(qpos.size()), lk = static_cast<int64_t>(kpos.size());
+  auto probs = make_problems(position_runs(qpos), position_runs(kpos), causal, bs, lq, lk, nullptr, pairs);
+  if (pairs) *pairs *= heads;
+  spattn::BwdArgs a{};
+  DevBuf delta(static_cast<size_t>(bs * lq * heads * 4), s);
+  a.q = q, a.k = k, a.v = v, a.o = out, a.dout = dout, a.lse = lse, a.delta = delta.as<float>();
+  a.dq_acc = dq, a.dk_acc = dk, a.dv_acc = dv;
+  a.q_row_stride = static_cast<int64_t>(heads) * dim;
+  a.kv_row_stride = static_cast<int64_t>(kv_heads) * dim;
+  a.o_row_stride = a.q_row_stride;
+  a.dq_row_stride = a.q_row_stride;
+  a.dkv_row_stride = a.kv_row_stride;
+  a.lse_row_stride = heads;
+  a.d = dim;
+  a.scale = static_cast<float>(scale);
+  a.hm = {heads, kv_heads, 0, 0, heads / kv_heads};
+  spattn::launch_attn_bwd_pre(a, static_cast<int>(bs * lq), s);
+  check_launch();
+  if (!probs.empty()) attention_backward(s, a, probs);
+}
+
+void all_to_all(RankCtx& ctx, const CommGroup& group, const void* local, int64_t bs, int64_t len,
+                int64_t heads, int64_t dim, int elem_bytes, int scatter_dim, int gather_dim,
+                void* out) {
+  const int G = group.size();
+  const int me = group.index_of(ctx.rank);
+  (void)me;
+  MoveSpec m;
+  m.bs = bs;
+  m.elem = elem_bytes;
+  if (scatter_dim == 2 && gather_dim == 1) {
+    if (heads % G) throw ShapeError("all_to_all: extent " + std::to_string(heads) + " of axis 2 not divisible by group size " + std::to_string(G));
+    const int64_t hn = heads / G;
+    m.lloc = len, m.lg = len * G, m.xw = heads * dim;
+    for (int j = 0; j < G; ++j) {
+      m.win.push_back({j * hn * dim, 0, hn * dim, 0});
+      m.yw.push_back(hn * dim);
+      m.runs.push_back({{0, j * len, len}});
+    }
+    move_forward(ctx, group, m, local, out, ctx.stream);
+  } else if (scatter_dim == 1 && gather_dim == 2) {
+    if (len % G) throw ShapeError("all_to_all: extent " + std::to_string(len) + " of axis 1 not divisible by group size " + std::to_string(G));
+    const int64_t lo = len / G;
+    m.lloc = lo, m.lg = len, m.xw = heads * dim * G;
+    for (int j = 0; j < G; ++j) {
+      m.win.push_back({j * heads * dim, 0, heads * dim, 0});
+      m.yw.push_back(heads * dim);
+      m.runs.push_back({{0, j * lo, lo}});
+    }
+    move_reverse(ctx, group, m, local, out, false, ctx.stream);
+  } else {
+    throw ConfigError("all_to_all: only (scatter 2, gather 1) and (scatter 1, gather 2) are supported");
+  }
+}
+
+}  // namespace seqpar

@@ -1,0 +1,256 @@
+// HBM-bound data-movement kernels of the SP layer:
+//   * the fused pack/pad -> exchange -> unpack/unpad row copier used by every all-to-all
+//     (all_to_all_values + copy_region, comm.cpp:247-321; pad_axis_zeros / slice_axis,
+//     tensor.cpp:360-416), the zigzag/naive row permutation (shard_rows / gather_rows,
+//     partition.cpp:124-158) and the ring KV rotation (ring_shift, comm.cpp:449-460);
+//   * the LSE merge (merge_piece, attention.cpp:117-149);
+//   * fp32 <-> bf16 conversions for gradient accumulators.
+// All copies are byte-exact (dtype-agnostic, 16-byte vectorised when alignment allows).
+#include <atomic>
+
+#include "common.cuh"
+
+namespace spattn {
+namespace {
+
+struct CopyLaunch {
+  CopyTaskSet ts;
+  int64_t row_prefix[kMaxCopyTasks + 1];
+};
+
+template <int VW>
+struct Vec;
+template <>
+struct Vec<16> { using T = uint4; };
+template <>
+struct Vec<8> { using T = uint2; };
+template <>
+struct Vec<4> { using T = uint32_t; };
+template <>
+struct Vec<2> { using T = uint16_t; };
+template <>
+struct Vec<1> { using T = uint8_t; };
+
+// One warp per (task, row); lanes stride 16-byte (or narrower) vectors across the row.
+template <int VW>
+__global__ void __launch_bounds__(256) copy_rows_kernel(CopyLaunch L, int elem_bytes) {
+  using V = typename Vec<VW>::T;
+  const int64_t total = L.row_prefix[L.ts.n];
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; w < total; w += warps) {
+    int ti = 0;
+    while (ti + 1 < L.ts.n && L.row_prefix[ti + 1] <= w) ++ti;
+    const CopyTask& T = L.ts.t[ti];
+    const int64_t r = w - L.row_prefix[ti];
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(T.src) +
+                         ((T.src_row0 + r) * T.src_row_stride + T.src_col0) * elem_bytes;
+    uint8_t* dst = reinterpret_cast<uint8_t*>(T.dst) +
+                   ((T.dst_row0 + r) * T.dst_row_stride + T.dst_col0) * elem_bytes;
+    const int64_t nv = T.cols * elem_bytes / VW;
+    const V* s = reinterpret_cast<const V*>(src);
+    V* d = reinterpret_cast<V*>(dst);
+    for (int64_t i = lane; i < nv; i += 32) d[i] = s[i];
+    const int64_t nz = T.zero_cols * elem_bytes / VW;
+    V z;
+    memset(&z, 0, sizeof(V));
+    for (int64_t i = lane; i < nz; i += 32) d[nv + i] = z;
+  }
+}
+
+// fp32 variant that accumulates: dst += src (the repeat_heads backward group sum,
+// tensor.cpp:437-447, when kv windows of different ranks share a head).
+__global__ void __launch_bounds__(256) add_rows_kernel(CopyLaunch L) {
+  const int64_t total = L.row_prefix[L.ts.n];
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; w < total; w += warps) {
+    int ti = 0;
+    while (ti + 1 < L.ts.n && L.row_prefix[ti + 1] <= w) ++ti;
+    const CopyTask& T = L.ts.t[ti];
+    const int64_t r = w - L.row_prefix[ti];
+    const float* src = reinterpret_cast<const float*>(T.src) + (T.src_row0 + r) * T.src_row_stride + T.src_col0;
+    float* dst = reinterpret_cast<float*>(T.dst) + (T.dst_row0 + r) * T.dst_row_stride + T.dst_col0;
+    for (int64_t i = lane; i < T.cols; i += 32) dst[i] += src[i];
+  }
+}
+
+__global__ void lse_merge_kernel(float* acc_o, float* acc_lse, const float* o, const float* lse,
+                                 int64_t rows, int d) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const float la = acc_lse[row], lb = lse[row];
+  const float mx = fmaxf(la, lb);
+  if (lb == -INFINITY) return;  // empty piece: acc unchanged (attention.cpp:130-134)
+  float wa, wb, ln;
+  if (la == -INFINITY) {  // empty accumulator adopts the piece (attention.cpp:118-121)
+    wa = 0.f, wb = 1.f, ln = lb;
+  } else {
+    ln = mx + log1pf(__expf(fminf(la, lb) - mx));
+    wa = __expf(la - ln);
+    wb = __expf(lb - ln);
+  }
+  float* ap = acc_o + row * d;
+  const float* bp = o + row * d;
+  for (int i = lane; i < d; i += 32) ap[i] = la == -INFINITY ? bp[i] : ap[i] * wa + bp[i] * wb;
+  __syncwarp();
+  if (lane == 0) acc_lse[row] = ln;
+}
+
+__global__ void fill_f32_kernel(float* p, float v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void f32_to_bf16_2d_kernel(__nv_bfloat16* dst, int64_t dst_stride, const float* src,
+                                      int64_t src_stride, int64_t rows, int64_t cols, float scale) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    dst[r * dst_stride + c] = __float2bfloat16_rn(src[r * src_stride + c] * scale);
+  }
+}
+
+__global__ void f32_to_bf16_kernel(__nv_bfloat162* dst, const float2* src, float scale, int64_t n2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 v = src[i];
+    dst[i] = __floats2bfloat162_rn(v.x * scale, v.y * scale);
+  }
+}
+
+__global__ void bf16_to_f32_kernel(float* dst, const __nv_bfloat16* src, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __bfloat162float(src[i]);
+}
+
+__global__ void f32_add_2d_kernel(float* dst, int64_t dst_stride, const float* src,
+                                  int64_t src_stride, int64_t rows, int64_t cols) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    dst[r * dst_stride + c] += src[r * src_stride + c];
+  }
+}
+
+int grid_for(int64_t n, int per_block) {
+  int64_t b = (n + per_block - 1) / per_block;
+  const int64_t cap = 148 * 16;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    const int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a < 0 ? -a : a;
+}
+
+}  // namespace
+
+namespace {
+std::atomic<long long> g_launches{0};
+}
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+void launch_copy_tasks(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s) {
+  CopyLaunch L;
+  L.ts = ts;
+  L.row_prefix[0] = 0;
+  int64_t align = 16;
+  for (int i = 0; i < ts.n; ++i) {
+    const CopyTask& t = ts.t[i];
+    L.row_prefix[i + 1] = L.row_prefix[i] + t.rows;
+    for (int64_t v : {(int64_t)reinterpret_cast<uintptr_t>(t.src), (int64_t)reinterpret_cast<uintptr_t>(t.dst),
+                      t.src_row_stride * elem_bytes, t.dst_row_stride * elem_bytes,
+                      (t.src_row0 * t.src_row_stride + t.src_col0) * elem_bytes,
+                      (t.dst_row0 * t.dst_row_stride + t.dst_col0) * elem_bytes, t.cols * elem_bytes,
+                      t.zero_cols * elem_bytes})
+      align = gcd64(align, v == 0 ? 16 : v);
+  }
+  const int64_t total = L.row_prefix[ts.n];
+  if (total == 0) return;
+  const int grid = grid_for(total, 8);
+  switch (align) {
+    case 16: copy_rows_kernel<16><<<grid, 256, 0, s>>>(L, elem_bytes);
+  note_launch(); break;
+    case 8: copy_rows_kernel<8><<<grid, 256, 0, s>>>(L, elem_bytes);
+  note_launch(); break;
+    case 4: copy_rows_kernel<4><<<grid, 256, 0, s>>>(L, elem_bytes);
+  note_launch(); break;
+    case 2: copy_rows_kernel<2><<<grid, 256, 0, s>>>(L, elem_bytes);
+  note_launch(); break;
+    default: copy_rows_kernel<1><<<grid, 256, 0, s>>>(L, elem_bytes);
+  note_launch(); break;
+  }
+}
+
+void launch_add_tasks_f32(const CopyTaskSet& ts, cudaStream_t s) {
+  CopyLaunch L;
+  L.ts = ts;
+  L.row_prefix[0] = 0;
+  for (int i = 0; i < ts.n; ++i) L.row_prefix[i + 1] = L.row_prefix[i] + ts.t[i].rows;
+  const int64_t total = L.row_prefix[ts.n];
+  if (total == 0) return;
+  add_rows_kernel<<<grid_for(total, 8), 256, 0, s>>>(L);
+  note_launch();
+}
+
+void launch_lse_merge(float* acc_o, float* acc_lse, const float* o, const float* lse, int64_t rows,
+                      int d, cudaStream_t s) {
+  if (rows == 0) return;
+  lse_merge_kernel<<<(int)((rows + 7) / 8), 256, 0, s>>>(acc_o, acc_lse, o, lse, rows, d);
+  note_launch();
+}
+
+void launch_fill_f32(float* p, float v, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  fill_f32_kernel<<<grid_for(n, 1024), 256, 0, s>>>(p, v, n);
+  note_launch();
+}
+
+void launch_f32_to_bf16(void* dst, const float* src, float scale, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  if (n % 2 == 0) {
+    f32_to_bf16_kernel<<<grid_for(n / 2, 1024), 256, 0, s>>>(
+        reinterpret_cast<__nv_bfloat162*>(dst), reinterpret_cast<const float2*>(src), scale, n / 2);
+  note_launch();
+  } else {
+    f32_to_bf16_2d_kernel<<<grid_for(n, 1024), 256, 0, s>>>(reinterpret_cast<__nv_bfloat16*>(dst),
+                                                            n, src, n, 1, n, scale);
+  note_launch();
+  }
+}
+
+void launch_bf16_to_f32(float* dst, const void* src, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  bf16_to_f32_kernel<<<grid_for(n, 1024), 256, 0, s>>>(
+      dst, reinterpret_cast<const __nv_bfloat16*>(src), n);
+  note_launch();
+}
+
+void launch_f32_to_bf16_2d(void* dst, int64_t dst_stride, const float* src, int64_t src_stride,
+                           int64_t rows, int64_t cols, float scale, cudaStream_t s) {
+  if (rows * cols == 0) return;
+  f32_to_bf16_2d_kernel<<<grid_for(rows * cols, 1024), 256, 0, s>>>(
+      reinterpret_cast<__nv_bfloat16*>(dst), dst_stride, src, src_stride, rows, cols, scale);
+  note_launch();
+}
+
+void launch_f32_add_2d(float* dst, int64_t dst_stride, const float* src, int64_t src_stride,
+                       int64_t rows, int64_t cols, cudaStream_t s) {
+  if (rows * cols == 0) return;
+  f32_add_2d_kernel<<<grid_for(rows * cols, 1024), 256, 0, s>>>(dst, dst_stride, src, src_stride,
+                                                                rows, cols);
+  note_launch();
+}
+
+}  // namespace spattn

@@ -1,0 +1,115 @@
+// Internal kernel-launch interface between the C++ engines (engine.cpp) and the sm_100a
+// kernels. Plain structs, device pointers, explicit streams.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace spattn {
+
+// One rectangular attention problem in the flattened [rows, heads, dim] row space.
+// Key c (0-based within the k run) is admitted for query a (0-based within the q run) iff
+// !causal || c <= a + off. This is the reference's `kpos[j] <= qpos[i]` rule
+// (attention.cpp:89) for contiguous position runs: off = qpos0 - kpos0.
+struct AttnProblem {
+  int q_row0, nq;
+  int k_row0, nk;
+  int off;
+  int causal;
+};
+
+constexpr int kMaxProblems = 48;
+
+struct ProblemSet {
+  AttnProblem p[kMaxProblems];
+  int tile_prefix[kMaxProblems + 1];  // cumulative q tiles (of the launching kernel's BLOCK_M)
+  int n;
+};
+
+// Head mapping of a rank's local tensors: local q head h is global head q_head_base + h; it
+// reads kv head (q_head_base + h) / rep - kv_head_base of the local kv tensor. This indexes
+// GQA groups in place of repeat_heads (tensor.cpp:418-450).
+struct HeadMap {
+  int hq;            // local q heads computed
+  int hkv;           // local kv heads stored
+  int q_head_base;
+  int kv_head_base;
+  int rep;
+};
+
+struct FwdArgs {
+  const void* q;  // bf16 [rows, q_heads_stride, d]
+  const void* k;  // bf16 [rows_k, kv_heads_stride, d]
+  const void* v;
+  void* o;        // bf16 out (plain mode)
+  float* lse;     // [rows, q_heads_stride] natural-log LSE
+  float* acc_o;   // merge mode: fp32 [rows, q_heads_stride, d] running output (lse = running)
+  int64_t q_row_stride, kv_row_stride, o_row_stride;  // elements between consecutive rows
+  int lse_row_stride;                                 // floats between rows of lse
+  int d;
+  float scale;
+  HeadMap hm;
+};
+
+struct BwdArgs {
+  const void* q;
+  const void* k;
+  const void* v;
+  const void* o;
+  const void* dout;
+  const float* lse;    // natural log
+  float* delta;        // [rows, lse_row_stride] (filled by the preprocess kernel)
+  float* dq_acc;       // fp32 [rows, q heads, d] (atomic)
+  float* dk_acc;       // fp32 [rows_k, kv heads, d] (atomic)
+  float* dv_acc;
+  int64_t q_row_stride, kv_row_stride, o_row_stride;
+  int64_t dq_row_stride, dkv_row_stride;  // fp32 accumulator row strides
+  int lse_row_stride;
+  int d;
+  float scale;
+  HeadMap hm;
+};
+
+// Launch accounting (bench.py's gpu_launches): every launcher in this library calls this.
+void note_launch(int n = 1);
+long long launch_count();
+
+// ---- attention kernels (attn_mma.cu / attn_tc.cu) ----
+void launch_attn_fwd(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s);
+void launch_attn_bwd_pre(const BwdArgs& a, int rows, cudaStream_t s);
+void launch_attn_bwd(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
+
+// ---- element kernels (permute.cu) ----
+// One row-run copy task of the fused pack/pad -> exchange -> unpack/unpad permutation.
+// Copies `rows` rows: for r in [0, rows): dst[(dst_row0 + r) * dst_row_stride + dst_col0 ..]
+// <- src[(src_row0 + r) * src_row_stride + src_col0 ..] for `cols` elements, and zero-fills
+// the `zero_cols` elements that follow in dst (dummy-head padding). Strides in elements.
+struct CopyTask {
+  const void* src;
+  void* dst;
+  int64_t src_row_stride, dst_row_stride;
+  int64_t src_row0, dst_row0;
+  int64_t src_col0, dst_col0;
+  int64_t rows, cols, zero_cols;
+};
+constexpr int kMaxCopyTasks = 64;
+struct CopyTaskSet {
+  CopyTask t[kMaxCopyTasks];
+  int n;
+};
+void launch_copy_tasks(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s);
+
+// acc (fp32 out + lse) merge of a finished piece (fp32 out + lse) — merge_piece
+// (attention.cpp:117-149) in LSE form.
+void launch_lse_merge(float* acc_o, float* acc_lse, const float* o, const float* lse, int64_t rows,
+                      int d, cudaStream_t s);
+void launch_fill_f32(float* p, float v, int64_t n, cudaStream_t s);
+// dst_bf16[i] = src_f32[i] * scale
+void launch_f32_to_bf16(void* dst, const float* src, float scale, int64_t n, cudaStream_t s);
+void launch_bf16_to_f32(float* dst, const void* src, int64_t n, cudaStream_t s);
+// Strided variant: rows x cols block with independent row strides (elements).
+void launch_f32_to_bf16_2d(void* dst, int64_t dst_stride, const float* src, int64_t src_stride,
+                           int64_t rows, int64_t cols, float scale, cudaStream_t s);
+void launch_f32_add_2d(float* dst, int64_t dst_stride, const float* src, int64_t src_stride,
+                       int64_t rows, int64_t cols, cudaStream_t s);
+
+}  // namespace spattn

@@ -1,0 +1,403 @@
+"""Python surface of the B200 SP attention layer, mirroring the reference module ``_seqpar``
+(/root/reference/proj/bindings/py_module.cpp:315-401): same function names and argument
+meaning, ValueError subclasses for configuration/shape errors. Differences: tensors are torch
+CUDA tensors (bf16 compute), and ``engine_attention`` is differentiable (the reference binding
+is forward-only, py_module.cpp:111-180).
+
+Everything here calls libspattn.so through its C ABI (``_lib``); there is no CPU path."""
+from __future__ import annotations
+
+import ctypes
+import weakref
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib as C
+from ._lib import ConfigError, PeerAbort, ShapeError, StateError  # noqa: F401
+
+__version__ = "0.1.0"
+
+
+def _i64(n=1):
+    return (ctypes.c_int64 * n)()
+
+
+# ----------------------------------------------------------------------- layouts and counts
+def engine_names() -> list[str]:
+    return list(C.ENGINES)
+
+
+def shard_positions(mode: str, len: int, sp: int, index: int, ulysses_degree: int = 0,
+                    ring_degree: int = 0) -> list[int]:
+    """ShardLayout::positions_of (reference partition.cpp:105-111)."""
+    lay = C.make_layout(mode, len, sp, ulysses_degree, ring_degree)
+    n = len // sp if sp > 0 else 0
+    out = _i64(max(n, 1))
+    C.check(C.lib().spattn_layout_positions(ctypes.byref(lay), index, out))
+    return list(out[:n])
+
+
+position_ids = shard_positions  # make_position_ids (partition.cpp:160-162)
+
+
+def causal_pairs(mode: str, len: int, sp: int, index: int, ulysses_degree: int = 0,
+                 ring_degree: int = 0) -> int:
+    lay = C.make_layout(mode, len, sp, ulysses_degree, ring_degree)
+    out = _i64()
+    C.check(C.lib().spattn_causal_pairs(ctypes.byref(lay), index, out))
+    return out[0]
+
+
+def pad_length(len: int, sp: int, cutoff_len: int, pad_to_cutoff: bool = False) -> int:
+    out = _i64()
+    C.check(C.lib().spattn_pad_length(len, sp, cutoff_len, int(pad_to_cutoff), out))
+    return out[0]
+
+
+def pick_xtuner_insp(heads: int, sp: int, head_dim: int) -> int:
+    out = ctypes.c_int()
+    C.check(C.lib().spattn_pick_xtuner_insp(heads, sp, head_dim, ctypes.byref(out)))
+    return out.value
+
+
+def _ref_bytes(engine, bs, len, heads, head_dim, sp, u=0, r=0):
+    out = _i64()
+    C.check(C.lib().spattn_reference_bytes(C.engine_id(engine), bs, len, heads, head_dim, sp, u, r,
+                                           out))
+    return out[0]
+
+
+def ulysses_bytes(bs, len, heads, head_dim, sp):
+    return _ref_bytes("ulysses", bs, len, heads, head_dim, sp)
+
+
+def ring_bytes(bs, len, heads, head_dim, sp):
+    return _ref_bytes("ring", bs, len, heads, head_dim, sp)
+
+
+def dummy_head_bytes(bs, len, heads, head_dim, sp):
+    return _ref_bytes("dummy_head", bs, len, heads, head_dim, sp)
+
+
+def xtuner_bytes(bs, len, heads, head_dim, sp):
+    return _ref_bytes("xtuner", bs, len, heads, head_dim, sp)
+
+
+def usp_bytes(bs, len, heads, head_dim, ulysses_degree, ring_degree):
+    return _ref_bytes("usp", bs, len, heads, head_dim, ulysses_degree * ring_degree,
+                      ulysses_degree, ring_degree)
+
+
+def set_kernel_family(name: str) -> None:
+    """'tcgen05' (default where supported) or 'mma'."""
+    C.check(C.lib().spattn_set_kernel_family({"tcgen05": 0, "mma": 1}[name]))
+
+
+def kernel_family() -> str:
+    return ["tcgen05", "mma"][C.lib().spattn_get_kernel_family()]
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+# -------------------------------------------------------------------- row (re)distribution
+def _layout_for(mode: str, engine: str, length: int, sp: int, u: int, r: int):
+    if mode == "auto":  # py_module.cpp:39-47
+        mode = "zigzag" if engine == "ring" else "usp" if engine == "usp" else "naive"
+    return mode, C.make_layout(mode, length, sp, u, r)
+
+
+def shard_rows(x: torch.Tensor, mode: str, sp: int, index: int, ulysses_degree: int = 0,
+               ring_degree: int = 0) -> torch.Tensor:
+    """shard_rows (partition.cpp:124-139) on a CUDA tensor [L, ...] or [bs, L, ...] (dim 1 is the
+    sequence when x.dim() >= 3). Byte-exact for any dtype."""
+    seq_dim = 0 if x.dim() <= 2 else 1
+    L = x.shape[seq_dim]
+    lay = C.make_layout(mode, L, sp, ulysses_degree, ring_degree)
+    x = x.contiguous()
+    bs = 1 if seq_dim == 0 else x.shape[0]
+    row = x[0].numel() * x.element_size() if seq_dim == 0 else x[0, 0].numel() * x.element_size()
+    shape = list(x.shape)
+    shape[seq_dim] = L // sp
+    out = torch.empty(shape, dtype=x.dtype, device=x.device)
+    C.check(C.lib().spattn_shard_rows(_stream(), ctypes.byref(lay), index, bs, row, x.data_ptr(),
+                                      out.data_ptr()))
+    return out
+
+
+def gather_rows(shards: Sequence[torch.Tensor], mode: str, sp: int, ulysses_degree: int = 0,
+                ring_degree: int = 0) -> torch.Tensor:
+    """gather_rows (partition.cpp:141-158): inverse of shard_rows."""
+    if len(shards) != sp:
+        raise ShapeError(f"gather: got {len(shards)} shards for sp {sp}")
+    x0 = shards[0]
+    seq_dim = 0 if x0.dim() <= 2 else 1
+    L = x0.shape[seq_dim] * sp
+    lay = C.make_layout(mode, L, sp, ulysses_degree, ring_degree)
+    shape = list(x0.shape)
+    shape[seq_dim] = L
+    out = torch.empty(shape, dtype=x0.dtype, device=x0.device)
+    bs = 1 if seq_dim == 0 else x0.shape[0]
+    row = x0[0].numel() * x0.element_size() if seq_dim == 0 else x0[0, 0].numel() * x0.element_size()
+    for i, s in enumerate(shards):
+        s = s.contiguous()
+        C.check(C.lib().spattn_gather_rows(_stream(), ctypes.byref(lay), i, bs, row, s.data_ptr(),
+                                           out.data_ptr()))
+    return out
+
+
+# ---------------------------------------------------------------------------------- fabric
+class Fabric:
+    """Loopback CommFabric: ``world`` ranks as host threads sharing the current CUDA device
+    (comm.hpp:86-140). ``force_messages`` routes collectives through pack -> send/recv ->
+    unpack, the NCCL code path."""
+
+    def __init__(self, world: int, sp: Optional[int] = None, device: Optional[int] = None,
+                 force_messages: bool = False):
+        self.world = world
+        self.sp = sp or world
+        dev = torch.cuda.current_device() if device is None else device
+        h = ctypes.c_void_p()
+        C.check(C.lib().spattn_fabric_create(dev, world, self.sp, int(force_messages),
+                                             ctypes.byref(h)))
+        self._h = h
+        self._fin = weakref.finalize(self, C.lib().spattn_fabric_destroy, h)
+        self.ctxs = []
+        for r in range(world):
+            c = ctypes.c_void_p()
+            C.check(C.lib().spattn_fabric_ctx(h, r, ctypes.byref(c)))
+            self.ctxs.append(c)
+
+    def stats(self, rank: int) -> dict:
+        out = {}
+        for i, name in enumerate(C.PRIMITIVES):
+            calls, nbytes = _i64(), _i64()
+            C.check(C.lib().spattn_ctx_stats(self.ctxs[rank], i, calls, nbytes))
+            out[name] = (calls[0], nbytes[0])
+        return out
+
+    def total_bytes(self, rank: int) -> int:
+        return sum(b for _, b in self.stats(rank).values())
+
+    def flops(self, rank: int) -> int:
+        f = _i64()
+        C.check(C.lib().spattn_ctx_flops(self.ctxs[rank], f))
+        return f[0]
+
+    def reset_stats(self) -> None:
+        for c in self.ctxs:
+            C.check(C.lib().spattn_ctx_reset_stats(c))
+
+    def all_to_all(self, locals_: Sequence[torch.Tensor], scatter_dim: int,
+                   gather_dim: int) -> list[torch.Tensor]:
+        """all_to_all (comm.cpp:357-379) of 4-D [bs, len, heads, dim] tensors, any dtype."""
+        x0 = locals_[0]
+        bs, L, H, D = x0.shape
+        g = self.sp
+        if scatter_dim == 2 and gather_dim == 1:
+            shape = (bs, L * g, H // g if H % g == 0 else 0, D)
+        elif scatter_dim == 1 and gather_dim == 2:
+            shape = (bs, L // g if L % g == 0 else 0, H * g, D)
+        else:
+            raise ConfigError("all_to_all: unsupported dims")
+        outs = [torch.empty(shape, dtype=x0.dtype, device=x0.device) for _ in locals_]
+        torch.cuda.current_stream().synchronize()
+        ins = [x.contiguous() for x in locals_]
+        C.check(C.lib().spattn_fabric_all_to_all(
+            self._h, C.ptr_array([x.data_ptr() for x in ins]),
+            C.ptr_array([o.data_ptr() for o in outs]), bs, L, H, D, x0.element_size(),
+            scatter_dim, gather_dim))
+        return outs
+
+
+def _free_saved(handles):
+    for h in handles:
+        if h:
+            C.lib().spattn_saved_free(h)
+
+
+class _FabricEngine(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, fab, engine, cfg, lay, mode, u, r, docs, want_lse):
+        sp = fab.sp
+        qs = [shard_rows(q, mode, sp, i, u, r) for i in range(sp)]
+        ks = [shard_rows(k, mode, sp, i, u, r) for i in range(sp)]
+        vs = [shard_rows(v, mode, sp, i, u, r) for i in range(sp)]
+        outs = [torch.empty_like(x) for x in qs]
+        lses = [torch.empty(x.shape[:3], dtype=torch.float32, device=x.device) for x in qs]
+        torch.cuda.current_stream().synchronize()
+        saved = (ctypes.c_void_p * sp)()
+        nd = 0 if docs is None else len(docs)
+        darr = None if docs is None else (ctypes.c_int64 * nd)(*docs)
+        C.check(C.lib().spattn_fabric_fwd(
+            fab._h, C.engine_id(engine), ctypes.byref(cfg), ctypes.byref(lay), q.shape[0],
+            C.ptr_array([x.data_ptr() for x in qs]), C.ptr_array([x.data_ptr() for x in ks]),
+            C.ptr_array([x.data_ptr() for x in vs]), C.ptr_array([x.data_ptr() for x in outs]),
+            C.ptr_array([x.data_ptr() for x in lses]), darr, nd, saved))
+        handles = [saved[i] for i in range(sp)]
+        ctx.fab, ctx.mode, ctx.u, ctx.r = fab, mode, u, r
+        ctx.handles = handles
+        ctx.keep = (qs, ks, vs, outs)
+        ctx.fin = weakref.finalize(ctx.keep, _free_saved, handles)
+        out = gather_rows(outs, mode, sp, u, r)
+        lse = gather_rows(lses, mode, sp, u, r) if want_lse else None
+        ctx.mark_non_differentiable(*([lse] if lse is not None else []))
+        return out, lse
+
+    @staticmethod
+    def backward(ctx, dout, _dlse):
+        fab, mode, u, r = ctx.fab, ctx.mode, ctx.u, ctx.r
+        sp = fab.sp
+        qs, ks, vs, _ = ctx.keep
+        dos = [shard_rows(dout.contiguous(), mode, sp, i, u, r) for i in range(sp)]
+        dqs = [torch.empty_like(x) for x in qs]
+        dks = [torch.empty_like(x) for x in ks]
+        dvs = [torch.empty_like(x) for x in vs]
+        torch.cuda.current_stream().synchronize()
+        C.check(C.lib().spattn_fabric_bwd(
+            fab._h, C.ptr_array(ctx.handles), C.ptr_array([x.data_ptr() for x in dos]),
+            C.ptr_array([x.data_ptr() for x in dqs]), C.ptr_array([x.data_ptr() for x in dks]),
+            C.ptr_array([x.data_ptr() for x in dvs])))
+        ctx.fin()
+        dq = gather_rows(dqs, mode, sp, u, r)
+        dk = gather_rows(dks, mode, sp, u, r)
+        dv = gather_rows(dvs, mode, sp, u, r)
+        return dq, dk, dv, None, None, None, None, None, None, None, None, None
+
+
+def engine_attention(engine: str, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sp: int,
+                     layout: str = "auto", causal: bool = True, ulysses_degree: int = 0,
+                     ring_degree: int = 0, docs: Optional[Sequence[int]] = None,
+                     fabric: Optional[Fabric] = None, force_messages: bool = False,
+                     return_lse: bool = False):
+    """Sharded attention across ``sp`` loopback ranks on the current GPU, gathered back to the
+    full sequence (py_module.cpp:111-180), differentiable. q [bs, L, H, d] and k/v
+    [bs, L, Hkv, d] are bf16 CUDA tensors; ``docs`` are neat-packed document lengths."""
+    for t in (q, k, v):
+        if not t.is_cuda or t.dtype != torch.bfloat16:
+            raise ShapeError("engine_attention: q, k, v must be bf16 CUDA tensors")
+    bs, L, H, d = q.shape
+    Hkv = k.shape[2]
+    mode, lay = _layout_for(layout, engine, L, sp, ulysses_degree, ring_degree)
+    cfg = C.make_config(H, Hkv, d, causal, ulysses_degree, ring_degree)
+    fab = fabric or Fabric(sp, force_messages=force_messages)
+    if fab.sp != sp:
+        raise ConfigError("fabric sp does not match")
+    out, lse = _FabricEngine.apply(q.contiguous(), k.contiguous(), v.contiguous(), fab, engine,
+                                   cfg, lay, mode, ulysses_degree, ring_degree,
+                                   None if docs is None else list(docs), return_lse)
+    return (out, lse) if return_lse else out
+
+
+def oracle_attention(q, k, v, causal: bool = True, docs=None, return_lse: bool = False):
+    """Single-device attention (oracle engine, attention.cpp:218-260) on the GPU kernels."""
+    return engine_attention("oracle", q, k, v, 1, "naive", causal, docs=docs,
+                            return_lse=return_lse)
+
+
+def measure_engine_bytes(engine: str, len: int, heads: int, kv_heads: int, head_dim: int,
+                         sp: int, ulysses_degree: int = 0, ring_degree: int = 0, seed: int = 1,
+                         force_messages: bool = False) -> int:
+    """Per-rank bytes this implementation moves for one fwd+bwd (report.cpp:977-991), bf16
+    payloads and native GQA (the reference counts f64 and expanded KV); all ranks must agree."""
+    fab = Fabric(sp, force_messages=force_messages)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    q = torch.rand(1, len, heads, head_dim, device="cuda", generator=g).bfloat16() * 2 - 1
+    k = torch.rand(1, len, kv_heads, head_dim, device="cuda", generator=g).bfloat16() * 2 - 1
+    v = torch.rand(1, len, kv_heads, head_dim, device="cuda", generator=g).bfloat16() * 2 - 1
+    q.requires_grad_(True)
+    out = engine_attention(engine, q, k.requires_grad_(), v.requires_grad_(), sp,
+                           ulysses_degree=ulysses_degree, ring_degree=ring_degree, fabric=fab)
+    out.sum().backward()
+    totals = [fab.total_bytes(r) for r in range(sp)]
+    if len_set(totals) != 1:
+        raise StateError(f"per-rank byte totals differ: {totals}")
+    return totals[0]
+
+
+def len_set(xs):
+    return len(set(xs))
+
+
+# ------------------------------------------------------------------- multi-GPU (NCCL) path
+class RankContext:
+    """One GPU's RankCtx over NCCL (one process per GPU). Built collectively from an existing
+    torch.distributed process group, which only carries the 128-byte NCCL id."""
+
+    def __init__(self, sp: Optional[int] = None):
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        self.sp = sp or world
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = ctypes.create_string_buffer(128)
+            C.check(C.lib().spattn_nccl_unique_id(buf))
+            uid = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone()
+        if dist.get_backend() == "nccl":
+            uid = uid.cuda()
+        dist.broadcast(uid, 0)
+        raw = bytes(uid.cpu().tolist())
+        h = ctypes.c_void_p()
+        C.check(C.lib().spattn_ctx_create_nccl(torch.cuda.current_device(), rank, world, self.sp,
+                                               raw, ctypes.byref(h)))
+        self._h = h
+        self.rank, self.world = rank, world
+        self._fin = weakref.finalize(self, C.lib().spattn_ctx_destroy, h)
+
+    def stats(self) -> dict:
+        out = {}
+        for i, name in enumerate(C.PRIMITIVES):
+            calls, nbytes = _i64(), _i64()
+            C.check(C.lib().spattn_ctx_stats(self._h, i, calls, nbytes))
+            out[name] = (calls[0], nbytes[0])
+        return out
+
+
+class _RankEngine(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, rc, engine, cfg, lay, docs):
+        out = torch.empty_like(q)
+        lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
+        C.check(C.lib().spattn_ctx_set_stream(rc._h, _stream()))
+        saved = ctypes.c_void_p()
+        nd = 0 if docs is None else len(docs)
+        darr = None if docs is None else (ctypes.c_int64 * nd)(*docs)
+        C.check(C.lib().spattn_fwd(rc._h, C.engine_id(engine), ctypes.byref(cfg), ctypes.byref(lay),
+                                   q.shape[0], q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                   out.data_ptr(), lse.data_ptr(), darr, nd, ctypes.byref(saved)))
+        ctx.rc, ctx.h = rc, saved
+        ctx.save_for_backward(q, k, v, out)
+        ctx.fin = weakref.finalize(out, C.lib().spattn_saved_free, saved)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        q, k, v, out = ctx.saved_tensors
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        C.check(C.lib().spattn_ctx_set_stream(ctx.rc._h, _stream()))
+        C.check(C.lib().spattn_bwd(ctx.rc._h, ctx.h, dout.contiguous().data_ptr(), dq.data_ptr(),
+                                   dk.data_ptr(), dv.data_ptr()))
+        return dq, dk, dv, None, None, None, None, None
+
+
+class SequenceParallelAttention(torch.nn.Module):
+    """Per-rank SP attention layer (run_attention_engine, attention.hpp:90-92) over NCCL:
+    every rank of the SP group calls it with its sequence shard."""
+
+    def __init__(self, engine: str, heads: int, kv_heads: int, head_dim: int, seq_len: int,
+                 rank_ctx: RankContext, layout: str = "auto", causal: bool = True,
+                 ulysses_degree: int = 0, ring_degree: int = 0):
+        super().__init__()
+        self.engine = engine
+        self.rc = rank_ctx
+        self.mode, self.lay = _layout_for(layout, engine, seq_len, rank_ctx.sp, ulysses_degree,
+                                          ring_degree)
+        self.cfg = C.make_config(heads, kv_heads, head_dim, causal, ulysses_degree, ring_degree)
+
+    def forward(self, q, k, v, docs: Optional[Sequence[int]] = None):
+        return _RankEngine.apply(q.contiguous(), k.contiguous(), v.contiguous(), self.rc,
+                                 self.engine, self.cfg, self.lay,
+                                 None if docs is None else list(docs))

@@ -1,0 +1,65 @@
+"""CPU checks of the C-ABI boundary: libspattn.so loads without a GPU, exports every symbol
+include/spattn.h declares, and its host (integer) functions reproduce the reference's golden
+layouts, padding, xtuner factors and byte models (tests/golden/reference_api.json)."""
+import ctypes
+import json
+import os
+import re
+
+import pytest
+
+from paper_2505_22296_b200 import _lib as C
+import paper_2505_22296_b200 as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+API = json.load(open(os.path.join(ROOT, "tests", "golden", "reference_api.json")))["api"]
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "spattn.h")).read()
+    return sorted(set(re.findall(r"\b(spattn_\w+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert header_symbols() == sorted(C.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = C.lib()
+    for name in header_symbols():
+        assert hasattr(L, name), name
+    assert L.spattn_abi_version() == 1
+
+
+def test_layout_positions_and_pairs_match_reference():
+    for key, per_rank in API["positions"].items():
+        mode, L, sp, u, r = key.split("/")
+        L, sp, u, r = int(L), int(sp), int(u), int(r)
+        for i in range(sp):
+            assert P.shard_positions(mode, L, sp, i, u, r) == per_rank[i], key
+            assert P.causal_pairs(mode, L, sp, i, u, r) == API["causal_pairs"][key][i], key
+
+
+def test_pad_length_insp_bytes_match_reference():
+    for *args, want in API["pad_length"]:
+        assert P.pad_length(*args) == want
+    for *args, want in API["insp"]:
+        assert P.pick_xtuner_insp(*args) == want
+    for fn, args, want in API["bytes"]:
+        assert getattr(P, fn)(*args) == want, (fn, args)
+
+
+def test_errors_map_to_value_error():
+    # tests/test_partition.cpp:82-89 and attention.cpp:354-366 rejects
+    with pytest.raises(ValueError):
+        P.shard_positions("naive", 10, 4, 0)
+    with pytest.raises(ValueError):
+        P.shard_positions("zigzag", 12, 4, 0)
+    with pytest.raises(ValueError):
+        P.pick_xtuner_insp(3, 4, 9)
+    with pytest.raises(ValueError):
+        P.pad_length(50, 2, 32)
+    with pytest.raises(ValueError):
+        P.shard_positions("bogus", 16, 2, 0)
+    msg = C.lib().spattn_last_error().decode()
+    assert msg  # thread-local message of the last failing call
