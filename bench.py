@@ -213,7 +213,8 @@ def main():
     q, k, v, do = mk(heads), mk(kv), mk(kv), mk(heads)
     out, dq, dk, dv = (torch.empty_like(x) for x in (q, q, k, v))
     lse = torch.empty(1, lloc, heads, device="cuda", dtype=torch.float32)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # explicit stream: events and kernels share it
+    torch.cuda.set_stream(stream)
     C.check(C.lib().spattn_ctx_set_stream(ctx, stream.cuda_stream))
     eid = C.engine_id(engine)
 

@@ -74,7 +74,7 @@ int spattn_ctx_destroy(spattn_ctx* ctx);
 int spattn_fabric_create(int device, int world, int sp, int force_messages, spattn_fabric** out);
 int spattn_fabric_destroy(spattn_fabric* f);
 int spattn_fabric_ctx(spattn_fabric* f, int rank, spattn_ctx** out);
-/* Compute stream of a context (cudaStream_t); NULL restores the context's own stream. */
+/* Compute stream of a context (cudaStream_t; 0 is the legacy default stream). */
 int spattn_ctx_set_stream(spattn_ctx* ctx, void* stream);
 int spattn_ctx_stream(spattn_ctx* ctx, void** stream);
 /* send-side per-primitive counters (PrimitiveStats, comm.hpp:30-33) and flop counter */

@@ -225,7 +225,7 @@ int spattn_fabric_ctx(spattn_fabric* f, int rank, spattn_ctx** out) {
 }
 
 int spattn_ctx_set_stream(spattn_ctx* c, void* stream) {
-  return guard([&] { c->rc->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream; });
+  return guard([&] { c->rc->stream = static_cast<cudaStream_t>(stream); });
 }
 int spattn_ctx_stream(spattn_ctx* c, void** stream) {
   return guard([&] { *stream = c->rc->stream; });

@@ -420,11 +420,17 @@ void move_reverse(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
   if (G == 1 || ctx.transport->peer_access()) {
     std::vector<void*> ptrs{const_cast<void*>(y)};
     if (G > 1) ptrs = ctx.transport->exchange_ptrs(g, ctx.rank, const_cast<void*>(y), s);
+    // accumulating unpacks run one source per launch: overlapping windows of different
+    // members would otherwise race on the same destination elements
     std::vector<CopyTask> tasks;
     for (int j = 0; j < G; ++j) {
       auto t = gather_from(j, ptrs[static_cast<size_t>(j)], m.yw[static_cast<size_t>(j)],
                            m.win[static_cast<size_t>(j)].ycol, false);
       tasks.insert(tasks.end(), t.begin(), t.end());
+      if (add) {
+        run_tasks(tasks, m.elem, true, s);
+        tasks.clear();
+      }
     }
     run_tasks(tasks, m.elem, add, s);
     if (G > 1) ctx.transport->release(g, ctx.rank, s);
@@ -459,6 +465,10 @@ void move_reverse(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
     auto t = gather_from(j, static_cast<char*>(rbuf.p) + roff[j] * m.elem,
                          m.win[static_cast<size_t>(j)].n, 0, true);
     tasks.insert(tasks.end(), t.begin(), t.end());
+    if (add) {
+      run_tasks(tasks, m.elem, true, s);
+      tasks.clear();
+    }
   }
   run_tasks(tasks, m.elem, add, s);
 }

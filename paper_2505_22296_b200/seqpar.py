@@ -212,6 +212,13 @@ class Fabric:
         return outs
 
 
+class _Keep:
+    """Per-rank shards the saved forward state points into (weak-referenceable holder)."""
+
+    def __init__(self, *tensors):
+        self.tensors = tensors
+
+
 def _free_saved(handles):
     for h in handles:
         if h:
@@ -239,7 +246,7 @@ class _FabricEngine(torch.autograd.Function):
         handles = [saved[i] for i in range(sp)]
         ctx.fab, ctx.mode, ctx.u, ctx.r = fab, mode, u, r
         ctx.handles = handles
-        ctx.keep = (qs, ks, vs, outs)
+        ctx.keep = _Keep(qs, ks, vs, outs, lses)
         ctx.fin = weakref.finalize(ctx.keep, _free_saved, handles)
         out = gather_rows(outs, mode, sp, u, r)
         lse = gather_rows(lses, mode, sp, u, r) if want_lse else None
@@ -250,7 +257,7 @@ class _FabricEngine(torch.autograd.Function):
     def backward(ctx, dout, _dlse):
         fab, mode, u, r = ctx.fab, ctx.mode, ctx.u, ctx.r
         sp = fab.sp
-        qs, ks, vs, _ = ctx.keep
+        qs, ks, vs = ctx.keep.tensors[:3]
         dos = [shard_rows(dout.contiguous(), mode, sp, i, u, r) for i in range(sp)]
         dqs = [torch.empty_like(x) for x in qs]
         dks = [torch.empty_like(x) for x in ks]
