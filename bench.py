@@ -345,7 +345,8 @@ def main():
         except Exception as ex:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "error": str(ex)}
     print(json.dumps(line), flush=True)
-    del keep
+    torch.cuda.synchronize()
+    keep._fin()  # release the library's streams/communicators while CUDA is still up
     if dist:
         dist.destroy_process_group()
 
