@@ -1,9 +1,458 @@
-// tcgen05 / TMEM / TMA attention kernels for sm_100a (forward and backward).
-#include "common.cuh"
+// tcgen05 / TMEM / TMA attention kernels for sm_100a.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "tc.cuh"
 
 namespace spattn {
-bool tc_fwd_supported(const FwdArgs&) { return false; }
-void launch_attn_fwd_tc(const FwdArgs&, const ProblemSet&, cudaStream_t) {}
+
+// ------------------------------------------------------------------------ host: TMA maps
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeFn>(nullptr);
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+}  // namespace
+
+bool make_tma_2d(CUtensorMap* m, const void* base, uint64_t width, uint64_t rows,
+                 uint64_t row_stride_elems, uint32_t box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {width, rows};
+  cuuint64_t strides[1] = {row_stride_elems * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ------------------------------------------------------------- descriptor self-test GEMMs
+// D1 = A . B^T (B K-major, like S = Q K^T) and D2 = A . Bmn (B MN-major, like O = P V) for
+// 128x128x128 bf16 tiles, through TMA + tcgen05.mma + TMEM. Validates the descriptor
+// encodings the attention kernels use.
+namespace {
+__global__ void __launch_bounds__(128, 1)
+    umma_selftest_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                         const __grid_constant__ CUtensorMap tBmn, float* D1, float* D2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sA = smem_u32(smem), sB = sA + 32768, sC = sA + 65536;
+  __shared__ uint64_t bars[2];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t bar_load = smem_u32(&bars[0]), bar_mma = smem_u32(&bars[1]);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(bar_load, 1);
+    tc::mbar_init(bar_mma, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<256>(smem_u32(&tmem_base));
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  if (warp == 0 && lane == 0) {
+    tc::mbar_expect_tx(bar_load, 3 * 32768);
+    for (int b = 0; b < 2; ++b) {
+      tc::tma_load_2d(sA + b * 16384, &tA, b * 64, 0, bar_load);
+      tc::tma_load_2d(sB + b * 16384, &tB, b * 64, 0, bar_load);
+      tc::tma_load_2d(sC + b * 16384, &tBmn, b * 64, 0, bar_load);
+    }
+    tc::mbar_wait(bar_load, 0);
+    tc::fence_after();
+    constexpr uint32_t id_k = tc::idesc_bf16(128, 128, false, false);
+    constexpr uint32_t id_mn = tc::idesc_bf16(128, 128, false, true);
+    for (int ks = 0; ks < 8; ++ks) {
+      const uint32_t off = (ks / 4) * 16384 + (ks % 4) * 32;
+      tc::mma_ss(tmem, tc::sdesc(sA + off, 16, 1024), tc::sdesc(sB + off, 16, 1024), id_k, ks > 0);
+    }
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint32_t off = (kk / 4) * 16384 + (kk % 4) * 32;
+      tc::mma_ss(tmem + 128, tc::sdesc(sA + off, 16, 1024), tc::sdesc(sC + kk * 2048, 16384, 1024),
+                 id_mn, kk > 0);
+    }
+    tc::commit(bar_mma);
+  }
+  __syncwarp();
+  tc::mbar_wait(bar_mma, 0);
+  tc::fence_after();
+  const int row = warp * 32 + lane;
+  for (int half = 0; half < 2; ++half)
+    for (int c = 0; c < 128; c += 32) {
+      uint32_t r[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + half * 128 + c, r);
+      tc::tmem_wait_ld();
+      float* dst = (half ? D2 : D1) + row * 128 + c;
+      for (int i = 0; i < 32; ++i) dst[i] = __uint_as_float(r[i]);
+    }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<256>(tmem);
+}
+}  // namespace
+
+int umma_selftest(cudaStream_t s, const void* A, const void* B, const void* Bmn, float* D1, float* D2) {
+  CUtensorMap tA, tB, tC;
+  if (!make_tma_2d(&tA, A, 128, 128, 128, 128) || !make_tma_2d(&tB, B, 128, 128, 128, 128) ||
+      !make_tma_2d(&tC, Bmn, 128, 128, 128, 128))
+    return -1;
+  const int smem = 3 * 32768 + 1024;
+  cudaFuncSetAttribute(umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  umma_selftest_kernel<<<1, 128, smem, s>>>(tA, tB, tC, D1, D2);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+// =================================================================================
+// Forward: one CTA = 128 query rows x one head of one problem. Warp roles:
+//   warp 0      TMA producer (Q once; K_j, V_j into a 2-stage ring)
+//   warp 1      MMA issuer (one elected thread): S_j = Q K_j^T into TMEM S[j%2], then
+//               O += P_{j-1} V_{j-1} into TMEM O — S_{j+1} overlaps the softmax of tile j
+//   warp 2      TMEM allocator (512 columns: S0 | S1 | O)
+//   warps 4..7  softmax + epilogue: thread t owns query row t = TMEM lane t; P_j goes to a
+//               double-buffered 128B-swizzled smem tile (the A operand of the PV MMA)
+// O is rescaled in TMEM only when a row max grows by more than 2^8 (exponents stay <= 256),
+// and lse/out are finalised from TMEM. attn_block_forward + finalize_piece
+// (attention.cpp:61-115, :151-165); merge mode folds merge_piece (:117-149) into the epilogue.
+namespace {
+
+template <int D>
+struct FwdLayout {
+  static constexpr int QB = D / 64;
+  static constexpr int TILE = 128 * D * 2;  // Q, K or V tile (128 rows)
+  static constexpr int P_TILE = 128 * 128 * 2;
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = Q_OFF + TILE;
+  static constexpr int V_OFF = K_OFF + 2 * TILE;
+  static constexpr int P_OFF = V_OFF + 2 * TILE;
+  static constexpr int BAR_OFF = P_OFF + 2 * P_TILE;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+enum FwdBar { B_Q = 0, B_KF = 1, B_VF = 3, B_KVE = 5, B_SF = 7, B_SFREE = 9, B_PF = 11, B_PV = 13, B_N = 15 };
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, FwdArgs a, ProblemSet ps) {
+  using Lay = FwdLayout<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sQ = sbase + Lay::Q_OFF, sK = sbase + Lay::K_OFF, sV = sbase + Lay::V_OFF,
+                 sP = sbase + Lay::P_OFF;
+  const uint32_t bars = sbase + Lay::BAR_OFF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Lay::BAR_OFF + B_N * 8);
+  auto bar = [&](int i) { return bars + 8u * i; };
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // ---- tile decode (heavy causal tiles first)
+  int pi = 0;
+  while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= (int)blockIdx.x) ++pi;
+  const AttnProblem P = ps.p[pi];
+  int mt = blockIdx.x - ps.tile_prefix[pi];
+  if (P.causal) mt = (ps.tile_prefix[pi + 1] - ps.tile_prefix[pi]) - 1 - mt;
+  const int m0 = mt * 128;
+  const int h = blockIdx.y;
+  const HeadMap hm = a.hm;
+  const int kvh = (hm.q_head_base + h) / hm.rep - hm.kv_head_base;
+  const int q_valid = min(128, P.nq - m0);
+  int n_end = P.nk;
+  if (P.causal) n_end = min(P.nk, m0 + q_valid - 1 + P.off + 1);
+  n_end = max(n_end, 0);
+  const int n_tiles = (n_end + 127) / 128;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < B_N; ++i) {
+      const bool sm = (i >= B_SFREE && i < B_SFREE + 2) || (i >= B_PF && i < B_PF + 2);
+      tc::mbar_init(bar(i), sm ? 128 : 1);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc<512>(smem_u32(tmem_slot));
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tO = tmem + 256;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      tc::tma_prefetch(&tmQ);
+      tc::tma_prefetch(&tmK);
+      tc::tma_prefetch(&tmV);
+      tc::mbar_expect_tx(bar(B_Q), Lay::TILE);
+      for (int b = 0; b < Lay::QB; ++b)
+        tc::tma_load_2d(sQ + b * 16384, &tmQ, h * D + b * 64, P.q_row0 + m0, bar(B_Q));
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1;
+        if (j >= 2) tc::mbar_wait(bar(B_KVE + st), ((j - 2) >> 1) & 1);
+        const int y = P.k_row0 + j * 128;
+        tc::mbar_expect_tx(bar(B_KF + st), Lay::TILE);
+        for (int b = 0; b < Lay::QB; ++b)
+          tc::tma_load_2d(sK + st * Lay::TILE + b * 16384, &tmK, kvh * D + b * 64, y, bar(B_KF + st));
+        tc::mbar_expect_tx(bar(B_VF + st), Lay::TILE);
+        for (int b = 0; b < Lay::QB; ++b)
+          tc::tma_load_2d(sV + st * Lay::TILE + b * 16384, &tmV, kvh * D + b * 64, y, bar(B_VF + st));
+      }
+    }
+  } else if (warp == 1) {
+    if (tc::elect_one()) {
+      constexpr uint32_t id_s = tc::idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_o = tc::idesc_bf16(128, D, false, true);
+      auto issue_pv = [&](int i) {
+        const int st = i & 1;
+        tc::mbar_wait(bar(B_PF + st), (i >> 1) & 1);
+        tc::mbar_wait(bar(B_VF + st), (i >> 1) & 1);
+        tc::fence_after();
+        const uint32_t pbase = sP + st * Lay::P_TILE, vbase = sV + st * Lay::TILE;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;
+          tc::mma_ss(tO, tc::sdesc(pbase + aoff, 16, 1024), tc::sdesc(vbase + kk * 2048, 16384, 1024),
+                     id_o, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::commit(bar(B_PV + st));
+        tc::commit(bar(B_KVE + st));
+      };
+      if (n_tiles > 0) tc::mbar_wait(bar(B_Q), 0);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1;
+        tc::mbar_wait(bar(B_KF + st), (j >> 1) & 1);
+        if (j >= 2) tc::mbar_wait(bar(B_SFREE + st), ((j - 2) >> 1) & 1);
+        tc::fence_after();
+        const uint32_t kbase = sK + st * Lay::TILE;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
+          tc::mma_ss(tmem + st * 128, tc::sdesc(sQ + off, 16, 1024), tc::sdesc(kbase + off, 16, 1024),
+                     id_s, ks > 0 ? 1u : 0u);
+        }
+        tc::commit(bar(B_SF + st));
+        if (j >= 1) issue_pv(j - 1);
+      }
+      if (n_tiles > 0) issue_pv(n_tiles - 1);
+    }
+  } else if (warp >= 4) {
+    const int row = threadIdx.x - 128;  // query row within the tile == TMEM lane
+    const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
+    const float sl2 = a.scale * kLog2e;
+    const int qa = m0 + row;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int st = j & 1;
+      tc::mbar_wait(bar(B_SF + st), (j >> 1) & 1);
+      tc::fence_after();
+      float x[128];
+      {
+        uint32_t r[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tc::tmem_ld32(tmem + lane_base + st * 128 + c * 32, r[c]);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[c * 32 + i] = __uint_as_float(r[c][i]);
+      }
+      tc::fence_before();
+      tc::mbar_arrive(bar(B_SFREE + st));
+      const int n0 = j * 128;
+      const bool need_mask = (n0 + 128 > P.nk) || (P.causal && n0 + 127 > m0 + P.off);
+      float mt = -INFINITY;
+      if (need_mask) {
+        const int lim = P.causal ? min(P.nk - 1, qa + P.off) - n0 : P.nk - 1 - n0;
+#pragma unroll
+        for (int i = 0; i < 128; ++i) {
+          x[i] = i <= lim ? x[i] * sl2 : -INFINITY;
+          mt = fmaxf(mt, x[i]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) {
+          x[i] *= sl2;
+          mt = fmaxf(mt, x[i]);
+        }
+      }
+      if (j == 0) {
+        m_run = mt;
+      } else if (__any_sync(0xffffffffu, mt > m_run + 8.f)) {
+        // lazy rescale of O (and l) to a new running max; O must hold P_{j-1} V_{j-1}
+        const float m_new = fmaxf(m_run, mt);
+        const float alpha = (m_run == -INFINITY || m_new == -INFINITY) ? (m_run == m_new ? 1.f : 0.f)
+                                                                        : fast_exp2(m_run - m_new);
+        tc::mbar_wait(bar(B_PV + ((j - 1) & 1)), ((j - 1) >> 1) & 1);
+        tc::fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          tc::tmem_ld32(tO + lane_base + c * 32, r);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tc::tmem_st32(tO + lane_base + c * 32, r);
+        }
+        tc::tmem_wait_st();
+        l_run *= alpha;
+        m_run = m_new;
+      }
+      const float muse = m_run == -INFINITY ? 0.f : m_run;
+      float rs = 0.f;
+      // P buffer st was last read by PV_{j-2}
+      if (j >= 2) tc::mbar_wait(bar(B_PV + st), ((j - 2) >> 1) & 1);
+      const uint32_t pbase = sP + st * Lay::P_TILE;
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p0 = fast_exp2(x[ch * 8 + 2 * e] - muse);
+          const float p1 = fast_exp2(x[ch * 8 + 2 * e + 1] - muse);
+          rs += p0 + p1;
+          w[e] = pack_bf16(p0, p1);
+        }
+        const uint32_t addr = tc::sw128(pbase + (ch >> 3) * 16384, row, ch & 7);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(w[0]), "r"(w[1]),
+                     "r"(w[2]), "r"(w[3]));
+      }
+      l_run += rs;
+      tc::fence_proxy_async();
+      tc::mbar_arrive(bar(B_PF + st));
+    }
+    // ---- epilogue
+    const bool empty = !(l_run > 0.f);
+    const float inv = empty ? 0.f : 1.f / l_run;
+    const float lse_row = empty ? -INFINITY : (m_run + __log2f(l_run)) * kLn2;
+    if (n_tiles > 0) {
+      tc::mbar_wait(bar(B_PV + ((n_tiles - 1) & 1)), ((n_tiles - 1) >> 1) & 1);
+      tc::fence_after();
+    }
+    const bool valid = qa < P.nq;
+    const int64_t grow = (int64_t)(P.q_row0 + qa);
+    if (a.acc_o == nullptr) {
+      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(a.o) + grow * a.o_row_stride + h * D;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        if (n_tiles > 0) {
+          tc::tmem_ld32(tO + lane_base + c * 32, r);
+          tc::tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        uint32_t w[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          w[i] = pack_bf16(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
+        if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+        }
+      }
+      if (valid) a.lse[grow * a.lse_row_stride + h] = lse_row;
+    } else {
+      float* lp = a.lse + grow * a.lse_row_stride + h;
+      const float la = valid ? *lp : -INFINITY;
+      const float lb = lse_row;
+      const float mx = fmaxf(la, lb);
+      float wa = 1.f, wb = 0.f, ln = la;
+      if (mx != -INFINITY) {
+        ln = mx + __logf(__expf(la - mx) + __expf(lb - mx));
+        wa = __expf(la - ln);
+        wb = __expf(lb - ln) * inv;
+      }
+      float* arow = a.acc_o + grow * a.o_row_stride + h * D;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        if (n_tiles > 0) {
+          tc::tmem_ld32(tO + lane_base + c * 32, r);
+          tc::tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (valid) {
+          float4* ap = reinterpret_cast<float4*>(arow + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 cur = ap[i];
+            cur.x = cur.x * wa + __uint_as_float(r[4 * i]) * wb;
+            cur.y = cur.y * wa + __uint_as_float(r[4 * i + 1]) * wb;
+            cur.z = cur.z * wa + __uint_as_float(r[4 * i + 2]) * wb;
+            cur.w = cur.w * wa + __uint_as_float(r[4 * i + 3]) * wb;
+            ap[i] = cur;
+          }
+        }
+      }
+      if (valid) *lp = ln;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 2) tc::tmem_dealloc<512>(tmem);
+}
+
+int max_rows(const ProblemSet& ps, bool q) {
+  int m = 0;
+  for (int i = 0; i < ps.n; ++i) m = max(m, q ? ps.p[i].q_row0 + ps.p[i].nq : ps.p[i].k_row0 + ps.p[i].nk);
+  return m;
+}
+
+template <int D>
+void launch_fwd_tc_d(const FwdArgs& a, const ProblemSet& in, cudaStream_t s) {
+  ProblemSet ps = in;
+  ps.tile_prefix[0] = 0;
+  for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nq + 127) / 128;
+  const int tiles = ps.tile_prefix[ps.n];
+  if (tiles == 0 || a.hm.hq == 0) return;
+  CUtensorMap tq, tk, tv;
+  const uint64_t qw = (uint64_t)a.q_row_stride, kw = (uint64_t)a.kv_row_stride;
+  if (!make_tma_2d(&tq, a.q, qw, max_rows(ps, true), qw, 128) ||
+      !make_tma_2d(&tk, a.k, kw, max(1, max_rows(ps, false)), kw, 128) ||
+      !make_tma_2d(&tv, a.v, kw, max(1, max_rows(ps, false)), kw, 128)) {
+    cudaGetLastError();
+    return;
+  }
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FwdLayout<D>::SMEM);
+  });
+  attn_fwd_tc_kernel<D><<<dim3(tiles, a.hm.hq), 256, FwdLayout<D>::SMEM, s>>>(tq, tk, tv, a, ps);
+  note_launch();
+}
+
+}  // namespace
+
+bool tc_fwd_supported(const FwdArgs& a) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(a.q) % 16 == 0) && (reinterpret_cast<uintptr_t>(a.k) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(a.v) % 16 == 0) && (a.q_row_stride * 2) % 16 == 0 &&
+                       (a.kv_row_stride * 2) % 16 == 0;
+  return (a.d == 64 || a.d == 128) && aligned;
+}
+void launch_attn_fwd_tc(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
+  if (a.d == 64)
+    launch_fwd_tc_d<64>(a, ps, s);
+  else
+    launch_fwd_tc_d<128>(a, ps, s);
+}
 bool tc_bwd_supported(const BwdArgs&) { return false; }
 void launch_attn_bwd_tc(const BwdArgs&, const ProblemSet&, cudaStream_t) {}
+
 }  // namespace spattn

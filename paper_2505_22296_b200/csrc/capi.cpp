@@ -250,6 +250,19 @@ int spattn_set_kernel_family(int family) {
 }
 int spattn_get_kernel_family(void) { return seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 ? 0 : 1; }
 
+}  // extern "C"
+namespace spattn {
+int umma_selftest(cudaStream_t s, const void* A, const void* B, const void* Bmn, float* D1, float* D2);
+}
+extern "C" {
+int spattn_selftest_umma(void* stream, const void* a, const void* b, const void* b_mn, float* d1,
+                         float* d2) {
+  return guard([&] {
+    if (spattn::umma_selftest(static_cast<cudaStream_t>(stream), a, b, b_mn, d1, d2) != 0)
+      throw seqpar::StateError("umma self-test launch failed");
+  });
+}
+
 int64_t spattn_launch_count(void) { return spattn::launch_count(); }
 int spattn_profile_enable(int on) {
   return guard([&] { seqpar::profile_enable(on != 0); });

@@ -38,7 +38,7 @@ using spattn::HeadMap;
   } while (0)
 
 namespace {
-KernelFamily g_family = KernelFamily::mma;
+KernelFamily g_family = KernelFamily::tcgen05;
 }
 void set_kernel_family(KernelFamily f) { g_family = f; }
 KernelFamily kernel_family() { return g_family; }
