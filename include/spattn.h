@@ -91,10 +91,11 @@ int64_t spattn_launch_count(void);
 int spattn_profile_enable(int on);
 int spattn_profile_read(double ms[2], int64_t n[2]);
 
-/* Descriptor self-test of the tcgen05 path: d1 = a . b^T, d2 = a . b_mn for 128x128 bf16
- * row-major tiles through TMA + tcgen05.mma + TMEM (fp32 outputs, 128x128). */
+/* Descriptor self-test of the tcgen05 path: d1 = a . b^T, d2 = a . b_mn (smem operands) and
+ * d3 = a . b_mn with a read from TMEM, for 128x128 bf16 row-major tiles through TMA +
+ * tcgen05.mma + TMEM (fp32 outputs, 128x128; d3 may be NULL). */
 int spattn_selftest_umma(void* stream, const void* a, const void* b, const void* b_mn, float* d1,
-                         float* d2);
+                         float* d2, float* d3);
 
 /* ---- engine: run_attention_engine (attention.hpp:90-92) + its tape backward ----
  * Collective over the SP group: every rank calls with its shard. q [bs, local_len, heads, d],

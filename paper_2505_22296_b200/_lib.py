@@ -119,7 +119,7 @@ def lib() -> ctypes.CDLL:
         "spattn_block_bwd": [_vp, _i64, _i32, _i32, _i32, _vp, _i64p, _i64, _vp, _vp, _i64p,
                              _i64, _i32, ctypes.c_double, _vp, _vp, _vp, _vp, _vp, _vp, _i64p],
         "spattn_profile_enable": [_i32],
-        "spattn_selftest_umma": [_vp, _vp, _vp, _vp, _vp, _vp],
+        "spattn_selftest_umma": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
         "spattn_profile_read": [ctypes.POINTER(ctypes.c_double), _i64p],
         "spattn_shard_rows": [_vp, layp, _i32, _i64, _i64, _vp, _vp],
         "spattn_gather_rows": [_vp, layp, _i32, _i64, _i64, _vp, _vp],

@@ -252,13 +252,13 @@ int spattn_get_kernel_family(void) { return seqpar::kernel_family() == seqpar::K
 
 }  // extern "C"
 namespace spattn {
-int umma_selftest(cudaStream_t s, const void* A, const void* B, const void* Bmn, float* D1, float* D2);
+int umma_selftest(cudaStream_t s, const void* A, const void* B, const void* Bmn, float* D1, float* D2, float* D3);
 }
 extern "C" {
 int spattn_selftest_umma(void* stream, const void* a, const void* b, const void* b_mn, float* d1,
-                         float* d2) {
+                         float* d2, float* d3) {
   return guard([&] {
-    if (spattn::umma_selftest(static_cast<cudaStream_t>(stream), a, b, b_mn, d1, d2) != 0)
+    if (spattn::umma_selftest(static_cast<cudaStream_t>(stream), a, b, b_mn, d1, d2, d3) != 0)
       throw seqpar::StateError("umma self-test launch failed");
   });
 }
