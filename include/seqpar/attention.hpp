@@ -5,6 +5,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -93,6 +94,15 @@ void all_to_all(RankCtx& ctx, const CommGroup& group, const void* local, int64_t
 // Event timing of the attention kernels (bench.py): ms[0]/n[0] forward, ms[1]/n[1] backward.
 void profile_enable(bool on);
 void profile_read(double* ms, int64_t* n);
+
+// Host planners behind the engines (exported for multi-process tests of the N>1 logic):
+// per-member query/kv head windows of the head<->sequence moves, and the problem list
+// (q_row0, nq, k_row0, nk, off, causal) two position lists reduce to.
+void plan_head_windows(int heads, int kv_heads, int group, std::vector<int>& qlo,
+                       std::vector<int>& qn, std::vector<int>& kvlo, std::vector<int>& kvn);
+std::vector<std::array<int, 6>> plan_problems(const std::vector<int64_t>& qpos,
+                                              const std::vector<int64_t>& kpos, bool causal,
+                                              const Documents* docs, int64_t* pairs);
 
 // Which attention kernel family the engines launch.
 enum class KernelFamily { tcgen05, mma };

@@ -63,6 +63,17 @@ int spattn_pick_xtuner_insp(int heads, int sp, int head_dim, int* out);
 int spattn_reference_bytes(int engine, int64_t bs, int64_t len, int64_t heads, int64_t head_dim,
                            int sp, int u, int r, int64_t* out);
 
+/* Host planners of the engines (no GPU): per-member head windows of the Ulysses
+ * head<->sequence moves (query heads [q_lo, q_lo+q_n), kv heads [kv_lo, kv_lo+kv_n); dummy
+ * heads are virtual), and the attention problems two position lists reduce to: rows of 6
+ * int32 (q_row0, nq, k_row0, nk, off, causal) where key c is admitted for query a iff
+ * !causal || c <= a + off — the kpos <= qpos rule of attention.cpp:89. */
+int spattn_plan_heads(int heads, int kv_heads, int group, int32_t* q_lo, int32_t* q_n,
+                      int32_t* kv_lo, int32_t* kv_n);
+int spattn_plan_problems(const int64_t* qpos, int64_t lq, const int64_t* kpos, int64_t lk,
+                         int causal, const int64_t* doc_lens, int n_docs, int32_t* out,
+                         int max_problems, int* n_problems, int64_t* pairs);
+
 /* ---- contexts ---- */
 /* NCCL backend: one process per GPU. rank 0 creates the id, the launcher broadcasts it. */
 int spattn_nccl_unique_id(uint8_t out[128]);

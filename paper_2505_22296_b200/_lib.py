@@ -27,7 +27,7 @@ EXPORTS = [
     "spattn_saved_free", "spattn_fabric_fwd", "spattn_fabric_bwd", "spattn_fabric_all_to_all",
     "spattn_block_fwd", "spattn_block_finalize", "spattn_lse_merge", "spattn_block_bwd",
     "spattn_shard_rows", "spattn_gather_rows", "spattn_launch_count", "spattn_profile_enable",
-    "spattn_profile_read", "spattn_selftest_umma",
+    "spattn_profile_read", "spattn_selftest_umma", "spattn_plan_heads", "spattn_plan_problems",
 ]
 
 
@@ -119,6 +119,10 @@ def lib() -> ctypes.CDLL:
         "spattn_block_bwd": [_vp, _i64, _i32, _i32, _i32, _vp, _i64p, _i64, _vp, _vp, _i64p,
                              _i64, _i32, ctypes.c_double, _vp, _vp, _vp, _vp, _vp, _vp, _i64p],
         "spattn_profile_enable": [_i32],
+        "spattn_plan_heads": [_i32, _i32, _i32] + [ctypes.POINTER(ctypes.c_int32)] * 4,
+        "spattn_plan_problems": [_i64p, _i64, _i64p, _i64, _i32, _i64p, _i32,
+                                 ctypes.POINTER(ctypes.c_int32), _i32, ctypes.POINTER(ctypes.c_int),
+                                 _i64p],
         "spattn_selftest_umma": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
         "spattn_profile_read": [ctypes.POINTER(ctypes.c_double), _i64p],
         "spattn_shard_rows": [_vp, layp, _i32, _i64, _i64, _vp, _vp],

@@ -165,6 +165,30 @@ int spattn_reference_bytes(int engine, int64_t bs, int64_t len, int64_t heads, i
   });
 }
 
+int spattn_plan_heads(int heads, int kv_heads, int group, int32_t* q_lo, int32_t* q_n,
+                      int32_t* kv_lo, int32_t* kv_n) {
+  return guard([&] {
+    std::vector<int> a, b, c, d;
+    seqpar::plan_head_windows(heads, kv_heads, group, a, b, c, d);
+    for (int i = 0; i < group; ++i) q_lo[i] = a[i], q_n[i] = b[i], kv_lo[i] = c[i], kv_n[i] = d[i];
+  });
+}
+
+int spattn_plan_problems(const int64_t* qpos, int64_t lq, const int64_t* kpos, int64_t lk,
+                         int causal, const int64_t* doc_lens, int n_docs, int32_t* out,
+                         int max_problems, int* n_problems, int64_t* pairs) {
+  return guard([&] {
+    const auto D = docs_of(doc_lens, n_docs);
+    const auto v = seqpar::plan_problems(std::vector<int64_t>(qpos, qpos + lq),
+                                         std::vector<int64_t>(kpos, kpos + lk), causal != 0,
+                                         D.get(), pairs);
+    if (static_cast<int>(v.size()) > max_problems) throw seqpar::ConfigError("too many problems");
+    for (size_t i = 0; i < v.size(); ++i)
+      for (int j = 0; j < 6; ++j) out[6 * i + j] = v[i][static_cast<size_t>(j)];
+    *n_problems = static_cast<int>(v.size());
+  });
+}
+
 int spattn_nccl_unique_id(uint8_t out[128]) {
   return guard([&] { seqpar::nccl_unique_id(out); });
 }

@@ -18,6 +18,7 @@
 //   * Ulysses writes the gathered rows in natural position order, so the attention kernel sees
 //     contiguous causal runs for any layout.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -846,6 +847,26 @@ CommGroup subgroup(const CommGroup& parent, int from, int count, int stride) {
 }
 
 }  // namespace
+
+// ----------------------------------------------------------- host planners (exported)
+void plan_head_windows(int heads, int kv_heads, int group, std::vector<int>& qlo,
+                       std::vector<int>& qn, std::vector<int>& kvlo, std::vector<int>& kvn) {
+  if (heads <= 0 || kv_heads <= 0 || heads % kv_heads || group <= 0)
+    throw ConfigError("plan_head_windows: invalid heads/kv_heads/group");
+  const HeadPlan p = plan_heads(heads, kv_heads, group);
+  qlo = p.qlo, qn = p.qn, kvlo = p.kvlo, kvn = p.kvn;
+}
+
+std::vector<std::array<int, 6>> plan_problems(const std::vector<int64_t>& qpos,
+                                              const std::vector<int64_t>& kpos, bool causal,
+                                              const Documents* docs, int64_t* pairs) {
+  const auto probs = make_problems(position_runs(qpos), position_runs(kpos), causal, 1,
+                                   static_cast<int64_t>(qpos.size()),
+                                   static_cast<int64_t>(kpos.size()), docs, pairs);
+  std::vector<std::array<int, 6>> out;
+  for (const auto& p : probs) out.push_back({p.q_row0, p.nq, p.k_row0, p.nk, p.off, p.causal});
+  return out;
+}
 
 // =============================================================================== forward
 SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig& cfg,

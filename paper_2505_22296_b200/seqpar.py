@@ -89,6 +89,27 @@ def usp_bytes(bs, len, heads, head_dim, ulysses_degree, ring_degree):
                       ulysses_degree, ring_degree)
 
 
+def plan_heads(heads: int, kv_heads: int, group: int):
+    """Head windows of the Ulysses moves per group member: (q_lo, q_n, kv_lo, kv_n) lists."""
+    arrs = [(ctypes.c_int32 * group)() for _ in range(4)]
+    C.check(C.lib().spattn_plan_heads(heads, kv_heads, group, *arrs))
+    return tuple(list(a) for a in arrs)
+
+
+def plan_problems(qpos, kpos, causal: bool = True, docs=None, max_problems: int = 4096):
+    """Problem list (q_row0, nq, k_row0, nk, off, causal) for two position lists, and the
+    admitted pair count."""
+    qp = (ctypes.c_int64 * len(qpos))(*qpos)
+    kp = (ctypes.c_int64 * len(kpos))(*kpos)
+    nd = 0 if docs is None else len(docs)
+    darr = None if docs is None else (ctypes.c_int64 * nd)(*docs)
+    out = (ctypes.c_int32 * (6 * max_problems))()
+    n, pairs = ctypes.c_int(), _i64()
+    C.check(C.lib().spattn_plan_problems(qp, len(qpos), kp, len(kpos), int(causal), darr, nd, out,
+                                         max_problems, ctypes.byref(n), pairs))
+    return [tuple(out[6 * i:6 * i + 6]) for i in range(n.value)], pairs[0]
+
+
 def set_kernel_family(name: str) -> None:
     """'tcgen05' (default where supported) or 'mma'."""
     C.check(C.lib().spattn_set_kernel_family({"tcgen05": 0, "mma": 1}[name]))
