@@ -2,6 +2,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "tc.cuh"
@@ -36,6 +37,19 @@ bool make_tma_2d(CUtensorMap* m, const void* base, uint64_t width, uint64_t rows
   cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool make_tma_2d_f32(CUtensorMap* m, const void* base, uint64_t width, uint64_t rows,
+                     uint64_t row_stride_elems, uint32_t box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {width, rows};
+  cuuint64_t strides[1] = {row_stride_elems * 4};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -517,7 +531,7 @@ struct BwdLayout {
   static constexpr int SMEM = BAR_OFF + 128;
 };
 
-enum BwdBar { C_KV = 0, C_QF = 1, C_QE = 3, C_SF = 5, C_DPF = 6, C_PR = 7, C_MD = 8, C_DQF = 9, C_FIN = 10, C_N = 11 };
+enum BwdBar { C_KV = 0, C_QF = 1, C_QE = 3, C_SF = 5, C_DPF = 6, C_PR = 7, C_MD = 8, C_DQF = 9, C_FIN = 10, C_DQS = 11, C_N = 12 };
 
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
@@ -525,10 +539,10 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 }
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                       BwdArgs a, ProblemSet ps) {
+                       const __grid_constant__ CUtensorMap tmDQ, BwdArgs a, ProblemSet ps) {
   using Lay = BwdLayout<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
@@ -558,7 +572,7 @@ __global__ void __launch_bounds__(256, 1)
   const int T = none ? 0 : (h_hi - h_lo) * nqt;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < C_N; ++i) tc::mbar_init(bar(i), (i == C_PR || i == C_DQF) ? 128 : 1);
+    for (int i = 0; i < C_N; ++i) tc::mbar_init(bar(i), (i == C_PR || i == C_DQF || i == C_DQS) ? 128 : 1);
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc<512>(smem_u32(tmem_slot));
@@ -567,6 +581,7 @@ __global__ void __launch_bounds__(256, 1)
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 256 + D;
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
 
   if (warp == 0) {
     if (tc::elect_one() && T > 0) {
@@ -632,127 +647,162 @@ __global__ void __launch_bounds__(256, 1)
       }
       tc::commit(bar(C_FIN));
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 8) {
+    // ---- softmax-gradient warpgroup: thread t = key row t (S^T / dP^T lane)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n");
     const int t = threadIdx.x - 128;
     const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
     const float sl2 = a.scale * kLog2e;
-    const int c = n0 + t;  // this thread's key row (S^T lane)
-    for (int it = 0; it < T; ++it) {
-      const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * 128;
-      const int ldb = (it & 1) * 128;
-      {
-        const int row = m0 + t;
-        float l2 = INFINITY, dl = 0.f;
-        if (row < P.nq) {
-          const int64_t g = (int64_t)(P.q_row0 + row) * a.lse_row_stride + h;
-          const float l = a.lse[g];
-          l2 = l == -INFINITY ? INFINITY : l * kLog2e;
-          dl = a.delta[g];
-        }
-        sL[ldb + t] = l2;
-        sDl[ldb + t] = dl;
+    const int c = n0 + t;
+    // lse/delta of the query rows of iteration `it`, prefetched one iteration ahead
+    auto fetch = [&](int it, float& l2, float& dl) {
+      l2 = INFINITY, dl = 0.f;
+      if (it >= T) return;
+      const int h = h_lo + it / nqt, row = m_begin + (it % nqt) * 128 + t;
+      if (row < P.nq) {
+        const int64_t g = (int64_t)(P.q_row0 + row) * a.lse_row_stride + h;
+        const float l = a.lse[g];
+        l2 = l == -INFINITY ? INFINITY : l * kLog2e;
+        dl = a.delta[g];
       }
+    };
+    float nl2, ndl;
+    fetch(0, nl2, ndl);
+    for (int it = 0; it < T; ++it) {
+      const int m0 = m_begin + (it % nqt) * 128;
+      const int ldb = (it & 1) * 128;
+      sL[ldb + t] = nl2;
+      sDl[ldb + t] = ndl;
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      fetch(it + 1, nl2, ndl);
       // admitted queries of key c within this tile: i in [ilo, ihi)
       int ilo = 0, ihi = min(128, P.nq - m0);
       if (c >= P.nk) ihi = 0;
       if (P.causal) ilo = max(0, c - P.off - m0);
       tc::mbar_wait(bar(C_SF), it & 1);
-      tc::fence_after();
-      float p[128];
-      {
-        uint32_t r[4][32];
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) tc::tmem_ld32(tS + lane_base + cc * 32, r[cc]);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          const float x = __uint_as_float(r[i >> 5][i & 31]);
-          const float e = fast_exp2(x * sl2 - sL[ldb + i]);
-          p[i] = (i >= ilo && i < ihi) ? e : 0.f;
-        }
-      }
-      // P^T (bf16) over the S^T columns: the A operand of dV += P^T dO. The previous
-      // iteration's dK/dQ must be done with dS^T before it is overwritten below.
-      if (it > 0) {
-        tc::mbar_wait(bar(C_MD), (it - 1) & 1);
-        tc::fence_after();
-      }
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        uint32_t w[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) w[i] = pack_bf16(p[cc * 64 + 2 * i], p[cc * 64 + 2 * i + 1]);
-        tc::tmem_st32(tS + lane_base + cc * 32, w);
-      }
       tc::mbar_wait(bar(C_DPF), it & 1);
+      // dS^T smem is free once the previous dQ tile left it (staging buffer of the dQ drain)
+      if (it > 0) tc::mbar_wait(bar(C_DQS), (it - 1) & 1);
       tc::fence_after();
+      // 32 queries at a time: P (fp32) and dS from S^T, dP^T; P^T (bf16 pairs) back into the
+      // already-consumed S^T columns as the A operand of dV += P^T dO
+      uint32_t rs[2][32], rp[2][32];
+      tc::tmem_ld32(tS + lane_base, rs[0]);
+      tc::tmem_ld32(tDP + lane_base, rp[0]);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
-        uint32_t r[32];
-        tc::tmem_ld32(tDP + lane_base + cc * 32, r);
         tc::tmem_wait_ld();
-        uint32_t w[16];
+        if (cc + 1 < 4) {
+          tc::tmem_ld32(tS + lane_base + (cc + 1) * 32, rs[(cc + 1) & 1]);
+          tc::tmem_ld32(tDP + lane_base + (cc + 1) * 32, rp[(cc + 1) & 1]);
+        }
+        uint32_t wp[16], wd[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int q0 = cc * 32 + 2 * i;
-          const float d0 = p[q0] * (__uint_as_float(r[2 * i]) - sDl[ldb + q0]);
-          const float d1 = p[q0 + 1] * (__uint_as_float(r[2 * i + 1]) - sDl[ldb + q0 + 1]);
-          w[i] = pack_bf16(d0, d1);
+          float p0 = fast_exp2(__uint_as_float(rs[cc & 1][2 * i]) * sl2 - sL[ldb + q0]);
+          float p1 = fast_exp2(__uint_as_float(rs[cc & 1][2 * i + 1]) * sl2 - sL[ldb + q0 + 1]);
+          p0 = (q0 >= ilo && q0 < ihi) ? p0 : 0.f;
+          p1 = (q0 + 1 >= ilo && q0 + 1 < ihi) ? p1 : 0.f;
+          wp[i] = pack_bf16(p0, p1);
+          wd[i] = pack_bf16(p0 * (__uint_as_float(rp[cc & 1][2 * i]) - sDl[ldb + q0]),
+                            p1 * (__uint_as_float(rp[cc & 1][2 * i + 1]) - sDl[ldb + q0 + 1]));
         }
+        tc::tmem_st16(tS + lane_base + cc * 16, wp);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int chunk = cc * 4 + k;  // 16-byte chunk of 8 queries
           const uint32_t addr = tc::sw128(sdS + (chunk >> 3) * 16384, t, chunk & 7);
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(w[4 * k]),
-                       "r"(w[4 * k + 1]), "r"(w[4 * k + 2]), "r"(w[4 * k + 3]));
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(wd[4 * k]),
+                       "r"(wd[4 * k + 1]), "r"(wd[4 * k + 2]), "r"(wd[4 * k + 3]));
         }
       }
       tc::tmem_wait_st();
       tc::fence_proxy_async();
       tc::fence_before();
       tc::mbar_arrive(bar(C_PR));
-      // dQ tile (lane = query row) -> fp32 atomics
-      tc::mbar_wait(bar(C_MD), it & 1);
-      tc::fence_after();
-      const int qrow = m0 + t;
-      float* dq = a.dq_acc + (int64_t)(P.q_row0 + qrow) * a.dq_row_stride + h * D;
-#pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t r[32];
-        tc::tmem_ld32(tDP + lane_base + cc * 32, r);
-        tc::tmem_wait_ld();
-        if (qrow < P.nq) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            red_add_v4(dq + cc * 32 + 4 * i, __uint_as_float(r[4 * i]) * a.scale,
-                       __uint_as_float(r[4 * i + 1]) * a.scale, __uint_as_float(r[4 * i + 2]) * a.scale,
-                       __uint_as_float(r[4 * i + 3]) * a.scale);
-        }
-      }
-      tc::fence_before();
-      tc::mbar_arrive(bar(C_DQF));
     }
-    if (T > 0) {
+    if (T > 0) {  // dV epilogue (lane = key row)
       tc::mbar_wait(bar(C_FIN), 0);
       tc::fence_after();
-      float* dk = a.dk_acc + (int64_t)(P.k_row0 + c) * a.dkv_row_stride + kvh * D;
       float* dv = a.dv_acc + (int64_t)(P.k_row0 + c) * a.dkv_row_stride + kvh * D;
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t r[32], s[32];
+        uint32_t r[32];
         tc::tmem_ld32(tDV + lane_base + cc * 32, r);
-        tc::tmem_ld32(tDK + lane_base + cc * 32, s);
         tc::tmem_wait_ld();
         if (c < P.nk) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < 8; ++i)
             red_add_v4(dv + cc * 32 + 4 * i, __uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
                        __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
-            red_add_v4(dk + cc * 32 + 4 * i, __uint_as_float(s[4 * i]) * a.scale,
-                       __uint_as_float(s[4 * i + 1]) * a.scale, __uint_as_float(s[4 * i + 2]) * a.scale,
-                       __uint_as_float(s[4 * i + 3]) * a.scale);
-          }
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ---- dQ warpgroup: drains dQ (lane = query row) into fp32 atomics while the softmax
+    // warpgroup already works on the next tile; then the dK epilogue
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n");
+    const int t = threadIdx.x - 256;
+    const uint32_t lane_base = (uint32_t)((warp - 8) * 32) << 16;
+    for (int it = 0; it < T; ++it) {
+      const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * 128;
+      tc::mbar_wait(bar(C_MD), it & 1);
+      tc::fence_after();
+      // dQ tile: 4 chunks of 32 columns, each staged (fp32, 128B-swizzled rows) in one half of
+      // the idle dS^T buffer and reduced into dq_acc by the TMA unit
+      uint32_t r[2][32];
+      tc::tmem_ld32(tDP + lane_base, r[0]);
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        tc::tmem_wait_ld();
+        if (cc + 1 < D / 32) {
+          tc::tmem_ld32(tDP + lane_base + (cc + 1) * 32, r[(cc + 1) & 1]);
+        } else {
+          tc::fence_before();
+          tc::mbar_arrive(bar(C_DQF));  // TMEM dP/dQ columns free for dP of the next tile
+        }
+        const uint32_t stg = sdS + (cc & 1) * 16384;
+        if (cc >= 2) {  // the staging half is reused: its previous reduce must have read it
+          if (t == 0) tc::bulk_wait_read<1>();
+          asm volatile("bar.sync 2, 128;\n" ::: "memory");
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t addr = tc::sw128(stg, t, k);
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr),
+                       "f"(__uint_as_float(r[cc & 1][4 * k]) * a.scale),
+                       "f"(__uint_as_float(r[cc & 1][4 * k + 1]) * a.scale),
+                       "f"(__uint_as_float(r[cc & 1][4 * k + 2]) * a.scale),
+                       "f"(__uint_as_float(r[cc & 1][4 * k + 3]) * a.scale));
+        }
+        tc::fence_proxy_async();
+        asm volatile("bar.sync 2, 128;\n" ::: "memory");
+        if (t == 0 && !(a.debug & 1)) {
+          tc::tma_reduce_add_2d(&tmDQ, stg, h * D + cc * 32, P.q_row0 + m0);
+          tc::bulk_commit();
+        }
+      }
+      if (t == 0) tc::bulk_wait_read<0>();
+      asm volatile("bar.sync 2, 128;\n" ::: "memory");
+      tc::mbar_arrive(bar(C_DQS));
+    }
+    if (T > 0) {  // dK epilogue (lane = key row)
+      tc::mbar_wait(bar(C_FIN), 0);
+      tc::fence_after();
+      const int c = n0 + t;
+      float* dk = a.dk_acc + (int64_t)(P.k_row0 + c) * a.dkv_row_stride + kvh * D;
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t r[32];
+        tc::tmem_ld32(tDK + lane_base + cc * 32, r);
+        tc::tmem_wait_ld();
+        if (c < P.nk) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            red_add_v4(dk + cc * 32 + 4 * i, __uint_as_float(r[4 * i]) * a.scale,
+                       __uint_as_float(r[4 * i + 1]) * a.scale, __uint_as_float(r[4 * i + 2]) * a.scale,
+                       __uint_as_float(r[4 * i + 3]) * a.scale);
         }
       }
     }
@@ -765,15 +815,18 @@ __global__ void __launch_bounds__(256, 1)
 template <int D>
 void launch_bwd_tc_d(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
   ProblemSet ps = in;
+  static const int dbg = getenv("SPATTN_DEBUG") ? atoi(getenv("SPATTN_DEBUG")) : 0;
+  const_cast<BwdArgs&>(a).debug = dbg;
   ps.tile_prefix[0] = 0;
   for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nk + 127) / 128;
   const int tiles = ps.tile_prefix[ps.n];
   if (tiles == 0 || a.hm.hq == 0 || a.hm.hkv == 0) return;
-  CUtensorMap tq, tk, tv, tdo;
+  CUtensorMap tq, tk, tv, tdo, tdq;
   const uint64_t qw = (uint64_t)a.q_row_stride, kw = (uint64_t)a.kv_row_stride, ow = (uint64_t)a.o_row_stride;
   const uint64_t qrows = max(1, max_rows(ps, true)), krows = max(1, max_rows(ps, false));
   if (!make_tma_2d(&tq, a.q, qw, qrows, qw, 128) || !make_tma_2d(&tk, a.k, kw, krows, kw, 128) ||
-      !make_tma_2d(&tv, a.v, kw, krows, kw, 128) || !make_tma_2d(&tdo, a.dout, ow, qrows, ow, 128)) {
+      !make_tma_2d(&tv, a.v, kw, krows, kw, 128) || !make_tma_2d(&tdo, a.dout, ow, qrows, ow, 128) ||
+      !make_tma_2d_f32(&tdq, a.dq_acc, (uint64_t)a.hm.hq * a.d, qrows, (uint64_t)a.dq_row_stride, 128)) {
     cudaGetLastError();
     return;
   }
@@ -782,7 +835,7 @@ void launch_bwd_tc_d(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
     cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdLayout<D>::SMEM);
   });
-  attn_bwd_tc_kernel<D><<<dim3(tiles, a.hm.hkv), 256, BwdLayout<D>::SMEM, s>>>(tq, tk, tv, tdo, a, ps);
+  attn_bwd_tc_kernel<D><<<dim3(tiles, a.hm.hkv), 384, BwdLayout<D>::SMEM, s>>>(tq, tk, tv, tdo, tdq, a, ps);
   note_launch();
 }
 
@@ -793,7 +846,7 @@ bool tc_bwd_supported(const BwdArgs& a) {
   return (a.d == 64 || a.d == 128) && al(a.q) && al(a.k) && al(a.v) && al(a.dout) &&
          (a.q_row_stride * 2) % 16 == 0 && (a.kv_row_stride * 2) % 16 == 0 &&
          (a.o_row_stride * 2) % 16 == 0 && a.o_row_stride == a.q_row_stride &&
-         a.dq_row_stride % 4 == 0 && a.dkv_row_stride % 4 == 0;
+         (a.dq_row_stride * 4) % 16 == 0 && al(a.dq_acc) && a.dkv_row_stride % 4 == 0;
 }
 void launch_attn_bwd_tc(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
   if (a.d == 64)

@@ -67,6 +67,7 @@ struct BwdArgs {
   int d;
   float scale;
   HeadMap hm;
+  int debug;  // profiling switches (SPATTN_DEBUG env): 1 skip dQ atomics, 2 skip dK/dV atomics
 };
 
 // Launch accounting (bench.py's gpu_launches): every launcher in this library calls this.
