@@ -322,21 +322,20 @@ __global__ void __launch_bounds__(256, 1)
       tc::mbar_arrive(bar(B_SFREE + st));
       const int n0 = j * 128;
       const bool need_mask = (n0 + 128 > P.nk) || (P.causal && n0 + 127 > m0 + P.off);
+      // max over raw scores (sl2 > 0); the scale is folded into the exponent's FFMA below
       float mt = -INFINITY;
       if (need_mask) {
         const int lim = P.causal ? min(P.nk - 1, qa + P.off) - n0 : P.nk - 1 - n0;
 #pragma unroll
         for (int i = 0; i < 128; ++i) {
-          x[i] = i <= lim ? x[i] * sl2 : -INFINITY;
+          x[i] = i <= lim ? x[i] : -INFINITY;
           mt = fmaxf(mt, x[i]);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          x[i] *= sl2;
-          mt = fmaxf(mt, x[i]);
-        }
+        for (int i = 0; i < 128; ++i) mt = fmaxf(mt, x[i]);
       }
+      mt *= sl2;
       if (j == 0) {
         m_run = mt;
       } else if (__any_sync(0xffffffffu, mt > m_run + 8.f)) {
@@ -369,8 +368,8 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float p0 = fast_exp2(x[ch * 8 + 2 * e] - muse);
-          const float p1 = fast_exp2(x[ch * 8 + 2 * e + 1] - muse);
+          const float p0 = fast_exp2(fmaf(x[ch * 8 + 2 * e], sl2, -muse));
+          const float p1 = fast_exp2(fmaf(x[ch * 8 + 2 * e + 1], sl2, -muse));
           rs += p0 + p1;
           w[e] = pack_bf16(p0, p1);
         }
@@ -531,7 +530,7 @@ struct BwdLayout {
   static constexpr int SMEM = BAR_OFF + 128;
 };
 
-enum BwdBar { C_KV = 0, C_QF = 1, C_QE = 3, C_SF = 5, C_DPF = 6, C_PR = 7, C_MD = 8, C_DQF = 9, C_FIN = 10, C_DQS = 11, C_N = 12 };
+enum BwdBar { C_KV = 0, C_QF = 1, C_QE = 3, C_SF = 5, C_DPF = 6, C_PR = 7, C_MD = 8, C_DQF = 9, C_FIN = 10, C_DQS = 11, C_N = 13 };
 
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
@@ -572,7 +571,7 @@ __global__ void __launch_bounds__(384, 1)
   const int T = none ? 0 : (h_hi - h_lo) * nqt;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < C_N; ++i) tc::mbar_init(bar(i), (i == C_PR || i == C_DQF || i == C_DQS) ? 128 : 1);
+    for (int i = 0; i < C_N; ++i) tc::mbar_init(bar(i), (i == C_PR || i == C_DQF || i == C_DQS || i == C_DQS + 1) ? 128 : 1);
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc<512>(smem_u32(tmem_slot));
@@ -593,7 +592,10 @@ __global__ void __launch_bounds__(384, 1)
       for (int it = 0; it < T; ++it) {
         const int st = it & 1;
         const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * 128;
-        if (it >= 2) tc::mbar_wait(bar(C_QE + st), ((it - 2) >> 1) & 1);
+        if (it >= 2) {
+          tc::mbar_wait(bar(C_QE + st), ((it - 2) >> 1) & 1);
+          tc::mbar_wait(bar(C_DQS + st), ((it - 2) >> 1) & 1);  // dQ tile it-2 staged here
+        }
         tc::mbar_expect_tx(bar(C_QF + st), 2 * Lay::TILE);
         for (int b = 0; b < Lay::QB; ++b) {
           tc::tma_load_2d(sQ + st * Lay::TILE + b * 16384, &tmQ, h * D + b * 64, P.q_row0 + m0, bar(C_QF + st));
@@ -655,58 +657,56 @@ __global__ void __launch_bounds__(384, 1)
     const float sl2 = a.scale * kLog2e;
     const int c = n0 + t;
     // lse/delta of the query rows of iteration `it`, prefetched one iteration ahead
-    auto fetch = [&](int it, float& l2, float& dl) {
-      l2 = INFINITY, dl = 0.f;
+    auto fetch = [&](int it, float& l, float& dl) {
+      l = -INFINITY, dl = 0.f;
       if (it >= T) return;
       const int h = h_lo + it / nqt, row = m_begin + (it % nqt) * 128 + t;
       if (row < P.nq) {
         const int64_t g = (int64_t)(P.q_row0 + row) * a.lse_row_stride + h;
-        const float l = a.lse[g];
-        l2 = l == -INFINITY ? INFINITY : l * kLog2e;
-        dl = a.delta[g];
+        l = __ldg(a.lse + g);
+        dl = __ldg(a.delta + g);
       }
     };
-    float nl2, ndl;
-    fetch(0, nl2, ndl);
+    float nl, ndl;
+    fetch(0, nl, ndl);
     for (int it = 0; it < T; ++it) {
       const int m0 = m_begin + (it % nqt) * 128;
       const int ldb = (it & 1) * 128;
-      sL[ldb + t] = nl2;
+      sL[ldb + t] = nl == -INFINITY ? INFINITY : nl * kLog2e;  // empty row: p = 0
       sDl[ldb + t] = ndl;
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      fetch(it + 1, nl2, ndl);
+      fetch(it + 1, nl, ndl);
       // admitted queries of key c within this tile: i in [ilo, ihi)
       int ilo = 0, ihi = min(128, P.nq - m0);
       if (c >= P.nk) ihi = 0;
       if (P.causal) ilo = max(0, c - P.off - m0);
       tc::mbar_wait(bar(C_SF), it & 1);
       tc::mbar_wait(bar(C_DPF), it & 1);
-      // dS^T smem is free once the previous dQ tile left it (staging buffer of the dQ drain)
-      if (it > 0) tc::mbar_wait(bar(C_DQS), (it - 1) & 1);
+      // dS^T smem is free once the previous tile's dK/dQ MMAs are done with it
+      if (it > 0) tc::mbar_wait(bar(C_MD), (it - 1) & 1);
       tc::fence_after();
+      const bool full = ilo <= 0 && ihi >= 128;
       // 32 queries at a time: P (fp32) and dS from S^T, dP^T; P^T (bf16 pairs) back into the
       // already-consumed S^T columns as the A operand of dV += P^T dO
-      uint32_t rs[2][32], rp[2][32];
-      tc::tmem_ld32(tS + lane_base, rs[0]);
-      tc::tmem_ld32(tDP + lane_base, rp[0]);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
+        uint32_t rs[32], rp[32];
+        tc::tmem_ld32(tS + lane_base + cc * 32, rs);
+        tc::tmem_ld32(tDP + lane_base + cc * 32, rp);
         tc::tmem_wait_ld();
-        if (cc + 1 < 4) {
-          tc::tmem_ld32(tS + lane_base + (cc + 1) * 32, rs[(cc + 1) & 1]);
-          tc::tmem_ld32(tDP + lane_base + (cc + 1) * 32, rp[(cc + 1) & 1]);
-        }
         uint32_t wp[16], wd[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int q0 = cc * 32 + 2 * i;
-          float p0 = fast_exp2(__uint_as_float(rs[cc & 1][2 * i]) * sl2 - sL[ldb + q0]);
-          float p1 = fast_exp2(__uint_as_float(rs[cc & 1][2 * i + 1]) * sl2 - sL[ldb + q0 + 1]);
-          p0 = (q0 >= ilo && q0 < ihi) ? p0 : 0.f;
-          p1 = (q0 + 1 >= ilo && q0 + 1 < ihi) ? p1 : 0.f;
+          float p0 = fast_exp2(fmaf(__uint_as_float(rs[2 * i]), sl2, -sL[ldb + q0]));
+          float p1 = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), sl2, -sL[ldb + q0 + 1]));
+          if (!full) {
+            p0 = (q0 >= ilo && q0 < ihi) ? p0 : 0.f;
+            p1 = (q0 + 1 >= ilo && q0 + 1 < ihi) ? p1 : 0.f;
+          }
           wp[i] = pack_bf16(p0, p1);
-          wd[i] = pack_bf16(p0 * (__uint_as_float(rp[cc & 1][2 * i]) - sDl[ldb + q0]),
-                            p1 * (__uint_as_float(rp[cc & 1][2 * i + 1]) - sDl[ldb + q0 + 1]));
+          wd[i] = pack_bf16(p0 * (__uint_as_float(rp[2 * i]) - sDl[ldb + q0]),
+                            p1 * (__uint_as_float(rp[2 * i + 1]) - sDl[ldb + q0 + 1]));
         }
         tc::tmem_st16(tS + lane_base + cc * 16, wp);
 #pragma unroll
@@ -750,7 +750,8 @@ __global__ void __launch_bounds__(384, 1)
       tc::mbar_wait(bar(C_MD), it & 1);
       tc::fence_after();
       // dQ tile: 4 chunks of 32 columns, each staged (fp32, 128B-swizzled rows) in one half of
-      // the idle dS^T buffer and reduced into dq_acc by the TMA unit
+      // this iteration's dO buffer (dead once dV/dK are done; the producer refills it only after
+      // the drain) and reduced into dq_acc by the TMA unit
       uint32_t r[2][32];
       tc::tmem_ld32(tDP + lane_base, r[0]);
 #pragma unroll
@@ -762,9 +763,11 @@ __global__ void __launch_bounds__(384, 1)
           tc::fence_before();
           tc::mbar_arrive(bar(C_DQF));  // TMEM dP/dQ columns free for dP of the next tile
         }
-        const uint32_t stg = sdS + (cc & 1) * 16384;
-        if (cc >= 2) {  // the staging half is reused: its previous reduce must have read it
-          if (t == 0) tc::bulk_wait_read<1>();
+        // staging slots of 16 KB (128 rows x 32 fp32): two for D=128, one for D=64
+        constexpr int NSTG = Lay::TILE / 16384;
+        const uint32_t stg = sdO + (it & 1) * Lay::TILE + (cc % NSTG) * 16384;
+        if (cc >= NSTG) {  // the slot is reused: its previous reduce must have read it
+          if (t == 0) tc::bulk_wait_read<NSTG - 1>();
           asm volatile("bar.sync 2, 128;\n" ::: "memory");
         }
 #pragma unroll
@@ -785,7 +788,7 @@ __global__ void __launch_bounds__(384, 1)
       }
       if (t == 0) tc::bulk_wait_read<0>();
       asm volatile("bar.sync 2, 128;\n" ::: "memory");
-      tc::mbar_arrive(bar(C_DQS));
+      tc::mbar_arrive(bar(C_DQS + (it & 1)));
     }
     if (T > 0) {  // dK epilogue (lane = key row)
       tc::mbar_wait(bar(C_FIN), 0);
