@@ -136,6 +136,7 @@ class LoopbackFabric {
   bool abort_ = false;
   std::vector<std::unique_ptr<Transport>> transports_;
   std::vector<std::unique_ptr<RankCtx>> ctxs_;
+  std::vector<cudaStream_t> own_streams_;
 };
 
 // One process per GPU; NCCL loaded at run time (libnccl.so.2, the copy torch already mapped).

@@ -126,16 +126,19 @@ LoopbackFabric::LoopbackFabric(int world, int sp, int device, bool force_message
     c->sp_group = sp_group_of(r);
     SP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     SP_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    own_streams_.push_back(c->stream);
+    own_streams_.push_back(c->comm_stream);
     ctxs_.push_back(std::move(c));
   }
 }
 
 LoopbackFabric::~LoopbackFabric() {
-  for (auto& c : ctxs_) {
-    cudaStreamSynchronize(c->stream);
-    cudaStreamSynchronize(c->comm_stream);
-    cudaStreamDestroy(c->stream);
-    cudaStreamDestroy(c->comm_stream);
+  // only the streams this fabric created: a context's compute stream may have been replaced by
+  // the caller's (spattn_ctx_set_stream) and is not ours to destroy
+  for (auto& c : ctxs_) cudaStreamSynchronize(c->stream);
+  for (cudaStream_t s : own_streams_) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
   }
 }
 
