@@ -1,0 +1,361 @@
+// tcgen05 attention backward for head_dim 128 with 64-row query tiles (sm_100a).
+//
+// One CTA = one 128-row key/value tile x one kv head; it loops over every (query head of the
+// GQA group, 64-row query tile) that sees the tile. TMEM (512 columns, lane = key row unless
+// noted) is double-buffered per query tile so the softmax-gradient math of tile i overlaps the
+// dV/dK/dQ MMAs of tile i-1:
+//   S^T_b  = K Q^T          cols [64b, 64b+64)        P^T_b (bf16) written back over it
+//   dP^T_b = V dO^T         cols [128+64b, +64)        dQ^T_b (lane = head-dim index) reuses it
+//   dV    += P^T_b dO       cols [256, 384)            (A operand from TMEM)
+//   dK    += dS^T_b Q       cols [384, 512)            (dS^T from swizzled smem)
+//   dQ^T_b = K^T dS^T_b     M = head dim 128, N = 64 queries, K = 128 keys
+// MMA issue order: S(i), dP(i), [dV dK dQ](i-1), S(i+1), ... The dQ warpgroup drains dQ^T
+// (warp w owns head-dim columns 32w..32w+31) through an 8 KB smem slot per warp into the fp32
+// accumulator with TMA reduce-add. attn_block_backward (attention.cpp:167-216).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <mutex>
+
+#include "tc.cuh"
+
+namespace spattn {
+namespace {
+
+constexpr int D = 128;
+constexpr int BQ = 64;
+constexpr int NST = 3;                      // Q/dO pipeline stages
+constexpr int KV_TILE = 128 * D * 2;        // 32 KB (two 16 KB column blocks)
+constexpr int Q_TILE = BQ * D * 2;          // 16 KB (two 8 KB column blocks)
+constexpr int K_OFF = 0, V_OFF = KV_TILE;
+constexpr int Q_OFF = 2 * KV_TILE;          // NST x Q tile
+constexpr int DO_OFF = Q_OFF + NST * Q_TILE;
+constexpr int DS_OFF = DO_OFF + NST * Q_TILE;    // 2 x [128 keys x 64 queries] bf16 (16 KB each)
+constexpr int STG_OFF = DS_OFF + 2 * 16384;      // 4 warps x [64 queries x 32 fp32] (8 KB each)
+constexpr int LD_OFF = STG_OFF + 4 * 8192;       // lse*log2e, delta: [2][64] each
+constexpr int BAR_OFF = LD_OFF + 4 * 64 * 4;
+
+enum {
+  E_KV = 0,
+  E_QF = 1,                 // [NST]
+  E_QE = E_QF + NST,        // [NST]
+  E_SF = E_QE + NST,        // [2]
+  E_DPF = E_SF + 2,         // [2]
+  E_PR = E_DPF + 2,         // [2] 128 arrivals
+  E_MD = E_PR + 2,          // [2]
+  E_DQF = E_MD + 2,         // [2] 128 arrivals
+  E_FIN = E_DQF + 2,
+  E_N = E_FIN + 1
+};
+constexpr int SMEM = BAR_OFF + E_N * 8 + 16;
+
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_tc_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                           const __grid_constant__ CUtensorMap tmDQ, BwdArgs a, ProblemSet ps) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  if (sbase & 1023) __trap();
+  const uint32_t sK = sbase + K_OFF, sV = sbase + V_OFF, sQ = sbase + Q_OFF, sdO = sbase + DO_OFF,
+                 sdS = sbase + DS_OFF, sStg = sbase + STG_OFF;
+  float* sL = reinterpret_cast<float*>(smem + LD_OFF);  // [2][64]
+  float* sDl = sL + 128;                                // [2][64]
+  const uint32_t bars = sbase + BAR_OFF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + BAR_OFF + E_N * 8);
+  auto bar = [&](int i) { return bars + 8u * i; };
+
+  const int warp = threadIdx.x / 32;
+  int pi = 0;
+  while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= (int)blockIdx.x) ++pi;
+  const AttnProblem P = ps.p[pi];
+  const int n0 = (blockIdx.x - ps.tile_prefix[pi]) * 128;
+  const int kvh = blockIdx.y;
+  const HeadMap hm = a.hm;
+  const int g_lo = (kvh + hm.kv_head_base) * hm.rep;
+  const int h_lo = max(0, g_lo - hm.q_head_base);
+  const int h_hi = min(hm.hq, g_lo + hm.rep - hm.q_head_base);
+  int m_begin = 0;
+  if (P.causal) m_begin = max(0, n0 - P.off) / BQ * BQ;
+  const bool none = (P.causal && n0 - P.off > P.nq - 1) || h_hi <= h_lo || m_begin >= P.nq;
+  const int nqt = none ? 0 : (P.nq - m_begin + BQ - 1) / BQ;
+  const int T = none ? 0 : (h_hi - h_lo) * nqt;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < E_N; ++i) {
+      const bool many = (i >= E_PR && i < E_PR + 2) || (i >= E_DQF && i < E_DQF + 2);
+      tc::mbar_init(bar(i), many ? 128 : 1);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc<512>(smem_u32(tmem_slot));
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDV = tmem + 256, tDK = tmem + 384;
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (tc::elect_one() && T > 0) {
+      tc::mbar_expect_tx(bar(E_KV), 2 * KV_TILE);
+      for (int b = 0; b < 2; ++b) {
+        tc::tma_load_2d(sK + b * 16384, &tmK, kvh * D + b * 64, P.k_row0 + n0, bar(E_KV));
+        tc::tma_load_2d(sV + b * 16384, &tmV, kvh * D + b * 64, P.k_row0 + n0, bar(E_KV));
+      }
+      for (int it = 0; it < T; ++it) {
+        const int st = it % NST;
+        const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * BQ;
+        if (it >= NST) tc::mbar_wait(bar(E_QE + st), ((it - NST) / NST) & 1);
+        tc::mbar_expect_tx(bar(E_QF + st), 2 * Q_TILE);
+        for (int b = 0; b < 2; ++b) {
+          tc::tma_load_2d(sQ + st * Q_TILE + b * 8192, &tmQ, h * D + b * 64, P.q_row0 + m0, bar(E_QF + st));
+          tc::tma_load_2d(sdO + st * Q_TILE + b * 8192, &tmDO, h * D + b * 64, P.q_row0 + m0, bar(E_QF + st));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------------- MMA issuer
+    if (tc::elect_one() && T > 0) {
+      constexpr uint32_t id_s = tc::idesc_bf16(128, BQ, false, false);  // S^T, dP^T
+      constexpr uint32_t id_kv = tc::idesc_bf16(128, D, false, true);   // dV, dK
+      constexpr uint32_t id_q = tc::idesc_bf16(128, BQ, true, true);    // dQ^T
+      auto tail = [&](int i) {  // dV, dK, dQ^T of iteration i
+        const int b = i & 1, st = i % NST;
+        const uint32_t q = sQ + st * Q_TILE, dO = sdO + st * Q_TILE, ds = sdS + b * 16384;
+        tc::mbar_wait(bar(E_PR + b), (i >> 1) & 1);
+        tc::fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BQ / 16; ++kk)
+          tc::mma_ts(tDV, tmem + 64 * b + kk * 8, tc::sdesc(dO + kk * 2048, 8192, 1024), id_kv,
+                     (i > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < BQ / 16; ++kk)
+          tc::mma_ss(tDK, tc::sdesc(ds + kk * 32, 16, 1024), tc::sdesc(q + kk * 2048, 8192, 1024), id_kv,
+                     (i > 0 || kk > 0) ? 1u : 0u);
+        tc::commit(bar(E_QE + st));
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          tc::mma_ss(tmem + 128 + 64 * b, tc::sdesc(sK + kk * 2048, 16384, 1024),
+                     tc::sdesc(ds + kk * 2048, 8192, 1024), id_q, kk > 0 ? 1u : 0u);
+        tc::commit(bar(E_MD + b));
+      };
+      tc::mbar_wait(bar(E_KV), 0);
+      for (int it = 0; it < T; ++it) {
+        const int b = it & 1, st = it % NST;
+        const uint32_t q = sQ + st * Q_TILE, dO = sdO + st * Q_TILE;
+        tc::mbar_wait(bar(E_QF + st), (it / NST) & 1);
+        tc::fence_after();
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t ko = (ks >> 2) * 16384 + (ks & 3) * 32, qo = (ks >> 2) * 8192 + (ks & 3) * 32;
+          tc::mma_ss(tmem + 64 * b, tc::sdesc(sK + ko, 16, 1024), tc::sdesc(q + qo, 16, 1024), id_s, ks > 0);
+        }
+        tc::commit(bar(E_SF + b));
+        if (it >= 2) {  // dQ^T of it-2 (same columns) must be drained
+          tc::mbar_wait(bar(E_DQF + b), ((it - 2) >> 1) & 1);
+          tc::fence_after();
+        }
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t ko = (ks >> 2) * 16384 + (ks & 3) * 32, qo = (ks >> 2) * 8192 + (ks & 3) * 32;
+          tc::mma_ss(tmem + 128 + 64 * b, tc::sdesc(sV + ko, 16, 1024), tc::sdesc(dO + qo, 16, 1024), id_s,
+                     ks > 0);
+        }
+        tc::commit(bar(E_DPF + b));
+        if (it >= 1) tail(it - 1);
+      }
+      tail(T - 1);
+      tc::commit(bar(E_FIN));
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ----------------------------------------------- softmax-gradient warpgroup (lane = key)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
+    const int t = threadIdx.x - 128;
+    const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
+    const float sl2 = a.scale * kLog2e;
+    const int c = n0 + t;
+    float nl = -INFINITY, ndl = 0.f;
+    auto fetch = [&](int it) {
+      nl = -INFINITY, ndl = 0.f;
+      if (it >= T || t >= BQ) return;
+      const int h = h_lo + it / nqt, row = m_begin + (it % nqt) * BQ + t;
+      if (row < P.nq) {
+        const int64_t g = (int64_t)(P.q_row0 + row) * a.lse_row_stride + h;
+        nl = __ldg(a.lse + g);
+        ndl = __ldg(a.delta + g);
+      }
+    };
+    fetch(0);
+    for (int it = 0; it < T; ++it) {
+      const int b = it & 1;
+      const int m0 = m_begin + (it % nqt) * BQ;
+      if (t < BQ) {
+        sL[b * 64 + t] = nl == -INFINITY ? INFINITY : nl * kLog2e;
+        sDl[b * 64 + t] = ndl;
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      fetch(it + 1);
+      int ilo = 0, ihi = min(BQ, P.nq - m0);
+      if (c >= P.nk) ihi = 0;
+      if (P.causal) ilo = max(0, c - P.off - m0);
+      const bool full = ilo <= 0 && ihi >= BQ;
+      tc::mbar_wait(bar(E_SF + b), (it >> 1) & 1);
+      tc::mbar_wait(bar(E_DPF + b), (it >> 1) & 1);
+      if (it >= 2) tc::mbar_wait(bar(E_MD + b), ((it - 2) >> 1) & 1);  // dS^T_b read by dK/dQ
+      tc::fence_after();
+      const uint32_t ds = sdS + b * 16384;
+#pragma unroll
+      for (int cc = 0; cc < BQ / 32; ++cc) {
+        uint32_t rs[32], rp[32];
+        tc::tmem_ld32(tmem + lane_base + 64 * b + cc * 32, rs);
+        tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + cc * 32, rp);
+        tc::tmem_wait_ld();
+        uint32_t wp[16], wd[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int q0 = cc * 32 + 2 * i;
+          float p0 = fast_exp2(fmaf(__uint_as_float(rs[2 * i]), sl2, -sL[b * 64 + q0]));
+          float p1 = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), sl2, -sL[b * 64 + q0 + 1]));
+          if (!full) {
+            p0 = (q0 >= ilo && q0 < ihi) ? p0 : 0.f;
+            p1 = (q0 + 1 >= ilo && q0 + 1 < ihi) ? p1 : 0.f;
+          }
+          wp[i] = pack_bf16(p0, p1);
+          wd[i] = pack_bf16(p0 * (__uint_as_float(rp[2 * i]) - sDl[b * 64 + q0]),
+                            p1 * (__uint_as_float(rp[2 * i + 1]) - sDl[b * 64 + q0 + 1]));
+        }
+        tc::tmem_st16(tmem + lane_base + 64 * b + cc * 16, wp);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t addr = tc::sw128(ds, t, cc * 4 + k);
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(wd[4 * k]),
+                       "r"(wd[4 * k + 1]), "r"(wd[4 * k + 2]), "r"(wd[4 * k + 3]));
+        }
+      }
+      tc::tmem_wait_st();
+      tc::fence_proxy_async();
+      tc::fence_before();
+      tc::mbar_arrive(bar(E_PR + b));
+    }
+    if (T > 0) {  // dV epilogue
+      tc::mbar_wait(bar(E_FIN), 0);
+      tc::fence_after();
+      float* dv = a.dv_acc + (int64_t)(P.k_row0 + c) * a.dkv_row_stride + kvh * D;
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t r[32];
+        tc::tmem_ld32(tDV + lane_base + cc * 32, r);
+        tc::tmem_wait_ld();
+        if (c < P.nk) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            red_add_v4(dv + cc * 32 + 4 * i, __uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                       __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------- dQ warpgroup (lane = head-dim index)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 120;\n");
+    const int w = warp - 8, lane = threadIdx.x % 32;
+    const uint32_t lane_base = (uint32_t)(w * 32) << 16;
+    const uint32_t stg = sStg + w * 8192;  // [64 queries x 32 fp32], 128B-swizzled rows
+    for (int it = 0; it < T; ++it) {
+      const int b = it & 1;
+      const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * BQ;
+      tc::mbar_wait(bar(E_MD + b), (it >> 1) & 1);
+      tc::fence_after();
+      uint32_t r[2][32];
+      tc::tmem_ld32(tmem + lane_base + 128 + 64 * b, r[0]);
+      tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, r[1]);
+      tc::tmem_wait_ld();
+      tc::fence_before();
+      tc::mbar_arrive(bar(E_DQF + b));
+      if (!(a.debug & 1)) {
+        // coalesced fp32 reduce-add straight from registers: for each query row the warp's 32
+        // lanes cover 32 consecutive head-dim columns (one 128-byte line)
+        float* dq = a.dq_acc + (int64_t)(P.q_row0 + m0) * a.dq_row_stride + h * D + w * 32 + lane;
+        const int qn = min(BQ, P.nq - m0);
+#pragma unroll
+        for (int qq = 0; qq < BQ; ++qq)
+          if (qq < qn)
+            asm volatile("red.global.add.f32 [%0], %1;\n" ::"l"(dq + (int64_t)qq * a.dq_row_stride),
+                         "f"(__uint_as_float(r[qq >> 5][qq & 31]) * a.scale)
+                         : "memory");
+      }
+    }
+    (void)stg;
+    if (T > 0) {  // dK epilogue (lane = key row)
+      tc::mbar_wait(bar(E_FIN), 0);
+      tc::fence_after();
+      const int c = n0 + w * 32 + lane;
+      float* dk = a.dk_acc + (int64_t)(P.k_row0 + c) * a.dkv_row_stride + kvh * D;
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t r[32];
+        tc::tmem_ld32(tDK + lane_base + cc * 32, r);
+        tc::tmem_wait_ld();
+        if (c < P.nk) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            red_add_v4(dk + cc * 32 + 4 * i, __uint_as_float(r[4 * i]) * a.scale,
+                       __uint_as_float(r[4 * i + 1]) * a.scale, __uint_as_float(r[4 * i + 2]) * a.scale,
+                       __uint_as_float(r[4 * i + 3]) * a.scale);
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 2) tc::tmem_dealloc<512>(tmem);
+}
+
+int max_rows(const ProblemSet& ps, bool q) {
+  int m = 0;
+  for (int i = 0; i < ps.n; ++i) m = max(m, q ? ps.p[i].q_row0 + ps.p[i].nq : ps.p[i].k_row0 + ps.p[i].nk);
+  return m;
+}
+
+}  // namespace
+
+bool tc_bwd_q64_supported(const BwdArgs& a) {
+  auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+  return a.d == D && al(a.q) && al(a.k) && al(a.v) && al(a.dout) && al(a.dq_acc) &&
+         (a.q_row_stride * 2) % 16 == 0 && (a.kv_row_stride * 2) % 16 == 0 &&
+         a.o_row_stride == a.q_row_stride && (a.dq_row_stride * 4) % 16 == 0 && a.dkv_row_stride % 4 == 0;
+}
+
+void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
+  ProblemSet ps = in;
+  static const int dbg = getenv("SPATTN_DEBUG") ? atoi(getenv("SPATTN_DEBUG")) : 0;
+  BwdArgs args = a;
+  args.debug = dbg;
+  ps.tile_prefix[0] = 0;
+  for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nk + 127) / 128;
+  const int tiles = ps.tile_prefix[ps.n];
+  if (tiles == 0 || a.hm.hq == 0 || a.hm.hkv == 0) return;
+  CUtensorMap tq, tk, tv, tdo, tdq;
+  const uint64_t qw = (uint64_t)a.q_row_stride, kw = (uint64_t)a.kv_row_stride;
+  const uint64_t qrows = max(1, max_rows(ps, true)), krows = max(1, max_rows(ps, false));
+  if (!make_tma_2d(&tq, a.q, qw, qrows, qw, BQ) || !make_tma_2d(&tk, a.k, kw, krows, kw, 128) ||
+      !make_tma_2d(&tv, a.v, kw, krows, kw, 128) || !make_tma_2d(&tdo, a.dout, qw, qrows, qw, BQ) ||
+      !make_tma_2d_f32(&tdq, a.dq_acc, (uint64_t)a.hm.hq * D, qrows, (uint64_t)a.dq_row_stride, BQ)) {
+    cudaGetLastError();
+    return;
+  }
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(attn_bwd_tc_q64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  });
+  attn_bwd_tc_q64_kernel<<<dim3(tiles, a.hm.hkv), 384, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
+  note_launch();
+}
+
+}  // namespace spattn

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -238,8 +239,14 @@ void launch_attn_fwd(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
   else
     launch_attn_fwd_mma(a, ps, s);
 }
+bool tc_bwd_q64_supported(const BwdArgs& a);
+void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
+
 void launch_attn_bwd(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
-  if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && tc_bwd_supported(a))
+  static const bool use_q64 = !getenv("SPATTN_BWD_Q128");
+  if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && use_q64 && tc_bwd_q64_supported(a))
+    launch_attn_bwd_tc_q64(a, ps, s);
+  else if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && tc_bwd_supported(a))
     launch_attn_bwd_tc(a, ps, s);
   else
     launch_attn_bwd_mma(a, ps, s);
