@@ -99,6 +99,9 @@ int spattn_get_kernel_family(void);
 /* Diagnostics for the bench: number of kernels this library has launched, and CUDA-event
  * timing of the attention kernels (fwd: ms[0], n[0]; bwd: ms[1], n[1]) since enabling. */
 int64_t spattn_launch_count(void);
+/* Profiling: per-iteration clock64 event trace of backward CTA (0,0) into a device buffer of
+ * 16 int64 per iteration (NULL disables). */
+int spattn_debug_bwd_trace(void* device_buffer);
 int spattn_profile_enable(int on);
 int spattn_profile_read(double ms[2], int64_t n[2]);
 

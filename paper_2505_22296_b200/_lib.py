@@ -28,6 +28,7 @@ EXPORTS = [
     "spattn_block_fwd", "spattn_block_finalize", "spattn_lse_merge", "spattn_block_bwd",
     "spattn_shard_rows", "spattn_gather_rows", "spattn_launch_count", "spattn_profile_enable",
     "spattn_profile_read", "spattn_selftest_umma", "spattn_plan_heads", "spattn_plan_problems",
+    "spattn_debug_bwd_trace",
 ]
 
 
@@ -119,6 +120,7 @@ def lib() -> ctypes.CDLL:
         "spattn_block_bwd": [_vp, _i64, _i32, _i32, _i32, _vp, _i64p, _i64, _vp, _vp, _i64p,
                              _i64, _i32, ctypes.c_double, _vp, _vp, _vp, _vp, _vp, _vp, _i64p],
         "spattn_profile_enable": [_i32],
+        "spattn_debug_bwd_trace": [_vp],
         "spattn_plan_heads": [_i32, _i32, _i32] + [ctypes.POINTER(ctypes.c_int32)] * 4,
         "spattn_plan_problems": [_i64p, _i64, _i64p, _i64, _i32, _i64p, _i32,
                                  ctypes.POINTER(ctypes.c_int32), _i32, ctypes.POINTER(ctypes.c_int),

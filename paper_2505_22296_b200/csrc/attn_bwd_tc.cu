@@ -33,8 +33,8 @@ constexpr int Q_OFF = 2 * KV_TILE;          // NST x Q tile
 constexpr int DO_OFF = Q_OFF + NST * Q_TILE;
 constexpr int DS_OFF = DO_OFF + NST * Q_TILE;    // 2 x [128 keys x 64 queries] bf16 (16 KB each)
 constexpr int STG_OFF = DS_OFF + 2 * 16384;      // 4 warps x [64 queries x 32 fp32] (8 KB each)
-constexpr int LD_OFF = STG_OFF + 4 * 8192;       // lse*log2e, delta: [2][64] each
-constexpr int BAR_OFF = LD_OFF + 4 * 64 * 4;
+constexpr int LD_OFF = STG_OFF + 4 * 8192;       // lse*log2e, delta: [NST][64] each
+constexpr int BAR_OFF = LD_OFF + 2 * NST * 64 * 4;
 
 enum {
   E_KV = 0,
@@ -64,19 +64,24 @@ __global__ void __launch_bounds__(384, 1)
   if (sbase & 1023) __trap();
   const uint32_t sK = sbase + K_OFF, sV = sbase + V_OFF, sQ = sbase + Q_OFF, sdO = sbase + DO_OFF,
                  sdS = sbase + DS_OFF, sStg = sbase + STG_OFF;
-  float* sL = reinterpret_cast<float*>(smem + LD_OFF);  // [2][64]
-  float* sDl = sL + 128;                                // [2][64]
+  float* sL = reinterpret_cast<float*>(smem + LD_OFF);  // [NST][64] lse * log2e (+inf: empty row)
+  float* sDl = sL + NST * 64;                           // [NST][64] delta
   const uint32_t bars = sbase + BAR_OFF;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + BAR_OFF + E_N * 8);
   auto bar = [&](int i) { return bars + 8u * i; };
 
   const int warp = threadIdx.x / 32;
-  int pi = 0;
-  while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= (int)blockIdx.x) ++pi;
-  const AttnProblem P = ps.p[pi];
-  const int n0 = (blockIdx.x - ps.tile_prefix[pi]) * 128;
-  const int kvh = blockIdx.y;
+  long long* trace = (a.trace && blockIdx.x == 0) ? a.trace : nullptr;
+#define TR(slot, it) \
+  if (trace) trace[(it) * 16 + (slot)] = clock64()
+  // 1-D grid, kv head fastest: the heaviest causal key tiles of every head run first (LPT)
   const HeadMap hm = a.hm;
+  const int tile = blockIdx.x / hm.hkv;
+  const int kvh = blockIdx.x % hm.hkv;
+  int pi = 0;
+  while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= tile) ++pi;
+  const AttnProblem P = ps.p[pi];
+  const int n0 = (tile - ps.tile_prefix[pi]) * 128;
   const int g_lo = (kvh + hm.kv_head_base) * hm.rep;
   const int h_lo = max(0, g_lo - hm.q_head_base);
   const int h_hi = min(hm.hq, g_lo + hm.rep - hm.q_head_base);
@@ -89,7 +94,9 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < E_N; ++i) {
       const bool many = (i >= E_PR && i < E_PR + 2) || (i >= E_DQF && i < E_DQF + 2);
-      tc::mbar_init(bar(i), many ? 128 : 1);
+      // a stage is full after the TMA bytes and the producer warp's 32 lse/delta stores
+      const bool stage = i >= E_QF && i < E_QF + NST;
+      tc::mbar_init(bar(i), many ? 128 : stage ? 33 : 1);
     }
     tc::fence_barrier_init();
   }
@@ -103,21 +110,45 @@ __global__ void __launch_bounds__(384, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
-    if (tc::elect_one() && T > 0) {
-      tc::mbar_expect_tx(bar(E_KV), 2 * KV_TILE);
-      for (int b = 0; b < 2; ++b) {
-        tc::tma_load_2d(sK + b * 16384, &tmK, kvh * D + b * 64, P.k_row0 + n0, bar(E_KV));
-        tc::tma_load_2d(sV + b * 16384, &tmV, kvh * D + b * 64, P.k_row0 + n0, bar(E_KV));
+    // lane 0 issues the TMA loads; all 32 lanes stage this tile's lse/delta (2 query rows each)
+    // into the stage's smem slot and arrive on the stage barrier, so the softmax warpgroup
+    // never waits on global-memory latency
+    const int lane = threadIdx.x % 32;
+    if (T > 0) {
+      if (lane == 0) {
+        tc::mbar_expect_tx(bar(E_KV), 2 * KV_TILE);
+        for (int b = 0; b < 2; ++b) {
+          tc::tma_load_2d(sK + b * 16384, &tmK, kvh * D + b * 64, P.k_row0 + n0, bar(E_KV));
+          tc::tma_load_2d(sV + b * 16384, &tmV, kvh * D + b * 64, P.k_row0 + n0, bar(E_KV));
+        }
       }
       for (int it = 0; it < T; ++it) {
         const int st = it % NST;
         const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * BQ;
+        if (lane == 0) TR(14, it);
         if (it >= NST) tc::mbar_wait(bar(E_QE + st), ((it - NST) / NST) & 1);
-        tc::mbar_expect_tx(bar(E_QF + st), 2 * Q_TILE);
-        for (int b = 0; b < 2; ++b) {
-          tc::tma_load_2d(sQ + st * Q_TILE + b * 8192, &tmQ, h * D + b * 64, P.q_row0 + m0, bar(E_QF + st));
-          tc::tma_load_2d(sdO + st * Q_TILE + b * 8192, &tmDO, h * D + b * 64, P.q_row0 + m0, bar(E_QF + st));
+        if (lane == 0) {
+          TR(15, it);
+          tc::mbar_expect_tx(bar(E_QF + st), 2 * Q_TILE);
+          for (int b = 0; b < 2; ++b) {
+            tc::tma_load_2d(sQ + st * Q_TILE + b * 8192, &tmQ, h * D + b * 64, P.q_row0 + m0, bar(E_QF + st));
+            tc::tma_load_2d(sdO + st * Q_TILE + b * 8192, &tmDO, h * D + b * 64, P.q_row0 + m0, bar(E_QF + st));
+          }
         }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int r = lane + 32 * k, row = m0 + r;
+          float l2 = INFINITY, dl = 0.f;
+          if (row < P.nq) {
+            const int64_t g = (int64_t)(P.q_row0 + row) * a.lse_row_stride + h;
+            const float l = __ldg(a.lse + g);
+            l2 = l == -INFINITY ? INFINITY : l * kLog2e;
+            dl = __ldg(a.delta + g);
+          }
+          sL[st * 64 + r] = l2;
+          sDl[st * 64 + r] = dl;
+        }
+        tc::mbar_arrive(bar(E_QF + st));  // release: the stores above are visible to waiters
       }
     }
   } else if (warp == 1) {
@@ -129,7 +160,9 @@ __global__ void __launch_bounds__(384, 1)
       auto tail = [&](int i) {  // dV, dK, dQ^T of iteration i
         const int b = i & 1, st = i % NST;
         const uint32_t q = sQ + st * Q_TILE, dO = sdO + st * Q_TILE, ds = sdS + b * 16384;
+        TR(5, i);
         tc::mbar_wait(bar(E_PR + b), (i >> 1) & 1);
+        TR(6, i);
         tc::fence_after();
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk)
@@ -145,12 +178,15 @@ __global__ void __launch_bounds__(384, 1)
           tc::mma_ss(tmem + 128 + 64 * b, tc::sdesc(sK + kk * 2048, 16384, 1024),
                      tc::sdesc(ds + kk * 2048, 8192, 1024), id_q, kk > 0 ? 1u : 0u);
         tc::commit(bar(E_MD + b));
+        TR(7, i);
       };
       tc::mbar_wait(bar(E_KV), 0);
       for (int it = 0; it < T; ++it) {
         const int b = it & 1, st = it % NST;
         const uint32_t q = sQ + st * Q_TILE, dO = sdO + st * Q_TILE;
+        TR(0, it);
         tc::mbar_wait(bar(E_QF + st), (it / NST) & 1);
+        TR(1, it);
         tc::fence_after();
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
@@ -158,10 +194,12 @@ __global__ void __launch_bounds__(384, 1)
           tc::mma_ss(tmem + 64 * b, tc::sdesc(sK + ko, 16, 1024), tc::sdesc(q + qo, 16, 1024), id_s, ks > 0);
         }
         tc::commit(bar(E_SF + b));
+        TR(2, it);
         if (it >= 2) {  // dQ^T of it-2 (same columns) must be drained
           tc::mbar_wait(bar(E_DQF + b), ((it - 2) >> 1) & 1);
           tc::fence_after();
         }
+        TR(3, it);
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t ko = (ks >> 2) * 16384 + (ks & 3) * 32, qo = (ks >> 2) * 8192 + (ks & 3) * 32;
@@ -169,6 +207,7 @@ __global__ void __launch_bounds__(384, 1)
                      ks > 0);
         }
         tc::commit(bar(E_DPF + b));
+        TR(4, it);
         if (it >= 1) tail(it - 1);
       }
       tail(T - 1);
@@ -181,27 +220,11 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
     const float sl2 = a.scale * kLog2e;
     const int c = n0 + t;
-    float nl = -INFINITY, ndl = 0.f;
-    auto fetch = [&](int it) {
-      nl = -INFINITY, ndl = 0.f;
-      if (it >= T || t >= BQ) return;
-      const int h = h_lo + it / nqt, row = m_begin + (it % nqt) * BQ + t;
-      if (row < P.nq) {
-        const int64_t g = (int64_t)(P.q_row0 + row) * a.lse_row_stride + h;
-        nl = __ldg(a.lse + g);
-        ndl = __ldg(a.delta + g);
-      }
-    };
-    fetch(0);
     for (int it = 0; it < T; ++it) {
       const int b = it & 1;
       const int m0 = m_begin + (it % nqt) * BQ;
-      if (t < BQ) {
-        sL[b * 64 + t] = nl == -INFINITY ? INFINITY : nl * kLog2e;
-        sDl[b * 64 + t] = ndl;
-      }
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      fetch(it + 1);
+      const int lb = (it % NST) * 64;  // this tile's lse/delta slot (complete once S^T is)
+      if (t == 0) TR(8, it);
       int ilo = 0, ihi = min(BQ, P.nq - m0);
       if (c >= P.nk) ihi = 0;
       if (P.causal) ilo = max(0, c - P.off - m0);
@@ -210,6 +233,7 @@ __global__ void __launch_bounds__(384, 1)
       tc::mbar_wait(bar(E_DPF + b), (it >> 1) & 1);
       if (it >= 2) tc::mbar_wait(bar(E_MD + b), ((it - 2) >> 1) & 1);  // dS^T_b read by dK/dQ
       tc::fence_after();
+      if (t == 0) TR(9, it);
       const uint32_t ds = sdS + b * 16384;
 #pragma unroll
       for (int cc = 0; cc < BQ / 32; ++cc) {
@@ -221,15 +245,15 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int q0 = cc * 32 + 2 * i;
-          float p0 = fast_exp2(fmaf(__uint_as_float(rs[2 * i]), sl2, -sL[b * 64 + q0]));
-          float p1 = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), sl2, -sL[b * 64 + q0 + 1]));
+          float p0 = fast_exp2(fmaf(__uint_as_float(rs[2 * i]), sl2, -sL[lb + q0]));
+          float p1 = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), sl2, -sL[lb + q0 + 1]));
           if (!full) {
             p0 = (q0 >= ilo && q0 < ihi) ? p0 : 0.f;
             p1 = (q0 + 1 >= ilo && q0 + 1 < ihi) ? p1 : 0.f;
           }
           wp[i] = pack_bf16(p0, p1);
-          wd[i] = pack_bf16(p0 * (__uint_as_float(rp[2 * i]) - sDl[b * 64 + q0]),
-                            p1 * (__uint_as_float(rp[2 * i + 1]) - sDl[b * 64 + q0 + 1]));
+          wd[i] = pack_bf16(p0 * (__uint_as_float(rp[2 * i]) - sDl[lb + q0]),
+                            p1 * (__uint_as_float(rp[2 * i + 1]) - sDl[lb + q0 + 1]));
         }
         tc::tmem_st16(tmem + lane_base + 64 * b + cc * 16, wp);
 #pragma unroll
@@ -243,6 +267,7 @@ __global__ void __launch_bounds__(384, 1)
       tc::fence_proxy_async();
       tc::fence_before();
       tc::mbar_arrive(bar(E_PR + b));
+      if (t == 0) TR(10, it);
     }
     if (T > 0) {  // dV epilogue
       tc::mbar_wait(bar(E_FIN), 0);
@@ -272,12 +297,14 @@ __global__ void __launch_bounds__(384, 1)
       const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * BQ;
       tc::mbar_wait(bar(E_MD + b), (it >> 1) & 1);
       tc::fence_after();
+      if (w == 0 && lane == 0) TR(11, it);
       uint32_t r[2][32];
       tc::tmem_ld32(tmem + lane_base + 128 + 64 * b, r[0]);
       tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, r[1]);
       tc::tmem_wait_ld();
       tc::fence_before();
       tc::mbar_arrive(bar(E_DQF + b));
+      if (w == 0 && lane == 0) TR(12, it);
       // (per-lane red.global.add.f32 from registers measured 1.8x slower than this staging)
       if (lane == 0) tc::bulk_wait_read<0>();  // the slot's previous reduce has read it
       __syncwarp();
@@ -292,6 +319,7 @@ __global__ void __launch_bounds__(384, 1)
         tc::tma_reduce_add_2d(&tmDQ, stg, h * D + w * 32, P.q_row0 + m0);
         tc::bulk_commit();
       }
+      if (w == 0 && lane == 0) TR(13, it);
     }
     if (lane == 0) tc::bulk_wait_read<0>();
     if (T > 0) {  // dK epilogue (lane = key row)
@@ -327,6 +355,9 @@ int max_rows(const ProblemSet& ps, bool q) {
 
 }  // namespace
 
+long long* g_bwd_trace = nullptr;  // profiling (spattn_debug_bwd_trace)
+void set_bwd_trace(void* p) { g_bwd_trace = static_cast<long long*>(p); }
+
 bool tc_bwd_q64_supported(const BwdArgs& a) {
   auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
   return a.d == D && al(a.q) && al(a.k) && al(a.v) && al(a.dout) && al(a.dq_acc) &&
@@ -339,6 +370,7 @@ void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t
   static const int dbg = getenv("SPATTN_DEBUG") ? atoi(getenv("SPATTN_DEBUG")) : 0;
   BwdArgs args = a;
   args.debug = dbg;
+  args.trace = g_bwd_trace;
   ps.tile_prefix[0] = 0;
   for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nk + 127) / 128;
   const int tiles = ps.tile_prefix[ps.n];
@@ -356,7 +388,7 @@ void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t
   std::call_once(once, [] {
     cudaFuncSetAttribute(attn_bwd_tc_q64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   });
-  attn_bwd_tc_q64_kernel<<<dim3(tiles, a.hm.hkv), 384, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
+  attn_bwd_tc_q64_kernel<<<dim3(tiles * a.hm.hkv), 384, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
   note_launch();
 }
 

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(256, 1)
   auto bar = [&](int i) { return bars + 8u * i; };
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // ---- tile decode (heavy causal tiles first)
+  // ---- tile decode (heavy causal tiles first; one head's tiles run together, sharing K/V in L2)
   int pi = 0;
   while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= (int)blockIdx.x) ++pi;
   const AttnProblem P = ps.p[pi];

@@ -68,6 +68,7 @@ struct BwdArgs {
   float scale;
   HeadMap hm;
   int debug;  // profiling switches (SPATTN_DEBUG env): 1 skip dQ atomics, 2 skip dK/dV atomics
+  long long* trace;  // profiling: per-iteration clock64 events of CTA (0,0), or null
 };
 
 // Launch accounting (bench.py's gpu_launches): every launcher in this library calls this.
