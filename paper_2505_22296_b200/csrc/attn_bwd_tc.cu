@@ -72,8 +72,10 @@ __global__ void __launch_bounds__(384, 1)
 
   const int warp = threadIdx.x / 32;
   long long* trace = (a.trace && blockIdx.x == 0) ? a.trace : nullptr;
+  // debug bit 4: record only the iteration-start event (minimal perturbation)
+  const bool tr_all = !(a.debug & 4);
 #define TR(slot, it) \
-  if (trace) trace[(it) * 16 + (slot)] = clock64()
+  if (trace && (tr_all || (slot) == 0)) trace[(it) * 16 + (slot)] = clock64()
   // 1-D grid, kv head fastest: the heaviest causal key tiles of every head run first (LPT)
   const HeadMap hm = a.hm;
   const int tile = blockIdx.x / hm.hkv;
@@ -100,15 +102,18 @@ __global__ void __launch_bounds__(384, 1)
     }
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc<512>(smem_u32(tmem_slot));
+  if (warp == 9) tc::tmem_alloc<512>(smem_u32(tmem_slot));
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tDV = tmem + 256, tDK = tmem + 384;
-  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
 
-  if (warp == 0) {
+  // Roles. The scheduler favours the highest warp id, so the single-thread MMA issuer is the
+  // last warp and the producer sits above the math warps: warps 0-3 softmax-gradient, 4-7 dQ
+  // drain, 8 TMA producer, 9 TMEM allocator, 11 MMA issuer.
+  if (warp == 8) {
     // ------------------------------------------------------------------ TMA producer
     // lane 0 issues the TMA loads; all 32 lanes stage this tile's lse/delta (2 query rows each)
     // into the stage's smem slot and arrive on the stage barrier, so the softmax warpgroup
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(384, 1)
         tc::mbar_arrive(bar(E_QF + st));  // release: the stores above are visible to waiters
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 11) {
     // ---------------------------------------------------------------------- MMA issuer
     if (tc::elect_one() && T > 0) {
       constexpr uint32_t id_s = tc::idesc_bf16(128, BQ, false, false);  // S^T, dP^T
@@ -213,11 +218,11 @@ __global__ void __launch_bounds__(384, 1)
       tail(T - 1);
       tc::commit(bar(E_FIN));
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp < 4) {
     // ----------------------------------------------- softmax-gradient warpgroup (lane = key)
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
-    const int t = threadIdx.x - 128;
-    const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
+    const int t = threadIdx.x;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     const float sl2 = a.scale * kLog2e;
     const int c = n0 + t;
     for (int it = 0; it < T; ++it) {
@@ -286,10 +291,10 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 4 && warp < 8) {
     // ------------------------------------------- dQ warpgroup (lane = head-dim index)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 120;\n");
-    const int w = warp - 8, lane = threadIdx.x % 32;
+    const int w = warp - 4, lane = threadIdx.x % 32;
     const uint32_t lane_base = (uint32_t)(w * 32) << 16;
     const uint32_t stg = sStg + w * 8192;  // [64 queries x 32 fp32], 128B-swizzled rows
     for (int it = 0; it < T; ++it) {
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(384, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 2) tc::tmem_dealloc<512>(tmem);
+  if (warp == 9) tc::tmem_dealloc<512>(tmem);
 }
 
 int max_rows(const ProblemSet& ps, bool q) {

@@ -233,14 +233,16 @@ __global__ void __launch_bounds__(256, 1)
     }
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc<512>(smem_u32(tmem_slot));
+  if (warp == 5) tc::tmem_alloc<512>(smem_u32(tmem_slot));
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tO = tmem + 256;
 
-  if (warp == 0) {
+  // Roles: warps 0-3 softmax + epilogue, 4 TMA producer, 5 TMEM allocator, 7 MMA issuer (the
+  // scheduler favours the highest warp id, so the single issuing thread is never starved).
+  if (warp == 4) {
     if (tc::elect_one()) {
       tc::tma_prefetch(&tmQ);
       tc::tma_prefetch(&tmK);
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(256, 1)
           tc::tma_load_2d(sV + st * Lay::TILE + b * 16384, &tmV, kvh * D + b * 64, y, bar(B_VF + st));
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 7) {
     if (tc::elect_one()) {
       constexpr uint32_t id_s = tc::idesc_bf16(128, 128, false, false);
       constexpr uint32_t id_o = tc::idesc_bf16(128, D, false, true);
@@ -297,9 +299,9 @@ __global__ void __launch_bounds__(256, 1)
       }
       if (n_tiles > 0) issue_pv(n_tiles - 1);
     }
-  } else if (warp >= 4) {
-    const int row = threadIdx.x - 128;  // query row within the tile == TMEM lane
-    const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
+  } else if (warp < 4) {
+    const int row = threadIdx.x;  // query row within the tile == TMEM lane
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     const float sl2 = a.scale * kLog2e;
     const int qa = m0 + row;
     float m_run = -INFINITY, l_run = 0.f;
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(256, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 2) tc::tmem_dealloc<512>(tmem);
+  if (warp == 5) tc::tmem_dealloc<512>(tmem);
 }
 
 int max_rows(const ProblemSet& ps, bool q) {

@@ -58,12 +58,31 @@ Engine engine_from_string(const std::string& s) {  // attention.cpp:10-28
 // ------------------------------------------------------------------------- device buffers
 namespace {
 
+// Engine workspaces come from the device's stream-ordered pool. Its default release threshold
+// (0) hands memory back to the driver at every synchronisation, so each step would re-map
+// ~1.5 GB of workspace; keep it cached instead (once per device).
+void keep_pool_cached() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  SP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (int d : done)
+    if (d == dev) return;
+  cudaMemPool_t pool;
+  SP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t keep = UINT64_MAX;
+  SP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  done.push_back(dev);
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(size_t n, cudaStream_t st) : bytes(n), s(st) {
+    keep_pool_cached();
     if (n) SP_CUDA(cudaMallocAsync(&p, n, st));
   }
   DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr; }
