@@ -115,8 +115,8 @@ int spattn_selftest_umma(void* stream, const void* a, const void* b, const void*
  * Collective over the SP group: every rank calls with its shard. q [bs, local_len, heads, d],
  * k/v [bs, local_len, kv_heads, d], out like q, lse optional. doc_lens (optional, n_docs>0)
  * cuts the global sequence into neat-packed documents (varlen). *saved must be released with
- * spattn_saved_free; q/k/v/out must stay valid until spattn_bwd. Stream-ordered on the
- * context's compute stream. */
+ * spattn_saved_free; q/k/v/out (and lse when given) must stay valid until spattn_bwd.
+ * Stream-ordered on the context's compute stream. */
 int spattn_fwd(spattn_ctx* ctx, int engine, const spattn_config* cfg, const spattn_layout* layout,
                int64_t bs, const void* q, const void* k, const void* v, void* out, float* lse,
                const int64_t* doc_lens, int n_docs, spattn_saved** saved);

@@ -397,6 +397,7 @@ class _RankEngine(torch.autograd.Function):
                                    q.shape[0], q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                    out.data_ptr(), lse.data_ptr(), darr, nd, ctypes.byref(saved)))
         ctx.rc, ctx.h = rc, saved
+        ctx.lse = lse  # the saved state reads this LSE in backward
         ctx.save_for_backward(q, k, v, out)
         ctx.fin = weakref.finalize(out, C.lib().spattn_saved_free, saved)
         return out
