@@ -252,8 +252,14 @@ bool tc_bwd_supported(const BwdArgs& a);
 void launch_attn_bwd_tc(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
 void launch_add_tasks_f32(const CopyTaskSet& ts, cudaStream_t s);
 
+bool tc_fwd_pp_supported(const FwdArgs& a);
+void launch_attn_fwd_tc_pp(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s);
+
 void launch_attn_fwd(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
-  if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && tc_fwd_supported(a))
+  static const bool use_pp = getenv("SPATTN_FWD_PP") != nullptr;  // 1-tile kernel measured faster
+  if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && use_pp && tc_fwd_pp_supported(a))
+    launch_attn_fwd_tc_pp(a, ps, s);
+  else if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && tc_fwd_supported(a))
     launch_attn_fwd_tc(a, ps, s);
   else
     launch_attn_fwd_mma(a, ps, s);
