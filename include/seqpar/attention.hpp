@@ -105,7 +105,7 @@ std::vector<std::array<int, 6>> plan_problems(const std::vector<int64_t>& qpos,
                                               const Documents* docs, int64_t* pairs);
 
 // Which attention kernel family the engines launch.
-enum class KernelFamily { tcgen05, mma };
+enum class KernelFamily { tcgen05, mma, tcgen05_pp };  // tcgen05_pp: two-tile ping-pong forward
 void set_kernel_family(KernelFamily f);
 KernelFamily kernel_family();
 

@@ -92,7 +92,8 @@ int spattn_ctx_stream(spattn_ctx* ctx, void** stream);
 int spattn_ctx_stats(spattn_ctx* ctx, int primitive, int64_t* calls, int64_t* bytes);
 int spattn_ctx_flops(spattn_ctx* ctx, int64_t* flops);
 int spattn_ctx_reset_stats(spattn_ctx* ctx);
-/* 0 = tcgen05/TMEM kernels (default where supported), 1 = mma.sync kernels */
+/* 0 = tcgen05/TMEM kernels (default where supported), 1 = mma.sync kernels,
+ * 2 = tcgen05 with the two-tile ping-pong forward */
 int spattn_set_kernel_family(int family);
 int spattn_get_kernel_family(void);
 

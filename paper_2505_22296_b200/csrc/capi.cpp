@@ -269,10 +269,11 @@ int spattn_ctx_reset_stats(spattn_ctx* c) {
 }
 int spattn_set_kernel_family(int family) {
   return guard([&] {
-    seqpar::set_kernel_family(family == 0 ? seqpar::KernelFamily::tcgen05 : seqpar::KernelFamily::mma);
+    if (family < 0 || family > 2) throw seqpar::ConfigError("kernel family must be 0, 1 or 2");
+    seqpar::set_kernel_family(static_cast<seqpar::KernelFamily>(family));
   });
 }
-int spattn_get_kernel_family(void) { return seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 ? 0 : 1; }
+int spattn_get_kernel_family(void) { return static_cast<int>(seqpar::kernel_family()); }
 
 }  // extern "C"
 namespace spattn {

@@ -256,10 +256,11 @@ bool tc_fwd_pp_supported(const FwdArgs& a);
 void launch_attn_fwd_tc_pp(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s);
 
 void launch_attn_fwd(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
-  static const bool use_pp = getenv("SPATTN_FWD_PP") != nullptr;  // 1-tile kernel measured faster
-  if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && use_pp && tc_fwd_pp_supported(a))
+  // the 1-tile kernel measures faster; the two-tile ping-pong forward is a selectable family
+  const bool use_pp = seqpar::kernel_family() == seqpar::KernelFamily::tcgen05_pp || getenv("SPATTN_FWD_PP");
+  if (use_pp && tc_fwd_pp_supported(a))
     launch_attn_fwd_tc_pp(a, ps, s);
-  else if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && tc_fwd_supported(a))
+  else if (seqpar::kernel_family() != seqpar::KernelFamily::mma && tc_fwd_supported(a))
     launch_attn_fwd_tc(a, ps, s);
   else
     launch_attn_fwd_mma(a, ps, s);
@@ -269,9 +270,10 @@ void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& ps, cudaStream_t
 
 void launch_attn_bwd(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
   static const bool use_q64 = !getenv("SPATTN_BWD_Q128");
-  if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && use_q64 && tc_bwd_q64_supported(a))
+  const bool tc = seqpar::kernel_family() != seqpar::KernelFamily::mma;
+  if (tc && use_q64 && tc_bwd_q64_supported(a))
     launch_attn_bwd_tc_q64(a, ps, s);
-  else if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05 && tc_bwd_supported(a))
+  else if (tc && tc_bwd_supported(a))
     launch_attn_bwd_tc(a, ps, s);
   else
     launch_attn_bwd_mma(a, ps, s);

@@ -111,12 +111,12 @@ def plan_problems(qpos, kpos, causal: bool = True, docs=None, max_problems: int 
 
 
 def set_kernel_family(name: str) -> None:
-    """'tcgen05' (default where supported) or 'mma'."""
-    C.check(C.lib().spattn_set_kernel_family({"tcgen05": 0, "mma": 1}[name]))
+    """'tcgen05' (default where supported), 'mma' or 'tcgen05_pp' (two-tile forward)."""
+    C.check(C.lib().spattn_set_kernel_family({"tcgen05": 0, "mma": 1, "tcgen05_pp": 2}[name]))
 
 
 def kernel_family() -> str:
-    return ["tcgen05", "mma"][C.lib().spattn_get_kernel_family()]
+    return ["tcgen05", "mma", "tcgen05_pp"][C.lib().spattn_get_kernel_family()]
 
 
 def _stream() -> int:

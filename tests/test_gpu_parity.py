@@ -9,7 +9,7 @@ from gpu_util import assert_close, np_, oracle_all, parity_inputs, to_dev, torch
 
 pytestmark = pytest.mark.gpu
 
-FAMILIES = ["tcgen05", "mma"]
+FAMILIES = ["tcgen05", "mma", "tcgen05_pp"]
 
 
 @pytest.fixture(scope="module")
