@@ -167,6 +167,9 @@ int umma_selftest(cudaStream_t s, const void* A, const void* B, const void* Bmn,
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
+__device__ long long* g_fwd_trace = nullptr;  // profiling: per-tile clock64 events of CTA (0,0)
+void set_fwd_trace(void* p) { cudaMemcpyToSymbol(g_fwd_trace, &p, sizeof(p)); }
+
 // =================================================================================
 // Forward: one CTA = 128 query rows x one head of one problem. Warp roles:
 //   warp 0      TMA producer (Q once; K_j, V_j into a 2-stage ring)
@@ -180,6 +183,12 @@ int umma_selftest(cudaStream_t s, const void* A, const void* B, const void* Bmn,
 // (attention.cpp:61-115, :151-165); merge mode folds merge_piece (:117-149) into the epilogue.
 namespace {
 
+#ifndef SPATTN_FWD_POLY_PAIRS
+#define SPATTN_FWD_POLY_PAIRS 0x8
+#endif
+// bit e set: the e-th exponential pair of every 8 columns uses poly_exp2x2 instead of the MUFU
+constexpr int kFwdPolyPairs = SPATTN_FWD_POLY_PAIRS;
+
 template <int D>
 struct FwdLayout {
   static constexpr int QB = D / 64;
@@ -190,26 +199,31 @@ struct FwdLayout {
   static constexpr int V_OFF = K_OFF + 2 * TILE;
   static constexpr int P_OFF = V_OFF + 2 * TILE;
   static constexpr int BAR_OFF = P_OFF + 2 * P_TILE;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int XCH_OFF = BAR_OFF + 256;  // [2 parity][2 halves][128 rows] partial row max
+  static constexpr int SMEM = XCH_OFF + 2 * 2 * 128 * 4;  // base is 1024-aligned (checked)
 };
 
-enum FwdBar { B_Q = 0, B_KF = 1, B_VF = 3, B_KVE = 5, B_SF = 7, B_SFREE = 9, B_PF = 11, B_PV = 13, B_N = 15 };
+// K stage s is released when S reading it completes, V stage s when PV reading it completes, so the
+// next K load overlaps the current softmax instead of waiting for PV.
+enum FwdBar {
+  B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_SFREE = 11, B_PF = 13, B_PV = 15, B_N = 17
+};
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(352, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, FwdArgs a, ProblemSet ps) {
   using Lay = FwdLayout<D>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
+  if (sbase & 1023) __trap();  // the swizzled operand tiles need 1024-byte alignment
   const uint32_t sQ = sbase + Lay::Q_OFF, sK = sbase + Lay::K_OFF, sV = sbase + Lay::V_OFF,
                  sP = sbase + Lay::P_OFF;
   const uint32_t bars = sbase + Lay::BAR_OFF;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Lay::BAR_OFF + B_N * 8);
   auto bar = [&](int i) { return bars + 8u * i; };
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int warp = threadIdx.x / 32;
   // ---- tile decode (heavy causal tiles first; one head's tiles run together, sharing K/V in L2)
   int pi = 0;
   while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= (int)blockIdx.x) ++pi;
@@ -225,24 +239,28 @@ __global__ void __launch_bounds__(256, 1)
   if (P.causal) n_end = min(P.nk, m0 + q_valid - 1 + P.off + 1);
   n_end = max(n_end, 0);
   const int n_tiles = (n_end + 127) / 128;
+  long long* trace = (g_fwd_trace && blockIdx.x == 0 && blockIdx.y == 0) ? g_fwd_trace : nullptr;
+#define FTR(slot, j) \
+  if (trace) trace[(j) * 16 + (slot)] = clock64()
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < B_N; ++i) {
       const bool sm = (i >= B_SFREE && i < B_SFREE + 2) || (i >= B_PF && i < B_PF + 2);
-      tc::mbar_init(bar(i), sm ? 128 : 1);
+      tc::mbar_init(bar(i), sm ? 256 : 1);
     }
     tc::fence_barrier_init();
   }
-  if (warp == 5) tc::tmem_alloc<512>(smem_u32(tmem_slot));
+  if (warp == 9) tc::tmem_alloc<512>(smem_u32(tmem_slot));
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tO = tmem + 256;
 
-  // Roles: warps 0-3 softmax + epilogue, 4 TMA producer, 5 TMEM allocator, 7 MMA issuer (the
-  // scheduler favours the highest warp id, so the single issuing thread is never starved).
-  if (warp == 4) {
+  // Roles: warps 0-7 softmax + epilogue (a query row is split across warps w and w+4, 64 key
+  // columns each), 8 TMA producer, 9 TMEM allocator, 10 MMA issuer (the scheduler favours the
+  // highest warp id, so the single issuing thread is never starved).
+  if (warp == 8) {
     if (tc::elect_one()) {
       tc::tma_prefetch(&tmQ);
       tc::tma_prefetch(&tmK);
@@ -250,25 +268,36 @@ __global__ void __launch_bounds__(256, 1)
       tc::mbar_expect_tx(bar(B_Q), Lay::TILE);
       for (int b = 0; b < Lay::QB; ++b)
         tc::tma_load_2d(sQ + b * 16384, &tmQ, h * D + b * 64, P.q_row0 + m0, bar(B_Q));
-      for (int j = 0; j < n_tiles; ++j) {
+      auto load_k = [&](int j) {
         const int st = j & 1;
-        if (j >= 2) tc::mbar_wait(bar(B_KVE + st), ((j - 2) >> 1) & 1);
-        const int y = P.k_row0 + j * 128;
+        if (j >= 2) tc::mbar_wait(bar(B_KE + st), ((j - 2) >> 1) & 1);
         tc::mbar_expect_tx(bar(B_KF + st), Lay::TILE);
         for (int b = 0; b < Lay::QB; ++b)
-          tc::tma_load_2d(sK + st * Lay::TILE + b * 16384, &tmK, kvh * D + b * 64, y, bar(B_KF + st));
+          tc::tma_load_2d(sK + st * Lay::TILE + b * 16384, &tmK, kvh * D + b * 64, P.k_row0 + j * 128,
+                          bar(B_KF + st));
+      };
+      // order K0, K1, V0, K2, V1, ...: K(j+1) waits for S(j-1), which the tensor pipe finishes
+      // before PV(j-2) that V(j) waits for
+      if (n_tiles > 0) load_k(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1;
+        if (j + 1 < n_tiles) load_k(j + 1);
+        if (j >= 2) tc::mbar_wait(bar(B_VE + st), ((j - 2) >> 1) & 1);
         tc::mbar_expect_tx(bar(B_VF + st), Lay::TILE);
         for (int b = 0; b < Lay::QB; ++b)
-          tc::tma_load_2d(sV + st * Lay::TILE + b * 16384, &tmV, kvh * D + b * 64, y, bar(B_VF + st));
+          tc::tma_load_2d(sV + st * Lay::TILE + b * 16384, &tmV, kvh * D + b * 64, P.k_row0 + j * 128,
+                          bar(B_VF + st));
       }
     }
-  } else if (warp == 7) {
+  } else if (warp == 10) {
     if (tc::elect_one()) {
       constexpr uint32_t id_s = tc::idesc_bf16(128, 128, false, false);
       constexpr uint32_t id_o = tc::idesc_bf16(128, D, false, true);
       auto issue_pv = [&](int i) {
         const int st = i & 1;
+        FTR(2, i);
         tc::mbar_wait(bar(B_PF + st), (i >> 1) & 1);
+        FTR(3, i);
         tc::mbar_wait(bar(B_VF + st), (i >> 1) & 1);
         tc::fence_after();
         const uint32_t pbase = sP + st * Lay::P_TILE, vbase = sV + st * Lay::TILE;
@@ -279,11 +308,13 @@ __global__ void __launch_bounds__(256, 1)
                      id_o, (i > 0 || kk > 0) ? 1u : 0u);
         }
         tc::commit(bar(B_PV + st));
-        tc::commit(bar(B_KVE + st));
+        FTR(4, i);
+        tc::commit(bar(B_VE + st));
       };
       if (n_tiles > 0) tc::mbar_wait(bar(B_Q), 0);
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j & 1;
+        FTR(0, j);
         tc::mbar_wait(bar(B_KF + st), (j >> 1) & 1);
         if (j >= 2) tc::mbar_wait(bar(B_SFREE + st), ((j - 2) >> 1) & 1);
         tc::fence_after();
@@ -295,111 +326,149 @@ __global__ void __launch_bounds__(256, 1)
                      id_s, ks > 0 ? 1u : 0u);
         }
         tc::commit(bar(B_SF + st));
+        tc::commit(bar(B_KE + st));
+        FTR(1, j);
         if (j >= 1) issue_pv(j - 1);
       }
       if (n_tiles > 0) issue_pv(n_tiles - 1);
     }
-  } else if (warp < 4) {
-    const int row = threadIdx.x;  // query row within the tile == TMEM lane
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  } else if (warp < 8) {
+    const int half = warp >> 2;            // key columns [64*half, 64*half+64) of every tile
+    const int row = threadIdx.x & 127;     // query row within the tile == TMEM lane
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    float* xch = reinterpret_cast<float*>(smem + Lay::XCH_OFF);  // [2][2][128]
+    const uint32_t pair_bar = 1 + (warp & 3);                     // warps w and w+4
     const float sl2 = a.scale * kLog2e;
     const int qa = m0 + row;
+    constexpr int DH = D / 2;              // O columns owned by this half
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
       const int st = j & 1;
+      if (threadIdx.x == 0) FTR(5, j);
       tc::mbar_wait(bar(B_SF + st), (j >> 1) & 1);
+      if (threadIdx.x == 0) FTR(6, j);
       tc::fence_after();
-      float x[128];
+      float x[64];
       {
-        uint32_t r[4][32];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tc::tmem_ld32(tmem + lane_base + st * 128 + c * 32, r[c]);
+        uint32_t r[2][32];
+        tc::tmem_ld32(tmem + lane_base + st * 128 + 64 * half, r[0]);
+        tc::tmem_ld32(tmem + lane_base + st * 128 + 64 * half + 32, r[1]);
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
           for (int i = 0; i < 32; ++i) x[c * 32 + i] = __uint_as_float(r[c][i]);
       }
+      if (threadIdx.x == 0) FTR(8, j);
       tc::fence_before();
       tc::mbar_arrive(bar(B_SFREE + st));
       const int n0 = j * 128;
       const bool need_mask = (n0 + 128 > P.nk) || (P.causal && n0 + 127 > m0 + P.off);
       // max over raw scores (sl2 > 0); the scale is folded into the exponent's FFMA below
-      float mt = -INFINITY;
+      // (four independent max chains: two softmax warps per SMSP cannot hide a 32-deep chain)
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       if (need_mask) {
-        const int lim = P.causal ? min(P.nk - 1, qa + P.off) - n0 : P.nk - 1 - n0;
+        const int lim = (P.causal ? min(P.nk - 1, qa + P.off) - n0 : P.nk - 1 - n0) - 64 * half;
 #pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          x[i] = i <= lim ? x[i] : -INFINITY;
-          mt = fmaxf(mt, x[i]);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 128; ++i) mt = fmaxf(mt, x[i]);
+        for (int i = 0; i < 64; ++i) x[i] = i <= lim ? x[i] : -INFINITY;
       }
-      mt *= sl2;
+#pragma unroll
+      for (int i = 0; i < 64; i += 8) {
+        mx[0] = fmaxf(mx[0], fmaxf(x[i], x[i + 1]));
+        mx[1] = fmaxf(mx[1], fmaxf(x[i + 2], x[i + 3]));
+        mx[2] = fmaxf(mx[2], fmaxf(x[i + 4], x[i + 5]));
+        mx[3] = fmaxf(mx[3], fmaxf(x[i + 6], x[i + 7]));
+      }
+      float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      // full-row max from the partner warp (the other 64 columns of the same rows)
+      xch[(st * 2 + half) * 128 + row] = mt;
+      asm volatile("bar.sync %0, 64;\n" ::"r"(pair_bar) : "memory");
+      mt = fmaxf(mt, xch[(st * 2 + (half ^ 1)) * 128 + row]) * sl2;
+      if (threadIdx.x == 0) FTR(9, j);
       if (j == 0) {
         m_run = mt;
       } else if (__any_sync(0xffffffffu, mt > m_run + 8.f)) {
-        // lazy rescale of O (and l) to a new running max; O must hold P_{j-1} V_{j-1}
+        // lazy rescale of this half's O columns (and l) to a new running max; O must hold
+        // P_{j-1} V_{j-1}. Both warps of a row take the same decision (same inputs).
         const float m_new = fmaxf(m_run, mt);
         const float alpha = (m_run == -INFINITY || m_new == -INFINITY) ? (m_run == m_new ? 1.f : 0.f)
                                                                         : fast_exp2(m_run - m_new);
         tc::mbar_wait(bar(B_PV + ((j - 1) & 1)), ((j - 1) >> 1) & 1);
         tc::fence_after();
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < DH / 32; ++c) {
           uint32_t r[32];
-          tc::tmem_ld32(tO + lane_base + c * 32, r);
+          tc::tmem_ld32(tO + lane_base + half * DH + c * 32, r);
           tc::tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-          tc::tmem_st32(tO + lane_base + c * 32, r);
+          tc::tmem_st32(tO + lane_base + half * DH + c * 32, r);
         }
         tc::tmem_wait_st();
         l_run *= alpha;
         m_run = m_new;
       }
       const float muse = m_run == -INFINITY ? 0.f : m_run;
-      float rs = 0.f;
+      uint64_t rs2[2] = {0ull, 0ull};  // packed (even, odd) partial row sums
+      const uint64_t sc2 = f2_pack(sl2, sl2), nm2 = f2_pack(-muse, -muse);
       // P buffer st was last read by PV_{j-2}
       if (j >= 2) tc::mbar_wait(bar(B_PV + st), ((j - 2) >> 1) & 1);
-      const uint32_t pbase = sP + st * Lay::P_TILE;
+      if (threadIdx.x == 0) FTR(10, j);
+      const uint32_t pbase = sP + st * Lay::P_TILE + half * 16384;  // this half's 64-key block
 #pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {
+      for (int ch = 0; ch < 8; ++ch) {
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float p0 = fast_exp2(fmaf(x[ch * 8 + 2 * e], sl2, -muse));
-          const float p1 = fast_exp2(fmaf(x[ch * 8 + 2 * e + 1], sl2, -muse));
-          rs += p0 + p1;
-          w[e] = pack_bf16(p0, p1);
+          const float2 av = f2_unpack(f2_fma(f2_pack(x[ch * 8 + 2 * e], x[ch * 8 + 2 * e + 1]), sc2, nm2));
+          // pairs in kFwdPolyPairs run on the FMA pipe: with packed FFMA2/FADD2 the issue slots
+          // and the MUFU (16/clk/SM) balance near half the exponentials
+          float2 pv;
+          if ((kFwdPolyPairs >> e) & 1) {
+            pv = poly_exp2x2(av.x, av.y);
+          } else {
+            pv.x = fast_exp2(av.x);
+            pv.y = fast_exp2(av.y);
+          }
+          const uint64_t p2 = f2_pack(pv.x, pv.y);
+          rs2[e & 1] = f2_add(rs2[e & 1], p2);
+          w[e] = pack_bf16(pv.x, pv.y);
         }
-        const uint32_t addr = tc::sw128(pbase + (ch >> 3) * 16384, row, ch & 7);
+        const uint32_t addr = tc::sw128(pbase, row, ch);
         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(w[0]), "r"(w[1]),
                      "r"(w[2]), "r"(w[3]));
       }
-      l_run += rs;
+      {
+        const float2 r = f2_unpack(f2_add(rs2[0], rs2[1]));
+        l_run += r.x + r.y;
+      }
+      if (threadIdx.x == 0) FTR(11, j);
       tc::fence_proxy_async();
       tc::mbar_arrive(bar(B_PF + st));
+      if (threadIdx.x == 0) FTR(7, j);
     }
-    // ---- epilogue
-    const bool empty = !(l_run > 0.f);
+    // ---- epilogue: combine the two halves' row sums; each half writes its O columns
+    const bool valid = qa < P.nq;
+    const int64_t grow = (int64_t)(P.q_row0 + qa);
+    float* lp = a.lse + grow * a.lse_row_stride + h;
+    const float la = (a.acc_o != nullptr && valid) ? *lp : -INFINITY;  // read before any write
+    xch[half * 128 + row] = l_run;
+    asm volatile("bar.sync %0, 64;\n" ::"r"(pair_bar) : "memory");
+    l_run += xch[(half ^ 1) * 128 + row];
+    const bool empty = m_run == -INFINITY || !(l_run > 0.f);  // poly_exp2 never returns 0
     const float inv = empty ? 0.f : 1.f / l_run;
     const float lse_row = empty ? -INFINITY : (m_run + __log2f(l_run)) * kLn2;
     if (n_tiles > 0) {
       tc::mbar_wait(bar(B_PV + ((n_tiles - 1) & 1)), ((n_tiles - 1) >> 1) & 1);
       tc::fence_after();
     }
-    const bool valid = qa < P.nq;
-    const int64_t grow = (int64_t)(P.q_row0 + qa);
     if (a.acc_o == nullptr) {
-      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(a.o) + grow * a.o_row_stride + h * D;
+      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(a.o) + grow * a.o_row_stride + h * D + half * DH;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < DH / 32; ++c) {
         uint32_t r[32];
         if (n_tiles > 0) {
-          tc::tmem_ld32(tO + lane_base + c * 32, r);
+          tc::tmem_ld32(tO + lane_base + half * DH + c * 32, r);
           tc::tmem_wait_ld();
         } else {
 #pragma unroll
@@ -415,10 +484,8 @@ __global__ void __launch_bounds__(256, 1)
           for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
       }
-      if (valid) a.lse[grow * a.lse_row_stride + h] = lse_row;
+      if (valid && half == 0) *lp = lse_row;
     } else {
-      float* lp = a.lse + grow * a.lse_row_stride + h;
-      const float la = valid ? *lp : -INFINITY;
       const float lb = lse_row;
       const float mx = fmaxf(la, lb);
       float wa = 1.f, wb = 0.f, ln = la;
@@ -427,12 +494,12 @@ __global__ void __launch_bounds__(256, 1)
         wa = __expf(la - ln);
         wb = __expf(lb - ln) * inv;
       }
-      float* arow = a.acc_o + grow * a.o_row_stride + h * D;
+      float* arow = a.acc_o + grow * a.o_row_stride + h * D + half * DH;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < DH / 32; ++c) {
         uint32_t r[32];
         if (n_tiles > 0) {
-          tc::tmem_ld32(tO + lane_base + c * 32, r);
+          tc::tmem_ld32(tO + lane_base + half * DH + c * 32, r);
           tc::tmem_wait_ld();
         } else {
 #pragma unroll
@@ -451,12 +518,12 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
       }
-      if (valid) *lp = ln;
+      if (valid && half == 0) *lp = ln;
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 5) tc::tmem_dealloc<512>(tmem);
+  if (warp == 9) tc::tmem_dealloc<512>(tmem);
 }
 
 int max_rows(const ProblemSet& ps, bool q) {
@@ -485,7 +552,7 @@ void launch_fwd_tc_d(const FwdArgs& a, const ProblemSet& in, cudaStream_t s) {
     cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          FwdLayout<D>::SMEM);
   });
-  attn_fwd_tc_kernel<D><<<dim3(tiles, a.hm.hq), 256, FwdLayout<D>::SMEM, s>>>(tq, tk, tv, a, ps);
+  attn_fwd_tc_kernel<D><<<dim3(tiles, a.hm.hq), 352, FwdLayout<D>::SMEM, s>>>(tq, tk, tv, a, ps);
   note_launch();
 }
 

@@ -291,10 +291,14 @@ int spattn_selftest_umma(void* stream, const void* a, const void* b, const void*
 }  // extern "C"
 namespace spattn {
 void set_bwd_trace(void* p);
+void set_fwd_trace(void* p);
 }
 extern "C" {
 int spattn_debug_bwd_trace(void* device_buffer) {
-  return guard([&] { spattn::set_bwd_trace(device_buffer); });
+  return guard([&] {
+    spattn::set_bwd_trace(device_buffer);
+    spattn::set_fwd_trace(device_buffer);
+  });
 }
 
 int64_t spattn_launch_count(void) { return spattn::launch_count(); }

@@ -56,6 +56,63 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// Packed fp32x2 arithmetic (FFMA2/FADD2, sm_100): one issue slot for two results. The softmax
+// loops are issue-bound (one instruction per clock per SMSP), so these halve their cost.
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// poly_exp2 (below) on a packed pair.
+__device__ __forceinline__ float2 poly_exp2x2(float a0, float a1) {
+  const uint64_t magic = f2_pack(12582912.f, 12582912.f);
+  const uint64_t x = f2_pack(fmaxf(a0, -126.f), fmaxf(a1, -126.f));
+  const uint64_t t = f2_add(x, magic);
+  const uint64_t f = f2_sub(x, f2_sub(t, magic));
+  uint64_t p = f2_fma(f2_pack(0.05517032742500305f, 0.05517032742500305f), f,
+                      f2_pack(0.24260781705379486f, 0.24260781705379486f));
+  p = f2_fma(p, f, f2_pack(0.693260908126831f, 0.693260908126831f));
+  p = f2_fma(p, f, f2_pack(0.9999282956123352f, 0.9999282956123352f));
+  const float2 pv = f2_unpack(p), tv = f2_unpack(t);
+  return make_float2(__int_as_float(__float_as_int(pv.x) + (__float_as_int(tv.x) << 23)),
+                     __int_as_float(__float_as_int(pv.y) + (__float_as_int(tv.y) << 23)));
+}
+
+// 2^x for x <= 0 on the FP32/INT pipes instead of the MUFU (16 results/clk/SM on B200), used for
+// a fraction of the softmax exponentials so the two pipes finish together. Round-to-nearest split
+// x = j + f, f in [-1/2, 1/2]; 2^f by a degree-3 fit (max relative error 7.6e-5, far below the
+// bf16 rounding of P); j added to the exponent field. Inputs below -126 clamp to ~2^-126.
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = __fadd_rn(x, 12582912.f);  // 1.5 * 2^23: integer part lands in the low bits
+  const float j = __fsub_rn(t, 12582912.f);
+  const float f = __fsub_rn(x, j);
+  const float p = fmaf(fmaf(fmaf(0.05517032742500305f, f, 0.24260781705379486f), f, 0.693260908126831f), f,
+                       0.9999282956123352f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 // Shared tile of `rows` x D bf16 stored with 16-byte chunks XOR-swizzled by (row & 7) so that
 // ldmatrix row gathers and cp.async row writes are bank-conflict free.
 template <int D>

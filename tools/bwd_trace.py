@@ -59,3 +59,6 @@ pairs = [(0, 1, "wait Q/dO"), (1, 2, "issue S"), (2, 3, "wait dQ drain"), (3, 4,
 for a_, b_, nm in pairs:
     print(f"  {nm:16s} {gap(a_, b_):7.0f}")
 print(f"  {'-> next iter':16s} {statistics.median([(t[i + 1, 0] - t[i, 7]).item() for i in range(200, n - 2)]):7.0f}  (tail(i) end -> iter i+2 start is: {statistics.median([(t[i + 2, 0] - t[i, 7]).item() for i in range(200, n - 3)]):.0f})")
+d1 = statistics.median([(t[i - 1, 5] - t[i, 4]).item() for i in range(201, n - 1)])
+d2 = statistics.median([(t[i + 1, 0] - t[i - 1, 7]).item() for i in range(201, n - 2)])
+print(f"GAP dP(i) issued -> tail(i-1) start: {d1:.0f}; tail(i-1) end -> iter i+1 start: {d2:.0f}")
