@@ -199,15 +199,13 @@ struct FwdLayout {
   static constexpr int V_OFF = K_OFF + 2 * TILE;
   static constexpr int P_OFF = V_OFF + 2 * TILE;
   static constexpr int BAR_OFF = P_OFF + 2 * P_TILE;
-  static constexpr int XCH_OFF = BAR_OFF + 256;  // [2 parity][2 halves][128 rows] partial row max
+  static constexpr int XCH_OFF = BAR_OFF + 256;  // epilogue exchange of the two streams' (max, sum)
   static constexpr int SMEM = XCH_OFF + 2 * 2 * 128 * 4;  // base is 1024-aligned (checked)
 };
 
-// K stage s is released when S reading it completes, V stage s when PV reading it completes, so the
-// next K load overlaps the current softmax instead of waiting for PV.
-enum FwdBar {
-  B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_SFREE = 11, B_PF = 13, B_PV = 15, B_N = 17
-};
+// K stage s is released by the S(j) completion barrier (B_SF), V stage s by the PV(j) one (B_PV),
+// so the next K load overlaps the current softmax instead of waiting for PV.
+enum FwdBar { B_Q = 0, B_KF = 1, B_VF = 3, B_SF = 5, B_SFREE = 7, B_PF = 9, B_PV = 11, B_N = 13 };
 
 template <int D>
 __global__ void __launch_bounds__(352, 1)
@@ -246,7 +244,7 @@ __global__ void __launch_bounds__(352, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < B_N; ++i) {
       const bool sm = (i >= B_SFREE && i < B_SFREE + 2) || (i >= B_PF && i < B_PF + 2);
-      tc::mbar_init(bar(i), sm ? 256 : 1);
+      tc::mbar_init(bar(i), sm ? 128 : 1);
     }
     tc::fence_barrier_init();
   }
@@ -257,32 +255,32 @@ __global__ void __launch_bounds__(352, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tO = tmem + 256;
 
-  // Roles: warps 0-7 softmax + epilogue (a query row is split across warps w and w+4, 64 key
-  // columns each), 8 TMA producer, 9 TMEM allocator, 10 MMA issuer (the scheduler favours the
+  // Roles: warps 0-7 softmax + epilogue (two warpgroups, alternate key tiles), 8 TMA producer, 9 TMEM allocator, 10 MMA issuer (the scheduler favours the
   // highest warp id, so the single issuing thread is never starved).
   if (warp == 8) {
+    // K producer (and Q): K stage s is refilled as soon as S reading it has completed
     if (tc::elect_one()) {
       tc::tma_prefetch(&tmQ);
       tc::tma_prefetch(&tmK);
-      tc::tma_prefetch(&tmV);
       tc::mbar_expect_tx(bar(B_Q), Lay::TILE);
       for (int b = 0; b < Lay::QB; ++b)
         tc::tma_load_2d(sQ + b * 16384, &tmQ, h * D + b * 64, P.q_row0 + m0, bar(B_Q));
-      auto load_k = [&](int j) {
+      for (int j = 0; j < n_tiles; ++j) {
         const int st = j & 1;
-        if (j >= 2) tc::mbar_wait(bar(B_KE + st), ((j - 2) >> 1) & 1);
+        if (j >= 2) tc::mbar_wait(bar(B_SF + st), ((j - 2) >> 1) & 1);  // S(j-2) done with K stage
         tc::mbar_expect_tx(bar(B_KF + st), Lay::TILE);
         for (int b = 0; b < Lay::QB; ++b)
           tc::tma_load_2d(sK + st * Lay::TILE + b * 16384, &tmK, kvh * D + b * 64, P.k_row0 + j * 128,
                           bar(B_KF + st));
-      };
-      // order K0, K1, V0, K2, V1, ...: K(j+1) waits for S(j-1), which the tensor pipe finishes
-      // before PV(j-2) that V(j) waits for
-      if (n_tiles > 0) load_k(0);
+      }
+    }
+  } else if (warp == 9) {
+    // V producer (this warp also owns the TMEM allocation)
+    if (tc::elect_one()) {
+      tc::tma_prefetch(&tmV);
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j & 1;
-        if (j + 1 < n_tiles) load_k(j + 1);
-        if (j >= 2) tc::mbar_wait(bar(B_VE + st), ((j - 2) >> 1) & 1);
+        if (j >= 2) tc::mbar_wait(bar(B_PV + st), ((j - 2) >> 1) & 1);  // PV(j-2) done with V stage
         tc::mbar_expect_tx(bar(B_VF + st), Lay::TILE);
         for (int b = 0; b < Lay::QB; ++b)
           tc::tma_load_2d(sV + st * Lay::TILE + b * 16384, &tmV, kvh * D + b * 64, P.k_row0 + j * 128,
@@ -293,6 +291,26 @@ __global__ void __launch_bounds__(352, 1)
     if (tc::elect_one()) {
       constexpr uint32_t id_s = tc::idesc_bf16(128, 128, false, false);
       constexpr uint32_t id_o = tc::idesc_bf16(128, D, false, true);
+      // S(j) -> S buffer j&1; needs K(j) and the group's previous tile j-2 read out of TMEM
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        FTR(0, j);
+        tc::mbar_wait(bar(B_KF + st), (j >> 1) & 1);
+        FTR(12, j);
+        if (j >= 2) tc::mbar_wait(bar(B_SFREE + st), ((j - 2) >> 1) & 1);
+        FTR(13, j);
+        tc::fence_after();
+        const uint32_t kbase = sK + st * Lay::TILE;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
+          tc::mma_ss(tmem + st * 128, tc::sdesc(sQ + off, 16, 1024), tc::sdesc(kbase + off, 16, 1024),
+                     id_s, ks > 0 ? 1u : 0u);
+        }
+        tc::commit(bar(B_SF + st));  // also releases K stage st (each commit costs ~27 pipe cycles)
+        FTR(1, j);
+      };
+      // O_{i&1} += P(i) V(i)
       auto issue_pv = [&](int i) {
         const int st = i & 1;
         FTR(2, i);
@@ -304,187 +322,184 @@ __global__ void __launch_bounds__(352, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;
-          tc::mma_ss(tO, tc::sdesc(pbase + aoff, 16, 1024), tc::sdesc(vbase + kk * 2048, 16384, 1024),
-                     id_o, (i > 0 || kk > 0) ? 1u : 0u);
+          tc::mma_ss(tO + st * D, tc::sdesc(pbase + aoff, 16, 1024),
+                     tc::sdesc(vbase + kk * 2048, 16384, 1024), id_o, (i > 1 || kk > 0) ? 1u : 0u);
         }
-        tc::commit(bar(B_PV + st));
+        tc::commit(bar(B_PV + st));  // also releases V stage st
         FTR(4, i);
-        tc::commit(bar(B_VE + st));
       };
-      if (n_tiles > 0) tc::mbar_wait(bar(B_Q), 0);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        FTR(0, j);
-        tc::mbar_wait(bar(B_KF + st), (j >> 1) & 1);
-        if (j >= 2) tc::mbar_wait(bar(B_SFREE + st), ((j - 2) >> 1) & 1);
-        tc::fence_after();
-        const uint32_t kbase = sK + st * Lay::TILE;
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-          tc::mma_ss(tmem + st * 128, tc::sdesc(sQ + off, 16, 1024), tc::sdesc(kbase + off, 16, 1024),
-                     id_s, ks > 0 ? 1u : 0u);
-        }
-        tc::commit(bar(B_SF + st));
-        tc::commit(bar(B_KE + st));
-        FTR(1, j);
-        if (j >= 1) issue_pv(j - 1);
+      // order S0 S1 | S2 PV0 | S3 PV1 | ...: S(j+2) only needs group j&1 to have read S(j) out of
+      // TMEM (early in its softmax), so it runs while that softmax is still computing P(j)
+      if (n_tiles > 0) {
+        tc::mbar_wait(bar(B_Q), 0);
+        issue_s(0);
       }
-      if (n_tiles > 0) issue_pv(n_tiles - 1);
+      if (n_tiles > 1) issue_s(1);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 2 < n_tiles) issue_s(j + 2);
+        issue_pv(j);
+      }
     }
   } else if (warp < 8) {
-    const int half = warp >> 2;            // key columns [64*half, 64*half+64) of every tile
-    const int row = threadIdx.x & 127;     // query row within the tile == TMEM lane
+    // Two independent online-softmax streams: warpgroup g owns the key tiles j = g (mod 2), its
+    // S buffer g, P buffer g and O accumulator g, with its own running max/sum. Two tiles are in
+    // flight at once, so one group's latency chain (TMEM load -> max -> exp -> P store) overlaps
+    // the other's; the two partial results are merged in the epilogue.
+    const int g = warp >> 2;
+    const int row = threadIdx.x & 127;  // query row within the tile == TMEM lane
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    float* xch = reinterpret_cast<float*>(smem + Lay::XCH_OFF);  // [2][2][128]
-    const uint32_t pair_bar = 1 + (warp & 3);                     // warps w and w+4
+    const uint32_t tS = tmem + g * 128 + lane_base, tOg = tO + g * D + lane_base;
     const float sl2 = a.scale * kLog2e;
     const int qa = m0 + row;
-    constexpr int DH = D / 2;              // O columns owned by this half
     float m_run = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < n_tiles; ++j) {
-      const int st = j & 1;
-      if (threadIdx.x == 0) FTR(5, j);
-      tc::mbar_wait(bar(B_SF + st), (j >> 1) & 1);
-      if (threadIdx.x == 0) FTR(6, j);
+    for (int j = g; j < n_tiles; j += 2) {
+      const int it = j >> 1;  // this group's iteration
+      if (row == 0) FTR(5, j);
+      tc::mbar_wait(bar(B_SF + g), it & 1);
+      if (row == 0) FTR(6, j);
       tc::fence_after();
-      float x[64];
+      float x[128];
       {
-        uint32_t r[2][32];
-        tc::tmem_ld32(tmem + lane_base + st * 128 + 64 * half, r[0]);
-        tc::tmem_ld32(tmem + lane_base + st * 128 + 64 * half + 32, r[1]);
+        uint32_t r[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tc::tmem_ld32(tS + c * 32, r[c]);
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) x[c * 32 + i] = __uint_as_float(r[c][i]);
+        for (int i = 0; i < 128; ++i) x[i] = __uint_as_float(r[i >> 5][i & 31]);
       }
-      if (threadIdx.x == 0) FTR(8, j);
+      if (row == 0) FTR(8, j);
       tc::fence_before();
-      tc::mbar_arrive(bar(B_SFREE + st));
+      tc::mbar_arrive(bar(B_SFREE + g));
       const int n0 = j * 128;
       const bool need_mask = (n0 + 128 > P.nk) || (P.causal && n0 + 127 > m0 + P.off);
-      // max over raw scores (sl2 > 0); the scale is folded into the exponent's FFMA below
-      // (four independent max chains: two softmax warps per SMSP cannot hide a 32-deep chain)
-      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       if (need_mask) {
-        const int lim = (P.causal ? min(P.nk - 1, qa + P.off) - n0 : P.nk - 1 - n0) - 64 * half;
+        const int lim = P.causal ? min(P.nk - 1, qa + P.off) - n0 : P.nk - 1 - n0;
 #pragma unroll
-        for (int i = 0; i < 64; ++i) x[i] = i <= lim ? x[i] : -INFINITY;
+        for (int i = 0; i < 128; ++i) x[i] = i <= lim ? x[i] : -INFINITY;
       }
+      // max over raw scores (sl2 > 0); four independent chains
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int i = 0; i < 64; i += 8) {
+      for (int i = 0; i < 128; i += 8) {
         mx[0] = fmaxf(mx[0], fmaxf(x[i], x[i + 1]));
         mx[1] = fmaxf(mx[1], fmaxf(x[i + 2], x[i + 3]));
         mx[2] = fmaxf(mx[2], fmaxf(x[i + 4], x[i + 5]));
         mx[3] = fmaxf(mx[3], fmaxf(x[i + 6], x[i + 7]));
       }
-      float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-      // full-row max from the partner warp (the other 64 columns of the same rows)
-      xch[(st * 2 + half) * 128 + row] = mt;
-      asm volatile("bar.sync %0, 64;\n" ::"r"(pair_bar) : "memory");
-      mt = fmaxf(mt, xch[(st * 2 + (half ^ 1)) * 128 + row]) * sl2;
-      if (threadIdx.x == 0) FTR(9, j);
-      if (j == 0) {
+      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sl2;
+      if (row == 0) FTR(9, j);
+      if (it == 0) {
         m_run = mt;
       } else if (__any_sync(0xffffffffu, mt > m_run + 8.f)) {
-        // lazy rescale of this half's O columns (and l) to a new running max; O must hold
-        // P_{j-1} V_{j-1}. Both warps of a row take the same decision (same inputs).
+        // lazy rescale of O_g and l to a new running max (threshold 2^8); O_g holds PV(j-2)
         const float m_new = fmaxf(m_run, mt);
         const float alpha = (m_run == -INFINITY || m_new == -INFINITY) ? (m_run == m_new ? 1.f : 0.f)
                                                                         : fast_exp2(m_run - m_new);
-        tc::mbar_wait(bar(B_PV + ((j - 1) & 1)), ((j - 1) >> 1) & 1);
+        tc::mbar_wait(bar(B_PV + g), (it - 1) & 1);
         tc::fence_after();
-#pragma unroll
-        for (int c = 0; c < DH / 32; ++c) {
-          uint32_t r[32];
-          tc::tmem_ld32(tO + lane_base + half * DH + c * 32, r);
+        // (8-column chunks: the 128 scores of this tile are live in registers)
+#pragma unroll 1
+        for (int c = 0; c < D / 8; ++c) {
+          uint32_t r[8];
+          tc::tmem_ld8(tOg + c * 8, r);
           tc::tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-          tc::tmem_st32(tO + lane_base + half * DH + c * 32, r);
+          for (int i = 0; i < 8; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tc::tmem_st8(tOg + c * 8, r);
         }
         tc::tmem_wait_st();
         l_run *= alpha;
         m_run = m_new;
       }
+      if (row == 0) FTR(10, j);
       const float muse = m_run == -INFINITY ? 0.f : m_run;
-      uint64_t rs2[2] = {0ull, 0ull};  // packed (even, odd) partial row sums
       const uint64_t sc2 = f2_pack(sl2, sl2), nm2 = f2_pack(-muse, -muse);
-      // P buffer st was last read by PV_{j-2}
-      if (j >= 2) tc::mbar_wait(bar(B_PV + st), ((j - 2) >> 1) & 1);
-      if (threadIdx.x == 0) FTR(10, j);
-      const uint32_t pbase = sP + st * Lay::P_TILE + half * 16384;  // this half's 64-key block
+      uint64_t rs2[2] = {0ull, 0ull};  // packed (even, odd) partial row sums
+      uint32_t pw[64];                 // P row as bf16 pairs
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 av = f2_unpack(f2_fma(f2_pack(x[ch * 8 + 2 * e], x[ch * 8 + 2 * e + 1]), sc2, nm2));
-          // pairs in kFwdPolyPairs run on the FMA pipe: with packed FFMA2/FADD2 the issue slots
-          // and the MUFU (16/clk/SM) balance near half the exponentials
-          float2 pv;
-          if ((kFwdPolyPairs >> e) & 1) {
-            pv = poly_exp2x2(av.x, av.y);
-          } else {
-            pv.x = fast_exp2(av.x);
-            pv.y = fast_exp2(av.y);
-          }
-          const uint64_t p2 = f2_pack(pv.x, pv.y);
-          rs2[e & 1] = f2_add(rs2[e & 1], p2);
-          w[e] = pack_bf16(pv.x, pv.y);
+      for (int e = 0; e < 64; ++e) {
+        const float2 av = f2_unpack(f2_fma(f2_pack(x[2 * e], x[2 * e + 1]), sc2, nm2));
+        // pairs in kFwdPolyPairs run on the FMA pipe instead of the MUFU (16/clk/SM)
+        float2 pv;
+        if ((kFwdPolyPairs >> (e & 3)) & 1) {
+          pv = poly_exp2x2(av.x, av.y);
+        } else {
+          pv.x = fast_exp2(av.x);
+          pv.y = fast_exp2(av.y);
         }
-        const uint32_t addr = tc::sw128(pbase, row, ch);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(w[0]), "r"(w[1]),
-                     "r"(w[2]), "r"(w[3]));
+        rs2[e & 1] = f2_add(rs2[e & 1], f2_pack(pv.x, pv.y));
+        pw[e] = pack_bf16(pv.x, pv.y);
+      }
+      // P buffer g was last read by PV(j-2); the wait is usually already satisfied here
+      if (it > 0) tc::mbar_wait(bar(B_PV + g), (it - 1) & 1);
+      const uint32_t pbase = sP + g * Lay::P_TILE;
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {
+        const uint32_t addr = tc::sw128(pbase + (ch >> 3) * 16384, row, ch & 7);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(pw[4 * ch]),
+                     "r"(pw[4 * ch + 1]), "r"(pw[4 * ch + 2]), "r"(pw[4 * ch + 3]));
       }
       {
         const float2 r = f2_unpack(f2_add(rs2[0], rs2[1]));
         l_run += r.x + r.y;
       }
-      if (threadIdx.x == 0) FTR(11, j);
+      if (row == 0) FTR(11, j);
+      tc::fence_before();
       tc::fence_proxy_async();
-      tc::mbar_arrive(bar(B_PF + st));
-      if (threadIdx.x == 0) FTR(7, j);
+      tc::mbar_arrive(bar(B_PF + g));
+      if (row == 0) FTR(7, j);
     }
-    // ---- epilogue: combine the two halves' row sums; each half writes its O columns
+    // ---- epilogue: merge the two streams; group g writes output columns [g*D/2, (g+1)*D/2)
     const bool valid = qa < P.nq;
     const int64_t grow = (int64_t)(P.q_row0 + qa);
     float* lp = a.lse + grow * a.lse_row_stride + h;
     const float la = (a.acc_o != nullptr && valid) ? *lp : -INFINITY;  // read before any write
-    xch[half * 128 + row] = l_run;
-    asm volatile("bar.sync %0, 64;\n" ::"r"(pair_bar) : "memory");
-    l_run += xch[(half ^ 1) * 128 + row];
-    const bool empty = m_run == -INFINITY || !(l_run > 0.f);  // poly_exp2 never returns 0
-    const float inv = empty ? 0.f : 1.f / l_run;
-    const float lse_row = empty ? -INFINITY : (m_run + __log2f(l_run)) * kLn2;
+    float* xch = reinterpret_cast<float*>(smem + Lay::XCH_OFF);    // [m: 2][128], [l: 2][128]
+    xch[g * 128 + row] = m_run;
+    xch[256 + g * 128 + row] = l_run;
+    asm volatile("bar.sync 1, 256;\n" ::: "memory");
+    const float m_o = xch[(g ^ 1) * 128 + row], l_o = xch[256 + (g ^ 1) * 128 + row];
+    const float m = fmaxf(m_run, m_o);
+    const float w_own = m_run == -INFINITY ? 0.f : fast_exp2(m_run - m);
+    const float w_oth = m_o == -INFINITY ? 0.f : fast_exp2(m_o - m);
+    const float l = l_run * w_own + l_o * w_oth;
+    const bool empty = m == -INFINITY || !(l > 0.f);  // poly_exp2 never returns exactly 0
+    const float inv = empty ? 0.f : 1.f / l;
+    const float lse_row = empty ? -INFINITY : (m + __log2f(l)) * kLn2;
+    const bool have_own = n_tiles > g, have_oth = n_tiles > (g ^ 1);
     if (n_tiles > 0) {
-      tc::mbar_wait(bar(B_PV + ((n_tiles - 1) & 1)), ((n_tiles - 1) >> 1) & 1);
+      tc::mbar_wait(bar(B_PV + ((n_tiles - 1) & 1)), ((n_tiles - 1) >> 1) & 1);  // all MMAs done
       tc::fence_after();
     }
+    const uint32_t tOo = tO + (g ^ 1) * D + lane_base;
+    constexpr int DH = D / 2;
+    // merged, normalised O column chunk c (32 columns) of this group's half
+    auto o_chunk = [&](int c, float* o) {
+      uint32_t r[32], q[32];
+      if (have_own) tc::tmem_ld32(tOg + g * DH + c * 32, r);
+      if (have_oth) tc::tmem_ld32(tOo + g * DH + c * 32, q);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        o[i] = ((have_own ? __uint_as_float(r[i]) * w_own : 0.f) +
+                (have_oth ? __uint_as_float(q[i]) * w_oth : 0.f)) * inv;
+    };
     if (a.acc_o == nullptr) {
-      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(a.o) + grow * a.o_row_stride + h * D + half * DH;
+      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(a.o) + grow * a.o_row_stride + h * D + g * DH;
 #pragma unroll
       for (int c = 0; c < DH / 32; ++c) {
-        uint32_t r[32];
-        if (n_tiles > 0) {
-          tc::tmem_ld32(tO + lane_base + half * DH + c * 32, r);
-          tc::tmem_wait_ld();
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = 0u;
-        }
+        float o[32];
+        o_chunk(c, o);
         uint32_t w[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          w[i] = pack_bf16(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
+        for (int i = 0; i < 16; ++i) w[i] = pack_bf16(o[2 * i], o[2 * i + 1]);
         if (valid) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
           for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
       }
-      if (valid && half == 0) *lp = lse_row;
+      if (valid && g == 0) *lp = lse_row;
     } else {
       const float lb = lse_row;
       const float mx = fmaxf(la, lb);
@@ -492,33 +507,27 @@ __global__ void __launch_bounds__(352, 1)
       if (mx != -INFINITY) {
         ln = mx + __logf(__expf(la - mx) + __expf(lb - mx));
         wa = __expf(la - ln);
-        wb = __expf(lb - ln) * inv;
+        wb = __expf(lb - ln);
       }
-      float* arow = a.acc_o + grow * a.o_row_stride + h * D + half * DH;
+      float* arow = a.acc_o + grow * a.o_row_stride + h * D + g * DH;
 #pragma unroll
       for (int c = 0; c < DH / 32; ++c) {
-        uint32_t r[32];
-        if (n_tiles > 0) {
-          tc::tmem_ld32(tO + lane_base + half * DH + c * 32, r);
-          tc::tmem_wait_ld();
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = 0u;
-        }
+        float o[32];
+        o_chunk(c, o);
         if (valid) {
           float4* ap = reinterpret_cast<float4*>(arow + c * 32);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             float4 cur = ap[i];
-            cur.x = cur.x * wa + __uint_as_float(r[4 * i]) * wb;
-            cur.y = cur.y * wa + __uint_as_float(r[4 * i + 1]) * wb;
-            cur.z = cur.z * wa + __uint_as_float(r[4 * i + 2]) * wb;
-            cur.w = cur.w * wa + __uint_as_float(r[4 * i + 3]) * wb;
+            cur.x = cur.x * wa + o[4 * i] * wb;
+            cur.y = cur.y * wa + o[4 * i + 1] * wb;
+            cur.z = cur.z * wa + o[4 * i + 2] * wb;
+            cur.w = cur.w * wa + o[4 * i + 3] * wb;
             ap[i] = cur;
           }
         }
       }
-      if (valid && half == 0) *lp = ln;
+      if (valid && g == 0) *lp = ln;
     }
   }
   tc::fence_before();

@@ -36,3 +36,7 @@ print("sm : max+exchange ", med(lambda i: (t[i, 9] - t[i, 8]).item()))
 print("sm : rescale+PVwait", med(lambda i: (t[i, 10] - t[i, 9]).item()))
 print("sm : exp+P store  ", med(lambda i: (t[i, 11] - t[i, 10]).item()))
 print("sm : fence+arrive ", med(lambda i: (t[i, 7] - t[i, 11]).item()))
+print("mma: wait KF      ", med(lambda i: (t[i, 12] - t[i, 0]).item()))
+print("mma: wait SFREE   ", med(lambda i: (t[i, 13] - t[i, 12]).item()))
+print("mma: S issue      ", med(lambda i: (t[i, 1] - t[i, 13]).item()))
+print("mma: S(j) issued -> P(j-2) wait start", med(lambda i: (t[i - 2, 2] - t[i, 1]).item()))
