@@ -40,3 +40,5 @@ print("mma: wait KF      ", med(lambda i: (t[i, 12] - t[i, 0]).item()))
 print("mma: wait SFREE   ", med(lambda i: (t[i, 13] - t[i, 12]).item()))
 print("mma: S issue      ", med(lambda i: (t[i, 1] - t[i, 13]).item()))
 print("mma: S(j) issued -> P(j-2) wait start", med(lambda i: (t[i - 2, 2] - t[i, 1]).item()))
+for i in (100, 101, 102, 103):
+    print(i, "S issue start", t[i,0]-t[100,0], "S issued", t[i,1]-t[100,0], "sm has S", t[i,6]-t[100,0], "P ready", t[i,7]-t[100,0], "PV sees P", t[i,3]-t[100,0], "PV issued", t[i,4]-t[100,0])

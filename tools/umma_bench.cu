@@ -33,8 +33,30 @@ __global__ void __launch_bounds__(256, 1) probe(long long* out, int iters, const
   if (warp == 7) {
     if (tc::elect_one()) {
       const uint32_t id = tc::idesc_bf16(128, N, false, false);
-      long long t0 = clock64();
-      for (int i = 0; i < iters; ++i) {
+      long long t0 = clock64(), wsum = 0, isum = 0;
+      if (MODE >= 11) {
+        constexpr int G = MODE == 12 ? 2 : 8;
+        __shared__ __align__(8) uint64_t pre;
+        tc::mbar_init(smem_u32(&pre), 1);
+        tc::fence_barrier_init();
+        tc::mbar_arrive(smem_u32(&pre));  // phase 0 complete
+        for (int i = 0; i < iters / 8; ++i) {
+          const long long a0 = clock64();
+#pragma unroll
+          for (int k = 0; k < G; ++k)
+            if (MODE != 14)
+              tc::mma_ss(tm, tc::sdesc(sb + k * 32, 16, 1024), tc::sdesc(sb + 65536 + k * 32, 16, 1024), id, 1u);
+          if (MODE != 13) tc::commit(smem_u32(&mb2[i & 1]));
+          const long long a1 = clock64();
+          tc::mbar_wait(smem_u32(&pre), 0);
+          const long long a2 = clock64();
+          isum += a1 - a0;
+          wsum += a2 - a1;
+        }
+        out[2 * gridDim.x + blockIdx.x] = wsum;
+        out[3 * gridDim.x + blockIdx.x] = isum;
+      }
+      for (int i = 0; i < (MODE >= 11 ? 0 : iters); ++i) {
         const uint32_t ko = (i & 3) * 32;
         if (MODE == 2)
           tc::mma_ts(tm, tm + 256 + (i & 3) * 8, tc::sdesc(sb + 65536 + ko, 16, 1024), id, 1u);
@@ -112,8 +134,8 @@ void run(const char* name, long long* d, int iters, const uint8_t* g) {
   cudaFuncSetAttribute(probe<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   for (int r = 0; r < 2; ++r) probe<MODE><<<148, 256, 200 * 1024>>>(d, iters, g);
   cudaError_t e = cudaDeviceSynchronize();
-  long long h[296];
-  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  long long h[600];
+  cudaMemcpy(h, d, 600 * 8, cudaMemcpyDeviceToHost);
   const int N = (MODE == 1) ? 256 : (MODE == 4 ? 64 : 128);
   const double cyc = (double)h[0] / iters;
   const double ideal = 128.0 * N * 16 * 2 / 8192.0;  // cycles at 8192 dense bf16 flop/clk/SM
@@ -121,6 +143,7 @@ void run(const char* name, long long* d, int iters, const uint8_t* g) {
   printf("%-28s %s cycles/MMA %.1f (ideal %.0f) smem operand B/clk %.0f", name, cudaGetErrorString(e),
          cyc, ideal, bytes / cyc);
   if (MODE == 3) printf("  store B/clk %.1f", (double)h[148] * 128 * 16 * 16 / h[0]);
+  if (MODE >= 11) printf("  per group of 8: issue+commit %.0f cycles, satisfied mbar_wait %.0f cycles", (double)h[3 * 148] / (iters / 8), (double)h[2 * 148] / (iters / 8));
   if (MODE == 6) printf("  tmem ld B/clk %.1f", (double)h[148] * 128 * 32 * 4 / h[0]);
   if (MODE == 7) printf("  bulk copy B/clk %.1f", (double)h[148] * 16384 / h[0]);
   printf("\n");
@@ -128,8 +151,8 @@ void run(const char* name, long long* d, int iters, const uint8_t* g) {
 
 int main() {
   long long* d;
-  cudaMalloc(&d, 296 * 8);
-  cudaMemset(d, 0, 296 * 8);
+  cudaMalloc(&d, 600 * 8);
+  cudaMemset(d, 0, 600 * 8);
   const int it = 1 << 16;
   uint8_t* g;
   cudaMalloc(&g, 148 * 4 * 16384);
@@ -141,6 +164,10 @@ int main() {
   run<8>("fwd pattern (8 S, 2 commits, 8 PV)", d, it, g);
   run<9>("fwd pattern, 1 commit", d, it, g);
   run<10>("fwd pattern, no commit", d, it, g);
+  run<11>("8 SS + commit + mbar_wait", d, it, g);
+  run<12>("2 SS + commit + mbar_wait", d, it, g);
+  run<13>("8 SS, no commit + mbar_wait", d, it, g);
+  run<14>("commit only + mbar_wait", d, it, g);
   run<3>("SS M128 N128 + st.shared", d, it, g);
   run<6>("SS M128 N128 + tcgen05.ld", d, it, g);
   run<7>("SS M128 N128 + bulk copy", d, it, g);
