@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(384, 1)
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tDV = tmem + 256, tDK = tmem + 384;
-  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+  // per SMSP: 232 (softmax) + 120 (dQ) + 152 (control) <= 512 registers per thread slot
+  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 152;\n");
 
   // Roles. The scheduler favours the highest warp id, so the single-thread MMA issuer is the
   // last warp and the producer sits above the math warps: warps 0-3 softmax-gradient, 4-7 dQ
