@@ -53,18 +53,33 @@ struct Documents {
   std::vector<int64_t> lengths;
 };
 
+// Rotary embedding of q and k ahead of attention (Model::forward's rope_apply calls,
+// model.cpp:342-343) with the caller's GLOBAL position ids of its local rows — a local 0-based
+// range corrupts the rotary phases when sp > 1 (model.cpp:313-318, the paper's §5.2 pitfall).
+struct Rope {
+  std::vector<int64_t> position_ids;  // local_len entries
+  double base = 10000.0;              // kRopeBase (tensor.hpp:141-144)
+};
+
 // attention.hpp:90-92. q [bs, local_len, heads, dim], k/v [bs, local_len, kv_heads, dim];
-// out has q's shape; lse (optional) is [bs, local_len, heads] fp32 natural log.
+// out has q's shape; lse (optional) is [bs, local_len, heads] fp32 natural log. With `rope`,
+// q and k are rotated first (fused into the all-to-all copy for Ulysses / Dummy-Head / USP) and
+// the backward returns gradients with respect to the unrotated q and k.
 SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig& cfg,
                               const ShardLayout& layout, const DeviceTensor& q,
                               const DeviceTensor& k, const DeviceTensor& v,
                               const DeviceTensor& out, float* lse,
-                              const Documents* docs = nullptr);
+                              const Documents* docs = nullptr, const Rope* rope = nullptr);
 
 // The tape node's backward: dq/dk/dv are written (not accumulated) in q/k/v's layouts.
 void run_attention_engine_backward(RankCtx& ctx, SavedState& saved, const DeviceTensor& dout,
                                    const DeviceTensor& dq, const DeviceTensor& dk,
                                    const DeviceTensor& dv);
+
+// rope_apply (tensor.cpp:548-607) on a bf16 [bs, len, heads, dim] device tensor (inverse:
+// the backward's rotation, tensor.cpp:589-600); out may alias x.
+void rope_apply(cudaStream_t s, int64_t bs, int64_t len, int64_t heads, int dim, const void* x,
+                const std::vector<int64_t>& position_ids, double base, bool inverse, void* out);
 
 // A view shaped like the forward's q (which=0) or k/v (which=1) over `data`.
 DeviceTensor saved_view(const SavedState& s, int which, void* data);

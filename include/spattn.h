@@ -121,6 +121,14 @@ int spattn_selftest_umma(void* stream, const void* a, const void* b, const void*
 int spattn_fwd(spattn_ctx* ctx, int engine, const spattn_config* cfg, const spattn_layout* layout,
                int64_t bs, const void* q, const void* k, const void* v, void* out, float* lse,
                const int64_t* doc_lens, int n_docs, spattn_saved** saved);
+/* spattn_fwd preceded by rope_apply of q and k (Model::forward, model.cpp:342-343; rope_apply,
+ * tensor.cpp:548-607) with the caller's GLOBAL position ids of its local rows (host, local_len
+ * entries; base = kRopeBase 10000, tensor.hpp:141-144). Ulysses / Dummy-Head / USP rotate
+ * inside the all-to-all copy; spattn_bwd then returns dq, dk of the UNROTATED q, k. */
+int spattn_fwd_rope(spattn_ctx* ctx, int engine, const spattn_config* cfg,
+                    const spattn_layout* layout, int64_t bs, const void* q, const void* k,
+                    const void* v, void* out, float* lse, const int64_t* doc_lens, int n_docs,
+                    const int64_t* position_ids, double rope_base, spattn_saved** saved);
 int spattn_bwd(spattn_ctx* ctx, spattn_saved* saved, const void* dout, void* dq, void* dk,
                void* dv);
 void spattn_saved_free(spattn_saved* saved);
@@ -132,6 +140,12 @@ int spattn_fabric_fwd(spattn_fabric* f, int engine, const spattn_config* cfg,
                       const void* const* k, const void* const* v, void* const* out,
                       float* const* lse, const int64_t* doc_lens, int n_docs,
                       spattn_saved** saved);
+int spattn_fabric_fwd_rope(spattn_fabric* f, int engine, const spattn_config* cfg,
+                           const spattn_layout* layout, int64_t bs, const void* const* q,
+                           const void* const* k, const void* const* v, void* const* out,
+                           float* const* lse, const int64_t* doc_lens, int n_docs,
+                           const int64_t* const* position_ids, double rope_base,
+                           spattn_saved** saved);
 int spattn_fabric_bwd(spattn_fabric* f, spattn_saved* const* saved, const void* const* dout,
                       void* const* dq, void* const* dk, void* const* dv);
 /* all_to_all (comm.cpp:357-379) on [bs, len, heads, dim] tensors of elem_bytes each */
@@ -157,6 +171,11 @@ int spattn_block_bwd(void* stream, int64_t bs, int heads, int kv_heads, int dim,
                      const int64_t* kpos, int64_t lk, int causal, double scale, const void* out,
                      const float* lse, const void* dout, float* dq, float* dk, float* dv,
                      int64_t* pairs);
+/* rope_apply (tensor.cpp:548-607) on bf16 [bs, len, heads, dim] device rows; position_ids is a
+ * host array of len global ids; inverse=1 is the backward rotation (tensor.cpp:589-600);
+ * out may alias x. */
+int spattn_rope_apply(void* stream, int64_t bs, int64_t len, int heads, int dim, const void* x,
+                      const int64_t* position_ids, double base, int inverse, void* out);
 /* shard_rows / gather_rows (partition.cpp:124-158) on device rows of row_bytes each,
  * batched over bs: full [bs, L, row] <-> local [bs, L/sp, row] */
 int spattn_shard_rows(void* stream, const spattn_layout* layout, int index, int64_t bs,

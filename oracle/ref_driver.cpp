@@ -9,6 +9,12 @@
 //       sharded run gathered to global order (mirrors report.cpp:95-133) + per-rank bytes
 //   ref_driver bench <engine> <sp> <L> <heads> <kv> <dim> <steps>
 //       wall time of fwd+bwd of run_attention_engine, one thread per rank (comm.cpp:197-222)
+//   ref_driver rope <L> <heads> <dim> <pos_scale> <pos_offset> <seed> <out.bin>
+//       rope_apply (tensor.cpp:548-607) of x ~ U(-2,2) at ids i*scale+offset, loss sum(y*R)
+//   ref_driver rope_engine <engine> <sp> <L> <heads> <kv> <dim> <u> <r> <pos_scale>
+//                          <pos_offset> <seed> <out.bin>
+//       as `engine`, with q and k rotated first by rope_apply at the GLOBAL ids of each rank's
+//       rows (Model::forward, model.cpp:339-344)
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -107,7 +113,7 @@ int golden(int argc, char** argv) {
   return 0;
 }
 
-int engine(int argc, char** argv) {
+int engine(int argc, char** argv, int64_t rope_scale = 0, int64_t rope_offset = 0) {
   if (argc != 12) return 2;
   const Engine e = engine_from_string(argv[2]);
   const int sp = std::atoi(argv[3]);
@@ -131,7 +137,14 @@ int engine(int argc, char** argv) {
     Tensor Rl = Tensor::from({1, l, heads, dim}, shard_rows(d.R, qw, layout, idx));
     Tape tape;
     TapeScope sc(&tape);
-    Tensor out = run_attention_engine(ctx, e, cfg, layout, ql, kl, vl);
+    Tensor qa = ql, ka = kl;
+    if (rope_scale != 0) {
+      std::vector<int64_t> ids;
+      for (int64_t p : layout.positions_of(idx)) ids.push_back(p * rope_scale + rope_offset);
+      qa = rope_apply(ql, ids);
+      ka = rope_apply(kl, ids);
+    }
+    Tensor out = run_attention_engine(ctx, e, cfg, layout, qa, ka, vl);
     tape.backward(sum_all(mul(out, Rl)));
     outs[idx].assign(out.values().begin(), out.values().end());
     dqs[idx].assign(ql.grad().begin(), ql.grad().end());
@@ -154,6 +167,42 @@ int engine(int argc, char** argv) {
   put(f, bytes); put(f, a2a); put(f, ag); put(f, p2p);
   std::fclose(f);
   return 0;
+}
+
+int rope(int argc, char** argv) {
+  if (argc != 9) return 2;
+  const int64_t L = std::atoll(argv[2]);
+  const int heads = std::atoi(argv[3]), dim = std::atoi(argv[4]);
+  const int64_t scale = std::atoll(argv[5]), offset = std::atoll(argv[6]);
+  const uint64_t seed = std::strtoull(argv[7], nullptr, 10);
+  Data d = make_data(seed, L, heads, heads, dim);
+  std::vector<int64_t> ids;
+  for (int64_t i = 0; i < L; ++i) ids.push_back(i * scale + offset);
+  Tensor x = Tensor::from({1, L, heads, dim}, d.q, true);
+  Tensor R = Tensor::from({1, L, heads, dim}, d.R);
+  std::vector<double> y;
+  Tape tape;
+  {
+    TapeScope sc(&tape);
+    Tensor o = rope_apply(x, ids);
+    tape.backward(sum_all(mul(o, R)));
+    y.assign(o.values().begin(), o.values().end());
+  }
+  FILE* f = std::fopen(argv[8], "wb");
+  if (!f) return 3;
+  put(f, d.q); put(f, d.R); put(f, y);
+  put(f, std::vector<double>(x.grad().begin(), x.grad().end()));
+  std::fclose(f);
+  return 0;
+}
+
+int rope_engine(int argc, char** argv) {
+  if (argc != 14) return 2;
+  // drop the two rope arguments and reuse the engine driver
+  std::vector<char*> a(argv, argv + 10);
+  a.push_back(argv[12]);
+  a.push_back(argv[13]);
+  return engine(12, a.data(), std::atoll(argv[10]), std::atoll(argv[11]));
 }
 
 int bench(int argc, char** argv) {
@@ -208,6 +257,8 @@ int main(int argc, char** argv) {
     if (mode == "golden") rc = golden(argc, argv);
     else if (mode == "engine") rc = engine(argc, argv);
     else if (mode == "bench") rc = bench(argc, argv);
+    else if (mode == "rope") rc = rope(argc, argv);
+    else if (mode == "rope_engine") rc = rope_engine(argc, argv);
     if (rc == 2) std::fprintf(stderr, "bad arguments for %s\n", mode.c_str());
     return rc;
   } catch (const std::exception& ex) {

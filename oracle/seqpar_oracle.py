@@ -381,6 +381,31 @@ def varlen_attention_fwd_bwd(q, k, v, dout, doc_lens: Sequence[int], causal=True
     return {"out": out, "lse": lse, "dq": dq, "dk": dk, "dv": dv}
 
 
+ROPE_BASE = 10000.0  # kRopeBase (tensor.hpp:141-144)
+
+
+def rope_apply(x: np.ndarray, position_ids, base: float = ROPE_BASE, inverse: bool = False):
+    """rope_apply (tensor.cpp:548-607) on f64 [bs, L, heads, dim]: half-dim pairing
+    (lo, hi) = (x[j], x[half + j]), theta_j = base^(-2j/dim) (:559-562), rotation by
+    p*theta_j (:571-576). inverse=True is the tape backward (:589-600)."""
+    if x.ndim != 4:
+        raise ShapeError(f"rope_apply expects [bs, L, heads, dim], got {list(x.shape)}")
+    bs, L, hs, dim = x.shape
+    if dim % 2 != 0:
+        raise ShapeError(f"rope head dim must be even, got {dim}")
+    pos = np.asarray(position_ids, dtype=np.int64)
+    if pos.shape != (L,):
+        raise ShapeError(f"position_ids length {pos.size} does not match sequence extent {L}")
+    half = dim // 2
+    theta = np.array([math.pow(base, -2.0 * j / dim) for j in range(half)])
+    ang = pos.astype(np.float64)[:, None] * theta[None, :]          # [L, half]
+    c, s = np.cos(ang)[None, :, None, :], np.sin(ang)[None, :, None, :]
+    if inverse:
+        s = -s
+    lo, hi = x[..., :half], x[..., half:]
+    return np.concatenate([lo * c - hi * s, lo * s + hi * c], axis=-1)
+
+
 def bf16_round(x: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even to bfloat16, returned as float64 (the inputs both sides see)."""
     f = np.ascontiguousarray(x, dtype=np.float32)

@@ -28,7 +28,7 @@ EXPORTS = [
     "spattn_block_fwd", "spattn_block_finalize", "spattn_lse_merge", "spattn_block_bwd",
     "spattn_shard_rows", "spattn_gather_rows", "spattn_launch_count", "spattn_profile_enable",
     "spattn_profile_read", "spattn_selftest_umma", "spattn_plan_heads", "spattn_plan_problems",
-    "spattn_debug_bwd_trace",
+    "spattn_debug_bwd_trace", "spattn_fwd_rope", "spattn_fabric_fwd_rope", "spattn_rope_apply",
 ]
 
 
@@ -105,10 +105,17 @@ def lib() -> ctypes.CDLL:
         "spattn_set_kernel_family": [_i32],
         "spattn_fwd": [_vp, _i32, cfgp, layp, _i64, _vp, _vp, _vp, _vp, _vp, _i64p, _i32,
                        ctypes.POINTER(_vp)],
+        "spattn_fwd_rope": [_vp, _i32, cfgp, layp, _i64, _vp, _vp, _vp, _vp, _vp, _i64p, _i32,
+                            _i64p, ctypes.c_double, ctypes.POINTER(_vp)],
         "spattn_bwd": [_vp, _vp, _vp, _vp, _vp, _vp],
         "spattn_fabric_fwd": [_vp, _i32, cfgp, layp, _i64, ctypes.POINTER(_vp),
                               ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                               ctypes.POINTER(_vp), _i64p, _i32, ctypes.POINTER(_vp)],
+        "spattn_fabric_fwd_rope": [_vp, _i32, cfgp, layp, _i64, ctypes.POINTER(_vp),
+                                   ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                   ctypes.POINTER(_vp), _i64p, _i32, ctypes.POINTER(_i64p),
+                                   ctypes.c_double, ctypes.POINTER(_vp)],
+        "spattn_rope_apply": [_vp, _i64, _i64, _i32, _i32, _vp, _i64p, ctypes.c_double, _i32, _vp],
         "spattn_fabric_bwd": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                               ctypes.POINTER(_vp), ctypes.POINTER(_vp)],
         "spattn_fabric_all_to_all": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, _i64,

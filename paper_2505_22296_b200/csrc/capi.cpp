@@ -309,16 +309,35 @@ int spattn_profile_read(double ms[2], int64_t n[2]) {
   return guard([&] { seqpar::profile_read(ms, n); });
 }
 
+namespace {
+std::unique_ptr<seqpar::Rope> rope_of(const int64_t* position_ids, int64_t n, double base) {
+  if (!position_ids) return nullptr;
+  auto r = std::make_unique<seqpar::Rope>();
+  r->position_ids.assign(position_ids, position_ids + n);
+  r->base = base;
+  return r;
+}
+}  // namespace
+
 int spattn_fwd(spattn_ctx* ctx, int engine, const spattn_config* cfg, const spattn_layout* layout,
                int64_t bs, const void* q, const void* k, const void* v, void* out, float* lse,
                const int64_t* doc_lens, int n_docs, spattn_saved** saved) {
+  return spattn_fwd_rope(ctx, engine, cfg, layout, bs, q, k, v, out, lse, doc_lens, n_docs, nullptr,
+                         0.0, saved);
+}
+
+int spattn_fwd_rope(spattn_ctx* ctx, int engine, const spattn_config* cfg,
+                    const spattn_layout* layout, int64_t bs, const void* q, const void* k,
+                    const void* v, void* out, float* lse, const int64_t* doc_lens, int n_docs,
+                    const int64_t* position_ids, double rope_base, spattn_saved** saved) {
   return guard([&] {
     const auto c = make_cfg(cfg);
     const auto L = make_layout(layout);
     const auto w = views(c, L, bs, q, k, v, out);
     const auto D = docs_of(doc_lens, n_docs);
+    const auto R = rope_of(position_ids, w.q.len, rope_base);
     auto s = seqpar::run_attention_engine(*ctx->rc, make_engine(engine), c, L, w.q, w.k, w.v, w.o,
-                                          lse, D.get());
+                                          lse, D.get(), R.get());
     if (saved) {
       *saved = new spattn_saved{std::move(s)};
     }
@@ -342,6 +361,16 @@ int spattn_fabric_fwd(spattn_fabric* f, int engine, const spattn_config* cfg,
                       const spattn_layout* layout, int64_t bs, const void* const* q,
                       const void* const* k, const void* const* v, void* const* out,
                       float* const* lse, const int64_t* doc_lens, int n_docs, spattn_saved** saved) {
+  return spattn_fabric_fwd_rope(f, engine, cfg, layout, bs, q, k, v, out, lse, doc_lens, n_docs,
+                                nullptr, 0.0, saved);
+}
+
+int spattn_fabric_fwd_rope(spattn_fabric* f, int engine, const spattn_config* cfg,
+                           const spattn_layout* layout, int64_t bs, const void* const* q,
+                           const void* const* k, const void* const* v, void* const* out,
+                           float* const* lse, const int64_t* doc_lens, int n_docs,
+                           const int64_t* const* position_ids, double rope_base,
+                           spattn_saved** saved) {
   return guard([&] {
     const auto c = make_cfg(cfg);
     const auto L = make_layout(layout);
@@ -351,7 +380,9 @@ int spattn_fabric_fwd(spattn_fabric* f, int engine, const spattn_config* cfg,
     f->f->run([&](seqpar::RankCtx& rc) {
       const size_t r = static_cast<size_t>(rc.rank);
       const auto w = views(c, L, bs, q[r], k[r], v[r], out[r]);
-      res[r] = seqpar::run_attention_engine(rc, e, c, L, w.q, w.k, w.v, w.o, lse ? lse[r] : nullptr, D.get());
+      const auto R = rope_of(position_ids ? position_ids[r] : nullptr, w.q.len, rope_base);
+      res[r] = seqpar::run_attention_engine(rc, e, c, L, w.q, w.k, w.v, w.o, lse ? lse[r] : nullptr, D.get(),
+                                            R.get());
     });
     for (size_t r = 0; r < res.size(); ++r)
       if (saved) saved[r] = new spattn_saved{std::move(res[r])};
@@ -425,3 +456,13 @@ int spattn_gather_rows(void* stream, const spattn_layout* layout, int index, int
 }
 
 }  // extern "C"
+
+extern "C" int spattn_rope_apply(void* stream, int64_t bs, int64_t len, int heads, int dim,
+                                 const void* x, const int64_t* position_ids, double base,
+                                 int inverse, void* out) {
+  return guard([&] {
+    if (!position_ids) throw seqpar::ShapeError("rope_apply: position ids are required");
+    seqpar::rope_apply(static_cast<cudaStream_t>(stream), bs, len, heads, dim, x,
+                       std::vector<int64_t>(position_ids, position_ids + len), base, inverse != 0, out);
+  });
+}

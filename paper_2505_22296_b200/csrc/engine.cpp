@@ -372,8 +372,24 @@ struct MoveSpec {
   int elem = 2;
 };
 
+// RoPE fused into a move (rope.cu): the rotating side is always the sequence-sharded X side,
+// whose local row r (within a batch entry) uses row r of the owner's angle table.
+struct RopeMove {
+  const float2* table = nullptr;  // this rank's float2(cos, sin)[lloc][d/2]
+  int dim = 0;
+  int sign = 1;  // +1 forward rotation (q, k), -1 inverse (dq, dk)
+};
+
+void set_rope(CopyTask& t, const float2* table, int64_t row0, int64_t mod, int dim, int sign) {
+  t.rope = table;
+  t.rope_row0 = row0;
+  t.rope_mod = mod;
+  t.rope_dim = dim;
+  t.rope_sign = sign;
+}
+
 void move_forward(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const void* x, void* y,
-                  cudaStream_t s) {
+                  cudaStream_t s, const RopeMove* rope = nullptr) {
   const int G = g.size(), me = g.index_of(ctx.rank);
   int64_t sent = 0;
   for (int j = 0; j < G; ++j)
@@ -381,20 +397,27 @@ void move_forward(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
   ctx.count(Primitive::all_to_all, sent);
   const Window& w = m.win[static_cast<size_t>(me)];
   const int64_t yw = m.yw[static_cast<size_t>(me)];
-  auto unpack = [&](int i, const void* src, int64_t src_stride, int64_t src_col0) {
+  auto unpack = [&](int i, const void* src, int64_t src_stride, int64_t src_col0,
+                    const float2* table) {
     std::vector<CopyTask> t;
     for (int64_t b = 0; b < m.bs; ++b)
-      for (const auto& r : m.runs[static_cast<size_t>(i)])
+      for (const auto& r : m.runs[static_cast<size_t>(i)]) {
         t.push_back({src, y, src_stride, yw, b * m.lloc + r.row0, b * m.lg + r.pos0, src_col0,
                      w.ycol, r.n, w.n, w.pad});
+        if (table) set_rope(t.back(), table, r.row0, m.lloc, rope->dim, rope->sign);
+      }
     return t;
   };
   if (G == 1 || ctx.transport->peer_access()) {
     std::vector<void*> ptrs{const_cast<void*>(x)};
     if (G > 1) ptrs = ctx.transport->exchange_ptrs(g, ctx.rank, const_cast<void*>(x), s);
+    // peer reads rotate with the SOURCE member's table (its rows' global position ids)
+    std::vector<void*> tabs{rope ? const_cast<float2*>(rope->table) : nullptr};
+    if (rope && G > 1) tabs = ctx.transport->exchange_ptrs(g, ctx.rank, tabs[0], s);
     std::vector<CopyTask> tasks;
     for (int i = 0; i < G; ++i) {
-      auto t = unpack(i, ptrs[static_cast<size_t>(i)], m.xw, w.xcol);
+      auto t = unpack(i, ptrs[static_cast<size_t>(i)], m.xw, w.xcol,
+                      rope ? static_cast<const float2*>(tabs[static_cast<size_t>(i)]) : nullptr);
       tasks.insert(tasks.end(), t.begin(), t.end());
     }
     run_tasks(tasks, m.elem, false, s);
@@ -413,6 +436,7 @@ void move_forward(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
     if (wj.n == 0) continue;
     pack.push_back({x, static_cast<char*>(sbuf.p) + soff[j] * m.elem, m.xw, wj.n, 0, 0, wj.xcol, 0,
                     rows, wj.n, 0});
+    if (rope) set_rope(pack.back(), rope->table, 0, m.lloc, rope->dim, rope->sign);
   }
   run_tasks(pack, m.elem, false, s);
   std::vector<Msg> sends, recvs;
@@ -426,14 +450,14 @@ void move_forward(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
   std::vector<CopyTask> tasks;
   for (int i = 0; i < G; ++i) {
     if (w.n == 0 && w.pad == 0) continue;
-    auto t = unpack(i, static_cast<char*>(rbuf.p) + roff[i] * m.elem, w.n, 0);
+    auto t = unpack(i, static_cast<char*>(rbuf.p) + roff[i] * m.elem, w.n, 0, nullptr);
     tasks.insert(tasks.end(), t.begin(), t.end());
   }
   run_tasks(tasks, m.elem, false, s);
 }
 
 void move_reverse(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const void* y, void* x,
-                  bool add, cudaStream_t s) {
+                  bool add, cudaStream_t s, const RopeMove* rope = nullptr) {
   const int G = g.size(), me = g.index_of(ctx.rank);
   const Window& wm = m.win[static_cast<size_t>(me)];
   ctx.count(Primitive::all_to_all, (G - 1) * m.bs * m.lloc * wm.n * m.elem);
@@ -444,12 +468,15 @@ void move_reverse(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
     if (wj.n == 0) return t;
     if (packed_rows) {
       t.push_back({src, x, src_stride, m.xw, 0, 0, src_col0, wj.xcol, m.bs * m.lloc, wj.n, 0});
+      if (rope) set_rope(t.back(), rope->table, 0, m.lloc, rope->dim, rope->sign);
       return t;
     }
     for (int64_t b = 0; b < m.bs; ++b)
-      for (const auto& r : m.runs[static_cast<size_t>(me)])
+      for (const auto& r : m.runs[static_cast<size_t>(me)]) {
         t.push_back({src, x, src_stride, m.xw, b * m.lg + r.pos0, b * m.lloc + r.row0, src_col0,
                      wj.xcol, r.n, wj.n, 0});
+        if (rope) set_rope(t.back(), rope->table, r.row0, m.lloc, rope->dim, rope->sign);
+      }
     return t;
   };
   if (G == 1 || ctx.transport->peer_access()) {
@@ -595,6 +622,8 @@ struct SavedState {
   std::vector<std::vector<PosRun>> ring_runs;  // per ring member: local row -> position
   // xtuner
   int insp = 1;
+  // rope (q, k rotated before attention; dq, dk rotated back): angle table of the local rows
+  const float2* rope_table = nullptr;
 };
 
 void saved_state_free(SavedState* s) { delete s; }
@@ -618,6 +647,32 @@ void profile_read(double* ms, int64_t* n) {
     cudaEventDestroy(r.b);
   }
   g_prof.recs.clear();
+}
+
+namespace {
+// rope_apply (tensor.cpp:548-607) of a whole [bs, lloc, heads, d] bf16 tensor; src == dst is
+// allowed (in place).
+void rope_rows(const void* src, void* dst, int64_t bs, int64_t lloc, int64_t heads, int d,
+               const float2* table, int sign, cudaStream_t s) {
+  CopyTask c{src, dst, heads * d, heads * d, 0, 0, 0, 0, bs * lloc, heads * d, 0};
+  set_rope(c, table, 0, lloc, d, sign);
+  run_tasks({c}, 2, false, s);
+}
+}  // namespace
+
+void rope_apply(cudaStream_t s, int64_t bs, int64_t len, int64_t heads, int dim, const void* x,
+                const std::vector<int64_t>& position_ids, double base, bool inverse, void* out) {
+  if (bs < 0 || len < 0 || heads < 0) throw ShapeError("rope_apply: negative extent");
+  if (dim <= 0 || dim % 2 != 0) throw ShapeError("rope head dim must be even, got " + std::to_string(dim));
+  if (static_cast<int64_t>(position_ids.size()) != len)
+    throw ShapeError("position_ids length " + std::to_string(position_ids.size()) +
+                     " does not match sequence extent " + std::to_string(len));
+  if (bs * len * heads == 0) return;
+  DevBuf table(static_cast<size_t>(len * (dim / 2) * 8), s), dpos(static_cast<size_t>(len * 8), s);
+  SP_CUDA(cudaMemcpyAsync(dpos.p, position_ids.data(), static_cast<size_t>(len * 8), cudaMemcpyHostToDevice, s));
+  spattn::launch_rope_table(table.as<float2>(), dpos.as<int64_t>(), len, dim, base, s);
+  rope_rows(x, out, bs, len, heads, dim, table.as<float2>(), inverse ? -1 : 1, s);
+  check_launch();
 }
 
 DeviceTensor saved_view(const SavedState& s, int which, void* data) {
@@ -906,7 +961,8 @@ std::vector<std::array<int, 6>> plan_problems(const std::vector<int64_t>& qpos,
 SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig& cfg,
                               const ShardLayout& layout, const DeviceTensor& q,
                               const DeviceTensor& k, const DeviceTensor& v,
-                              const DeviceTensor& out, float* lse, const Documents* docs) {
+                              const DeviceTensor& out, float* lse, const Documents* docs,
+                              const Rope* rope) {
   validate(ctx, cfg, layout, q, k, v);
   if (docs && !docs->lengths.empty()) {
     int64_t t = 0;
@@ -972,16 +1028,48 @@ SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig
   if (!lse_local) lse_local = static_cast<float*>(keep(static_cast<size_t>(bs * lloc * H * 4)));
   S->lse = lse_local;
 
-  if (engine == Engine::oracle || (engine != Engine::usp && engine != Engine::xtuner &&
-                                   engine != Engine::ring && G == 1)) {
+  const bool single = engine == Engine::oracle || (engine != Engine::usp && engine != Engine::xtuner &&
+                                                   engine != Engine::ring && G == 1);
+  // RoPE with the caller's global position ids (Model::forward, model.cpp:342-343). Ulysses,
+  // Dummy-Head and USP rotate q and k inside the sequence->head copy of the all-to-all; the
+  // other engines rotate into a workspace copy first.
+  const void* qd = q.data;
+  const void* kd = k.data;
+  RopeMove rmove;
+  const RopeMove* rfwd = nullptr;
+  if (rope) {
+    if (d % 2 != 0) throw ShapeError("rope head dim must be even, got " + std::to_string(d));
+    if (static_cast<int64_t>(rope->position_ids.size()) != lloc)
+      throw ShapeError("rope: position ids length " + std::to_string(rope->position_ids.size()) +
+                       " for " + std::to_string(lloc) + " tokens");
+    float2* table = static_cast<float2*>(keep(static_cast<size_t>(lloc * (d / 2) * 8)));
+    DevBuf dpos(static_cast<size_t>(lloc * 8), s);
+    SP_CUDA(cudaMemcpyAsync(dpos.p, rope->position_ids.data(), static_cast<size_t>(lloc * 8),
+                            cudaMemcpyHostToDevice, s));
+    spattn::launch_rope_table(table, dpos.as<int64_t>(), lloc, d, rope->base, s);
+    check_launch();
+    S->rope_table = table;
+    if (!single && (engine == Engine::ulysses || engine == Engine::dummy_head || engine == Engine::usp)) {
+      rmove = {table, d, 1};
+      rfwd = &rmove;
+    } else {
+      void* qr = keep(static_cast<size_t>(bs * lloc * H * d * 2));
+      void* kr = keep(static_cast<size_t>(bs * lloc * Hkv * d * 2));
+      rope_rows(q.data, qr, bs, lloc, H, d, table, 1, s);
+      rope_rows(k.data, kr, bs, lloc, Hkv, d, table, 1, s);
+      qd = qr, kd = kr;
+    }
+  }
+
+  if (single) {
     // single device: one block over the full sequence (attention.cpp:559-561)
-    Local Lc{q.data, k.data, v.data, bs * lloc, H * d, Hkv * d, {H, Hkv, 0, 0, rep}};
+    Local Lc{qd, kd, v.data, bs * lloc, H * d, Hkv * d, {H, Hkv, 0, 0, rep}};
     auto runs = concat_runs(layout, 0, G);
     int64_t pairs = 0;
     S->plain_probs = make_problems(runs, runs, cfg.causal, bs, lloc, lloc, D, &pairs);
     ctx.add_flops(4 * d * pairs * H);
     plain_forward(ctx, Lc, d, S->plain_probs, out.data, lse_local);
-    S->rq = q.data, S->rk = k.data, S->rv = v.data, S->ro = out.data;
+    S->rq = qd, S->rk = kd, S->rv = v.data, S->ro = out.data;
     S->rrows = bs * lloc;
     S->hm = Lc.hm;
     S->q_stride = H * d, S->kv_stride = Hkv * d;
@@ -990,12 +1078,12 @@ SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig
   }
 
   if (engine == Engine::ring) {
-    Local Lc{q.data, k.data, v.data, bs * lloc, H * d, Hkv * d, {H, Hkv, 0, 0, rep}};
+    Local Lc{qd, kd, v.data, bs * lloc, H * d, Hkv * d, {H, Hkv, 0, 0, rep}};
     S->ring = true;
     S->ring_group = ctx.sp_group;
     S->ring_runs = runs_of(layout, 0, G);
     ring_forward(ctx, ctx.sp_group, S->ring_runs, Lc, d, cfg.causal, bs, lloc, D, out.data, lse_local);
-    S->rq = q.data, S->rk = k.data, S->rv = v.data, S->ro = out.data;
+    S->rq = qd, S->rk = kd, S->rv = v.data, S->ro = out.data;
     S->rrows = bs * lloc;
     S->hm = Lc.hm;
     S->q_stride = H * d, S->kv_stride = Hkv * d;
@@ -1035,8 +1123,8 @@ SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig
     void* vg = keep(static_cast<size_t>(bs * lg * nkv * d * 2));
     void* og = keep(static_cast<size_t>(bs * lg * hv_local * d * 2));
     float* lg_lse = static_cast<float*>(keep(static_cast<size_t>(bs * lg * hv_local * 4)));
-    move_forward(ctx, ctx.sp_group, mq, q.data, qg, s);
-    move_forward(ctx, ctx.sp_group, mkv, k.data, kg, s);
+    move_forward(ctx, ctx.sp_group, mq, qd, qg, s);
+    move_forward(ctx, ctx.sp_group, mkv, kd, kg, s);
     move_forward(ctx, ctx.sp_group, mkv, v.data, vg, s);
     Local Lc{qg, kg, vg, bs * lg, hv_local * d, nkv * d,
              {hv_local, nkv, grp * hv_local, static_cast<int>(mkv.win[static_cast<size_t>(me)].xcol / d), rep}};
@@ -1097,8 +1185,8 @@ SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig
   void* vg = keep(static_cast<size_t>(bs * lg * nkv * d * 2));
   void* og = keep(static_cast<size_t>(bs * lg * nq * d * 2));
   float* glse = static_cast<float*>(keep(static_cast<size_t>(bs * lg * nq * 4)));
-  move_forward(ctx, inner, mq, q.data, qg, s);
-  move_forward(ctx, inner, mkv, k.data, kg, s);
+  move_forward(ctx, inner, mq, qd, qg, s, rfwd);
+  move_forward(ctx, inner, mkv, kd, kg, s, rfwd);
   move_forward(ctx, inner, mkv, v.data, vg, s);
   Local Lc{qg, kg, vg, bs * lg, nq * d, nkv * d,
            {nq, nkv, hp.qlo[static_cast<size_t>(iota)], hp.kvlo[static_cast<size_t>(iota)], rep}};
@@ -1163,6 +1251,10 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& S, const DeviceTens
                     dout.data, dqa.as<float>(), dk.data, dv.data, nullptr, nullptr);
     }
     spattn::launch_f32_to_bf16(dq.data, dqa.as<float>(), 1.f, rows * H * d, s);
+    if (S.rope_table) {  // rope_apply backward (tensor.cpp:589-600): inverse rotation
+      rope_rows(dq.data, dq.data, bs, lloc, H, d, S.rope_table, -1, s);
+      rope_rows(dk.data, dk.data, bs, lloc, Hkv, d, S.rope_table, -1, s);
+    }
     check_launch();
     return;
   }
@@ -1220,6 +1312,10 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& S, const DeviceTens
     move_reverse(ctx, ctx.sp_group, mk, dva.p, dvf.p, true, s);
     spattn::launch_f32_to_bf16(dk.data, dkf.as<float>(), 1.f, rows * Hkv * d, s);
     spattn::launch_f32_to_bf16(dv.data, dvf.as<float>(), 1.f, rows * Hkv * d, s);
+    if (S.rope_table) {
+      rope_rows(dq.data, dq.data, bs, lloc, H, d, S.rope_table, -1, s);
+      rope_rows(dk.data, dk.data, bs, lloc, Hkv, d, S.rope_table, -1, s);
+    }
     check_launch();
     return;
   }
@@ -1250,14 +1346,17 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& S, const DeviceTens
   }
   DevBuf dqg(static_cast<size_t>(bs * lg * nq * d * 2), s);
   spattn::launch_f32_to_bf16(dqg.p, dqa.as<float>(), 1.f, bs * lg * nq * d, s);
-  move_reverse(ctx, inner, mq, dqg.p, dq.data, false, s);
+  // the inverse rotation of dq/dk rides the head->sequence copy back (rope.cu)
+  const RopeMove rinv{S.rope_table, d, -1};
+  const RopeMove* rbwd = S.rope_table ? &rinv : nullptr;
+  move_reverse(ctx, inner, mq, dqg.p, dq.data, false, s, rbwd);
   MoveSpec mkv = head_move(hp, true, bs, lloc, Hkv, d, S.inner_runs, 2);
   const int64_t rows = bs * lloc;
   if (!windows_overlap(mkv.win)) {
     DevBuf dkg(static_cast<size_t>(bs * lg * nkv * d * 2), s), dvg(static_cast<size_t>(bs * lg * nkv * d * 2), s);
     spattn::launch_f32_to_bf16(dkg.p, dka.as<float>(), 1.f, bs * lg * nkv * d, s);
     spattn::launch_f32_to_bf16(dvg.p, dva.as<float>(), 1.f, bs * lg * nkv * d, s);
-    move_reverse(ctx, inner, mkv, dkg.p, dk.data, false, s);
+    move_reverse(ctx, inner, mkv, dkg.p, dk.data, false, s, rbwd);
     move_reverse(ctx, inner, mkv, dvg.p, dv.data, false, s);
   } else {
     // kv heads shared by members (Hkv % u != 0): sum fp32 partials (repeat_heads backward)
@@ -1268,6 +1367,7 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& S, const DeviceTens
     move_reverse(ctx, inner, mk4, dva.p, dvf.p, true, s);
     spattn::launch_f32_to_bf16(dk.data, dkf.as<float>(), 1.f, rows * Hkv * d, s);
     spattn::launch_f32_to_bf16(dv.data, dvf.as<float>(), 1.f, rows * Hkv * d, s);
+    if (S.rope_table) rope_rows(dk.data, dk.data, bs, lloc, Hkv, d, S.rope_table, -1, s);
   }
   check_launch();
 }

@@ -162,6 +162,7 @@ void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 void launch_copy_tasks(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s) {
+  if (ts.n > 0 && ts.t[0].rope) return launch_copy_tasks_rope(ts, s);
   CopyLaunch L;
   L.ts = ts;
   L.row_prefix[0] = 0;

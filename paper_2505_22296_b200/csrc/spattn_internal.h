@@ -92,6 +92,12 @@ struct CopyTask {
   int64_t src_row0, dst_row0;
   int64_t src_col0, dst_col0;
   int64_t rows, cols, zero_cols;
+  // RoPE fused into the copy (rope_apply, tensor.cpp:548-607; rope.cu): bf16 payload of whole
+  // heads of rope_dim columns, rotated by the float2(cos, sin) angle-table row
+  // (rope_row0 + r) % rope_mod; rope_sign -1 applies the inverse rotation (the backward).
+  const float2* rope = nullptr;
+  int64_t rope_row0 = 0, rope_mod = 1;
+  int rope_dim = 0, rope_sign = 1;
 };
 constexpr int kMaxCopyTasks = 64;
 struct CopyTaskSet {
@@ -99,6 +105,11 @@ struct CopyTaskSet {
   int n;
 };
 void launch_copy_tasks(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s);
+// rope.cu: angle table float2(cos, sin)[rows][dim/2] of device position ids, and the rotating
+// row copier (every task of the set carries a table)
+void launch_rope_table(float2* table, const int64_t* dpos, int64_t rows, int dim, double base,
+                       cudaStream_t s);
+void launch_copy_tasks_rope(const CopyTaskSet& ts, cudaStream_t s);
 
 // acc (fp32 out + lse) merge of a finished piece (fp32 out + lse) — merge_piece
 // (attention.cpp:117-149) in LSE form.

@@ -246,9 +246,48 @@ def _free_saved(handles):
             C.lib().spattn_saved_free(h)
 
 
+ROPE_BASE = 10000.0  # kRopeBase (reference tensor.hpp:141-144)
+
+
+def _i64_array(xs):
+    xs = [int(x) for x in xs]
+    return (ctypes.c_int64 * max(1, len(xs)))(*xs)
+
+
+class _Rope(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, pos, base):
+        out = torch.empty_like(x)
+        C.check(C.lib().spattn_rope_apply(_stream(), x.shape[0], x.shape[1], x.shape[2], x.shape[3],
+                                          x.data_ptr(), pos, base, 0, out.data_ptr()))
+        ctx.pos, ctx.base = pos, base
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        g = g.contiguous()
+        dx = torch.empty_like(g)
+        C.check(C.lib().spattn_rope_apply(_stream(), g.shape[0], g.shape[1], g.shape[2], g.shape[3],
+                                          g.data_ptr(), ctx.pos, ctx.base, 1, dx.data_ptr()))
+        return dx, None, None
+
+
+def rope_apply(x: torch.Tensor, position_ids: Sequence[int], base: float = ROPE_BASE):
+    """rope_apply (reference tensor.cpp:548-607) on a bf16 CUDA tensor [bs, L, heads, dim] with
+    one position id per sequence row; differentiable (the backward is the inverse rotation)."""
+    if x.dim() != 4:
+        raise ShapeError(f"rope_apply expects [bs, L, heads, dim], got {list(x.shape)}")
+    if not x.is_cuda or x.dtype != torch.bfloat16:
+        raise ShapeError("rope_apply: x must be a bf16 CUDA tensor")
+    if len(position_ids) != x.shape[1]:
+        raise ShapeError(f"position_ids length {len(position_ids)} does not match sequence "
+                         f"extent {x.shape[1]}")
+    return _Rope.apply(x.contiguous(), _i64_array(position_ids), float(base))
+
+
 class _FabricEngine(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, fab, engine, cfg, lay, mode, u, r, docs, want_lse):
+    def forward(ctx, q, k, v, fab, engine, cfg, lay, mode, u, r, docs, want_lse, pos=None):
         sp = fab.sp
         qs = [shard_rows(q, mode, sp, i, u, r) for i in range(sp)]
         ks = [shard_rows(k, mode, sp, i, u, r) for i in range(sp)]
@@ -259,11 +298,18 @@ class _FabricEngine(torch.autograd.Function):
         saved = (ctypes.c_void_p * sp)()
         nd = 0 if docs is None else len(docs)
         darr = None if docs is None else (ctypes.c_int64 * nd)(*docs)
-        C.check(C.lib().spattn_fabric_fwd(
+        if pos is not None:  # each rank rotates with the global ids of its own rows
+            lay_pos = [shard_positions(mode, q.shape[1], sp, i, u, r) for i in range(sp)]
+            parts = [_i64_array([pos[p] for p in lp]) for lp in lay_pos]
+            parr = (ctypes.POINTER(ctypes.c_int64) * sp)(
+                *[ctypes.cast(a, ctypes.POINTER(ctypes.c_int64)) for a in parts])
+        else:
+            parr = None
+        C.check(C.lib().spattn_fabric_fwd_rope(
             fab._h, C.engine_id(engine), ctypes.byref(cfg), ctypes.byref(lay), q.shape[0],
             C.ptr_array([x.data_ptr() for x in qs]), C.ptr_array([x.data_ptr() for x in ks]),
             C.ptr_array([x.data_ptr() for x in vs]), C.ptr_array([x.data_ptr() for x in outs]),
-            C.ptr_array([x.data_ptr() for x in lses]), darr, nd, saved))
+            C.ptr_array([x.data_ptr() for x in lses]), darr, nd, parr, ROPE_BASE, saved))
         handles = [saved[i] for i in range(sp)]
         ctx.fab, ctx.mode, ctx.u, ctx.r = fab, mode, u, r
         ctx.handles = handles
@@ -292,17 +338,20 @@ class _FabricEngine(torch.autograd.Function):
         dq = gather_rows(dqs, mode, sp, u, r)
         dk = gather_rows(dks, mode, sp, u, r)
         dv = gather_rows(dvs, mode, sp, u, r)
-        return dq, dk, dv, None, None, None, None, None, None, None, None, None
+        return dq, dk, dv, None, None, None, None, None, None, None, None, None, None
 
 
 def engine_attention(engine: str, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sp: int,
                      layout: str = "auto", causal: bool = True, ulysses_degree: int = 0,
                      ring_degree: int = 0, docs: Optional[Sequence[int]] = None,
                      fabric: Optional[Fabric] = None, force_messages: bool = False,
-                     return_lse: bool = False):
+                     return_lse: bool = False, position_ids: Optional[Sequence[int]] = None):
     """Sharded attention across ``sp`` loopback ranks on the current GPU, gathered back to the
     full sequence (py_module.cpp:111-180), differentiable. q [bs, L, H, d] and k/v
-    [bs, L, Hkv, d] are bf16 CUDA tensors; ``docs`` are neat-packed document lengths."""
+    [bs, L, Hkv, d] are bf16 CUDA tensors; ``docs`` are neat-packed document lengths.
+    ``position_ids`` (one global id per sequence row) applies rope_apply to q and k first, as
+    Model::forward does (model.cpp:342-343) — fused into the all-to-all copy for Ulysses,
+    Dummy-Head and USP; the gradients are those of the unrotated q and k."""
     for t in (q, k, v):
         if not t.is_cuda or t.dtype != torch.bfloat16:
             raise ShapeError("engine_attention: q, k, v must be bf16 CUDA tensors")
@@ -313,9 +362,12 @@ def engine_attention(engine: str, q: torch.Tensor, k: torch.Tensor, v: torch.Ten
     fab = fabric or Fabric(sp, force_messages=force_messages)
     if fab.sp != sp:
         raise ConfigError("fabric sp does not match")
+    if position_ids is not None and len(position_ids) != L:
+        raise ShapeError(f"position_ids length {len(position_ids)} for {L} tokens")
     out, lse = _FabricEngine.apply(q.contiguous(), k.contiguous(), v.contiguous(), fab, engine,
                                    cfg, lay, mode, ulysses_degree, ring_degree,
-                                   None if docs is None else list(docs), return_lse)
+                                   None if docs is None else list(docs), return_lse,
+                                   None if position_ids is None else list(position_ids))
     return (out, lse) if return_lse else out
 
 
@@ -386,16 +438,18 @@ class RankContext:
 
 class _RankEngine(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, rc, engine, cfg, lay, docs):
+    def forward(ctx, q, k, v, rc, engine, cfg, lay, docs, pos=None):
         out = torch.empty_like(q)
         lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
         C.check(C.lib().spattn_ctx_set_stream(rc._h, _stream()))
         saved = ctypes.c_void_p()
         nd = 0 if docs is None else len(docs)
         darr = None if docs is None else (ctypes.c_int64 * nd)(*docs)
-        C.check(C.lib().spattn_fwd(rc._h, C.engine_id(engine), ctypes.byref(cfg), ctypes.byref(lay),
-                                   q.shape[0], q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                                   out.data_ptr(), lse.data_ptr(), darr, nd, ctypes.byref(saved)))
+        parr = None if pos is None else _i64_array(pos)
+        C.check(C.lib().spattn_fwd_rope(rc._h, C.engine_id(engine), ctypes.byref(cfg),
+                                        ctypes.byref(lay), q.shape[0], q.data_ptr(), k.data_ptr(),
+                                        v.data_ptr(), out.data_ptr(), lse.data_ptr(), darr, nd,
+                                        parr, ROPE_BASE, ctypes.byref(saved)))
         ctx.rc, ctx.h = rc, saved
         ctx.lse = lse  # the saved state reads this LSE in backward
         ctx.save_for_backward(q, k, v, out)
@@ -409,7 +463,7 @@ class _RankEngine(torch.autograd.Function):
         C.check(C.lib().spattn_ctx_set_stream(ctx.rc._h, _stream()))
         C.check(C.lib().spattn_bwd(ctx.rc._h, ctx.h, dout.contiguous().data_ptr(), dq.data_ptr(),
                                    dk.data_ptr(), dv.data_ptr()))
-        return dq, dk, dv, None, None, None, None, None
+        return dq, dk, dv, None, None, None, None, None, None
 
 
 class SequenceParallelAttention(torch.nn.Module):
@@ -426,7 +480,12 @@ class SequenceParallelAttention(torch.nn.Module):
                                           ring_degree)
         self.cfg = C.make_config(heads, kv_heads, head_dim, causal, ulysses_degree, ring_degree)
 
-    def forward(self, q, k, v, docs: Optional[Sequence[int]] = None):
+    def forward(self, q, k, v, docs: Optional[Sequence[int]] = None,
+                position_ids: Optional[Sequence[int]] = None):
+        """``position_ids``: the GLOBAL ids of this rank's rows; when given q and k are rotated
+        (rope_apply) before attention — a local 0-based range would corrupt the rotary phases
+        (reference model.cpp:313-318)."""
         return _RankEngine.apply(q.contiguous(), k.contiguous(), v.contiguous(), self.rc,
                                  self.engine, self.cfg, self.lay,
-                                 None if docs is None else list(docs))
+                                 None if docs is None else list(docs),
+                                 None if position_ids is None else list(position_ids))

@@ -59,6 +59,52 @@ ENGINE_CASES = [
 ]
 
 
+ROPE_CASES = [
+    # name, L, heads, dim, pos_scale, pos_offset, seed
+    ("rope_L16_h2_d8", 16, 2, 8, 1, 0, 13),
+    ("rope_L12_h3_d6_far", 12, 3, 6, 7, 100000, 17),
+    ("rope_L8_h2_d64_far", 8, 2, 64, 1000, 3, 19),
+    ("rope_L6_h1_d16_neg", 6, 1, 16, -5, 2, 23),
+]
+
+ROPE_ENGINE_CASES = [
+    # engine, sp, L, heads, kv, dim, u, r, pos_scale, pos_offset, seed
+    ("ulysses", 2, 32, 4, 2, 8, 0, 0, 1, 0, 2000001),
+    ("ulysses", 4, 64, 8, 2, 16, 0, 0, 3, 5000, 2000002),
+    ("dummy_head", 4, 32, 6, 2, 8, 0, 0, 1, 0, 2000003),
+    ("xtuner", 4, 32, 6, 6, 8, 0, 0, 1, 0, 2000004),
+    ("ring", 4, 64, 4, 2, 8, 0, 0, 1, 0, 2000005),
+    ("usp", 4, 64, 4, 4, 8, 2, 2, 1, 0, 2000006),
+    ("oracle", 1, 32, 4, 2, 8, 0, 0, 1, 7, 2000007),
+]
+
+
+def make_rope(tmp):
+    """rope_apply (tensor.cpp:548-607) alone, and the engines with q/k rotated at global ids
+    (Model::forward, model.cpp:339-344) -> tests/golden/reference_rope.npz."""
+    arrays = {}
+    for name, L, h, d, sc, off, seed in ROPE_CASES:
+        p = os.path.join(tmp, name + ".bin")
+        subprocess.run([DRIVER, "rope", str(L), str(h), str(d), str(sc), str(off), str(seed), p],
+                       check=True)
+        x, R, y, dx = read_arrays(p)
+        for key, val in dict(x=x, R=R, y=y, dx=dx).items():
+            arrays[f"{name}/{key}"] = val
+        arrays[f"{name}/meta"] = np.array([L, h, d, sc, off, seed], np.int64)
+    for eng, sp, L, h, kv, d, u, r, sc, off, seed in ROPE_ENGINE_CASES:
+        name = f"rope_engine_{eng}_sp{sp}_L{L}_h{h}_kv{kv}_d{d}"
+        p = os.path.join(tmp, name + ".bin")
+        subprocess.run([DRIVER, "rope_engine", eng, str(sp), str(L), str(h), str(kv), str(d),
+                        str(u), str(r), str(sc), str(off), str(seed), p], check=True)
+        out, dq, dk, dv, tot, a2a, ag, p2p = read_arrays(p)
+        for key, val in dict(out=out, dq=dq, dk=dk, dv=dv).items():
+            arrays[f"{name}/{key}"] = val
+        arrays[f"{name}/meta"] = np.array([sp, L, h, kv, d, u, r, sc, off, seed], np.int64)
+        arrays[f"{name}/engine"] = np.frombuffer(eng.encode().ljust(16, b" "), np.uint8)
+    np.savez_compressed(os.path.join(HERE, "reference_rope.npz"), **arrays)
+    print("wrote", os.path.join(HERE, "reference_rope.npz"))
+
+
 def main():
     if not os.path.exists(DRIVER):
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
@@ -139,4 +185,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["rope"]:
+        make_rope(tempfile.mkdtemp())
+    else:
+        main()
+        make_rope(tempfile.mkdtemp())
