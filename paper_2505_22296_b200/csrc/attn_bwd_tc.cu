@@ -55,6 +55,49 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                : "memory");
 }
 
+// Softmax gradient of one 32-query chunk for one key (thread): P = 2^(s*scale*log2e - lse*log2e)
+// and dS = P (dP - delta), both packed to bf16 pairs (attention.cpp:199-209). Packed fp32x2
+// math; one pair in four takes the FMA-pipe exp2 so MUFU and FMA finish together. MASK (only
+// for tiles crossing the causal diagonal or the row end) zeroes queries outside [ilo, ihi).
+template <bool MASK, bool PACKED, bool POLY>
+__device__ __forceinline__ void grad_chunk(const uint32_t (&rs)[32], const uint32_t (&rp)[32], const float2* nl2,
+                                           const float2* dl2, uint64_t sl2x2, int ilo, int ihi, uint32_t (&wp)[16],
+                                           uint32_t (&wd)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float2 nl = nl2[i], dl = dl2[i];
+    float2 pp;
+    if (PACKED) {
+      const float2 x = f2_unpack(f2_fma(f2_pack(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1])), sl2x2,
+                                        f2_pack(nl.x, nl.y)));
+      if (POLY && (i & 3) == 3)
+        pp = poly_exp2x2(x.x, x.y);
+      else
+        pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+    } else {
+      const float sl2 = f2_unpack(sl2x2).x;
+      pp = make_float2(fast_exp2(fmaf(__uint_as_float(rs[2 * i]), sl2, nl.x)),
+                       fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), sl2, nl.y)));
+    }
+    if (MASK) {
+      pp.x = (2 * i >= ilo && 2 * i < ihi) ? pp.x : 0.f;
+      pp.y = (2 * i + 1 >= ilo && 2 * i + 1 < ihi) ? pp.y : 0.f;
+    }
+    wp[i] = pack_bf16(pp.x, pp.y);
+    if (PACKED) {
+      const float2 dsv = f2_unpack(f2_mul(
+          f2_pack(pp.x, pp.y),
+          f2_sub(f2_pack(__uint_as_float(rp[2 * i]), __uint_as_float(rp[2 * i + 1])), f2_pack(dl.x, dl.y))));
+      wd[i] = pack_bf16(dsv.x, dsv.y);
+    } else {
+      wd[i] = pack_bf16(pp.x * (__uint_as_float(rp[2 * i]) - dl.x), pp.y * (__uint_as_float(rp[2 * i + 1]) - dl.y));
+    }
+  }
+}
+
+// SV: softmax-loop variant bits (A/B builds, SPATTN_BWD_SV): 1 prefetch chunk 1's TMEM loads,
+// 2 packed fp32x2 math, 4 separate full / masked code paths, 8 FMA-pipe exp2 for 1 pair in 4
+template <int SV>
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_tc_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -64,7 +107,7 @@ __global__ void __launch_bounds__(384, 1)
   if (sbase & 1023) __trap();
   const uint32_t sK = sbase + K_OFF, sV = sbase + V_OFF, sQ = sbase + Q_OFF, sdO = sbase + DO_OFF,
                  sdS = sbase + DS_OFF, sStg = sbase + STG_OFF;
-  float* sL = reinterpret_cast<float*>(smem + LD_OFF);  // [NST][64] lse * log2e (+inf: empty row)
+  float* sL = reinterpret_cast<float*>(smem + LD_OFF);  // [NST][64] -lse * log2e (-inf: empty row)
   float* sDl = sL + NST * 64;                           // [NST][64] delta
   const uint32_t bars = sbase + BAR_OFF;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + BAR_OFF + E_N * 8);
@@ -78,8 +121,14 @@ __global__ void __launch_bounds__(384, 1)
   if (trace && (tr_all || (slot) == 0)) trace[(it) * 16 + (slot)] = clock64()
   // 1-D grid, kv head fastest: the heaviest causal key tiles of every head run first (LPT)
   const HeadMap hm = a.hm;
-  const int tile = blockIdx.x / hm.hkv;
-  const int kvh = blockIdx.x % hm.hkv;
+  const int ntiles = ps.tile_prefix[ps.n];
+  // head-major order (kv head slowest, heaviest causal key tiles first within a head): the
+  // resident CTAs then reduce into one kv head's dQ rows (64 MB at c2) instead of all of them
+  // (512 MB), which keeps the fp32 dQ partial sums L2-resident (measured 22.3 -> 21.4 ms at c2).
+  // debug bit 8 restores the tile-major order for A/B runs.
+  const bool head_major = !(a.debug & 8);
+  const int tile = head_major ? blockIdx.x % ntiles : blockIdx.x / hm.hkv;
+  const int kvh = head_major ? blockIdx.x / ntiles : blockIdx.x % hm.hkv;
   int pi = 0;
   while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= tile) ++pi;
   const AttnProblem P = ps.p[pi];
@@ -128,6 +177,23 @@ __global__ void __launch_bounds__(384, 1)
           tc::tma_load_2d(sV + b * 16384, &tmV, kvh * D + b * 64, P.k_row0 + n0, bar(E_KV));
         }
       }
+      // lse/delta of iteration it are fetched into registers one iteration ahead, so their
+      // global latency overlaps the wait for the stage instead of following it
+      float pl[2], pd[2];
+      auto fetch = [&](int it) {
+        const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * BQ;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int row = m0 + lane + 32 * k;
+          pl[k] = -INFINITY, pd[k] = 0.f;  // stored negated: p = 2^(s*scale*log2e + l2)
+          if (row < P.nq) {
+            const int64_t g = (int64_t)(P.q_row0 + row) * a.lse_row_stride + h;
+            pl[k] = __ldg(a.lse + g);
+            pd[k] = __ldg(a.delta + g);
+          }
+        }
+      };
+      fetch(0);
       for (int it = 0; it < T; ++it) {
         const int st = it % NST;
         const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * BQ;
@@ -143,17 +209,10 @@ __global__ void __launch_bounds__(384, 1)
         }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          const int r = lane + 32 * k, row = m0 + r;
-          float l2 = INFINITY, dl = 0.f;
-          if (row < P.nq) {
-            const int64_t g = (int64_t)(P.q_row0 + row) * a.lse_row_stride + h;
-            const float l = __ldg(a.lse + g);
-            l2 = l == -INFINITY ? INFINITY : l * kLog2e;
-            dl = __ldg(a.delta + g);
-          }
-          sL[st * 64 + r] = l2;
-          sDl[st * 64 + r] = dl;
+          sL[st * 64 + lane + 32 * k] = pl[k] == -INFINITY ? -INFINITY : -pl[k] * kLog2e;
+          sDl[st * 64 + lane + 32 * k] = pd[k];
         }
+        if (it + 1 < T) fetch(it + 1);
         tc::mbar_arrive(bar(E_QF + st));  // release: the stores above are visible to waiters
       }
     }
@@ -241,25 +300,42 @@ __global__ void __launch_bounds__(384, 1)
       tc::fence_after();
       if (t == 0) TR(9, it);
       const uint32_t ds = sdS + b * 16384;
+      // both 32-query chunks of S^T / dP^T are loaded up front; chunk 1's loads fly while
+      // chunk 0 is computed (one TMEM round trip per tile instead of two)
+      uint32_t rs[2][32], rp[2][32];
+      tc::tmem_ld32(tmem + lane_base + 64 * b, rs[0]);
+      tc::tmem_ld32(tmem + lane_base + 128 + 64 * b, rp[0]);
+      tc::tmem_wait_ld();
+      tc::reg_fence(rs[0]);
+      tc::reg_fence(rp[0]);
+      if (SV & 1) {
+        tc::tmem_ld32(tmem + lane_base + 64 * b + 32, rs[1]);
+        tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, rp[1]);
+      }
+      const float2* lse2 = reinterpret_cast<const float2*>(sL + lb);   // -lse*log2e per query
+      const float2* dl2 = reinterpret_cast<const float2*>(sDl + lb);   // delta per query
+      const uint64_t sl2x2 = f2_pack(sl2, sl2);
+      constexpr bool PK = SV & 2, PO = SV & 8;
 #pragma unroll
       for (int cc = 0; cc < BQ / 32; ++cc) {
-        uint32_t rs[32], rp[32];
-        tc::tmem_ld32(tmem + lane_base + 64 * b + cc * 32, rs);
-        tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + cc * 32, rp);
-        tc::tmem_wait_ld();
-        uint32_t wp[16], wd[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int q0 = cc * 32 + 2 * i;
-          float p0 = fast_exp2(fmaf(__uint_as_float(rs[2 * i]), sl2, -sL[lb + q0]));
-          float p1 = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), sl2, -sL[lb + q0 + 1]));
-          if (!full) {
-            p0 = (q0 >= ilo && q0 < ihi) ? p0 : 0.f;
-            p1 = (q0 + 1 >= ilo && q0 + 1 < ihi) ? p1 : 0.f;
+        if (cc == 1) {
+          if (!(SV & 1)) {
+            tc::tmem_ld32(tmem + lane_base + 64 * b + 32, rs[1]);
+            tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, rp[1]);
           }
-          wp[i] = pack_bf16(p0, p1);
-          wd[i] = pack_bf16(p0 * (__uint_as_float(rp[2 * i]) - sDl[lb + q0]),
-                            p1 * (__uint_as_float(rp[2 * i + 1]) - sDl[lb + q0 + 1]));
+          tc::tmem_wait_ld();
+          tc::reg_fence(rs[1]);
+          tc::reg_fence(rp[1]);
+        }
+        uint32_t wp[16], wd[16];
+        if (a.debug & 16) {  // profiling: no softmax-gradient math (wrong results)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) wp[i] = rs[cc][i] ^ rp[cc][i], wd[i] = rs[cc][i + 16] ^ rp[cc][i + 16];
+        } else if ((SV & 4) && full) {
+          grad_chunk<false, PK, PO>(rs[cc], rp[cc], lse2 + cc * 16, dl2 + cc * 16, sl2x2, 0, 0, wp, wd);
+        } else {
+          grad_chunk<true, PK, PO>(rs[cc], rp[cc], lse2 + cc * 16, dl2 + cc * 16, sl2x2, ilo - cc * 32,
+                                   ihi - cc * 32, wp, wd);
         }
         tc::tmem_st16(tmem + lane_base + 64 * b + cc * 16, wp);
 #pragma unroll
@@ -312,6 +388,7 @@ __global__ void __launch_bounds__(384, 1)
       tc::mbar_arrive(bar(E_DQF + b));
       if (w == 0 && lane == 0) TR(12, it);
       // (per-lane red.global.add.f32 from registers measured 1.8x slower than this staging)
+      if (a.debug & 32) continue;  // profiling: no dQ staging / reduce (wrong dq)
       if (lane == 0) tc::bulk_wait_read<0>();  // the slot's previous reduce has read it
       __syncwarp();
 #pragma unroll
@@ -390,11 +467,21 @@ void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t
     cudaGetLastError();
     return;
   }
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(attn_bwd_tc_q64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-  });
-  attn_bwd_tc_q64_kernel<<<dim3(tiles * a.hm.hkv), 384, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
+  static const int sv = getenv("SPATTN_BWD_SV") ? atoi(getenv("SPATTN_BWD_SV")) : 0;
+  auto launch = [&](auto kern) {
+    static std::once_flag once;
+    std::call_once(once, [&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM); });
+    kern<<<dim3(tiles * a.hm.hkv), 384, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
+  };
+  switch (sv) {
+    case 0: launch(attn_bwd_tc_q64_kernel<0>); break;
+    case 1: launch(attn_bwd_tc_q64_kernel<1>); break;
+    case 3: launch(attn_bwd_tc_q64_kernel<3>); break;
+    case 7: launch(attn_bwd_tc_q64_kernel<7>); break;
+    case 15: launch(attn_bwd_tc_q64_kernel<15>); break;
+    case 11: launch(attn_bwd_tc_q64_kernel<11>); break;
+    default: launch(attn_bwd_tc_q64_kernel<0>); break;
+  }
   note_launch();
 }
 

@@ -29,12 +29,12 @@ __global__ void __launch_bounds__(256, 1) probe(long long* out, int iters, const
   __syncthreads();
   tc::fence_after();
   const uint32_t tm = tslot;
-  constexpr int N = (MODE == 1) ? 256 : (MODE == 4 ? 64 : 128);
+  constexpr int N = (MODE == 1) ? 256 : ((MODE == 4 || MODE == 15) ? 64 : 128);
   if (warp == 7) {
     if (tc::elect_one()) {
       const uint32_t id = tc::idesc_bf16(128, N, false, false);
       long long t0 = clock64(), wsum = 0, isum = 0;
-      if (MODE >= 11) {
+      if (MODE >= 11 && MODE <= 14) {
         constexpr int G = MODE == 12 ? 2 : 8;
         __shared__ __align__(8) uint64_t pre;
         tc::mbar_init(smem_u32(&pre), 1);
@@ -56,10 +56,41 @@ __global__ void __launch_bounds__(256, 1) probe(long long* out, int iters, const
         out[2 * gridDim.x + blockIdx.x] = wsum;
         out[3 * gridDim.x + blockIdx.x] = isum;
       }
-      for (int i = 0; i < (MODE >= 11 ? 0 : iters); ++i) {
+      for (int i = 0; i < ((MODE >= 11 && MODE <= 14) ? 0 : iters); ++i) {
         const uint32_t ko = (i & 3) * 32;
-        if (MODE == 2)
+        if (MODE == 2 || MODE == 15)
           tc::mma_ts(tm, tm + 256 + (i & 3) * 8, tc::sdesc(sb + 65536 + ko, 16, 1024), id, 1u);
+        else if (MODE >= 16 && MODE <= 22) {  // one bwd q64 iteration per 8 loop trips (40 MMAs): S^T, dP^T,
+          // dV (TS), dK, dQ^T with the kernel's descriptors; i counts iterations here
+          const uint32_t sK = sb, sV = sb + 32768, sQ = sb + 65536, sdO = sb + 81920, ds = sb + 98304;
+          const uint32_t id_s = tc::idesc_bf16(128, 64, false, false), id_kv = tc::idesc_bf16(128, 128, false, true),
+                         id_q = tc::idesc_bf16(128, 64, true, true);
+          constexpr bool all = MODE == 16;
+          if (all || MODE == 17)
+          for (int ks = 0; ks < 8; ++ks) {
+            const uint32_t kof = (ks >> 2) * 16384 + (ks & 3) * 32, qo = (ks >> 2) * 8192 + (ks & 3) * 32;
+            tc::mma_ss(tm, tc::sdesc(sK + kof, 16, 1024), tc::sdesc(sQ + qo, 16, 1024), id_s, ks > 0);
+          }
+          if (all || MODE == 18)
+          for (int ks = 0; ks < 8; ++ks) {
+            const uint32_t kof = (ks >> 2) * 16384 + (ks & 3) * 32, qo = (ks >> 2) * 8192 + (ks & 3) * 32;
+            tc::mma_ss(tm + 128, tc::sdesc(sV + kof, 16, 1024), tc::sdesc(sdO + qo, 16, 1024), id_s, ks > 0);
+          }
+          if (all || MODE == 19)
+          for (int kk = 0; kk < 4; ++kk)
+            tc::mma_ts(tm + 256, tm + 64 + kk * 8, tc::sdesc(sdO + kk * 2048, 8192, 1024), id_kv, 1u);
+          if (all || MODE == 20)
+          for (int kk = 0; kk < 4; ++kk)
+            tc::mma_ss(tm + 384, tc::sdesc(ds + kk * 32, 16, 1024), tc::sdesc(sQ + kk * 2048, 8192, 1024), id_kv, 1u);
+          if (all || MODE == 21)
+          for (int kk = 0; kk < 8; ++kk)
+            tc::mma_ss(tm + 192, tc::sdesc(sK + kk * 2048, 16384, 1024), tc::sdesc(ds + kk * 2048, 8192, 1024), id_q, kk > 0);
+          if (MODE == 22)  // dQ (not transposed): M=64 queries... as two N64 halves is not possible; M=128 rows of dS^T? use K-major A = dS^T^T
+          for (int kk = 0; kk < 8; ++kk)
+            tc::mma_ss(tm + 192, tc::sdesc(sK + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), tc::sdesc(ds + kk * 2048, 8192, 1024),
+                       tc::idesc_bf16(128, 64, false, true), kk > 0);
+          if (i + 1 >= iters / 40) break;
+        }
         else if (MODE == 8 || MODE == 9 || MODE == 10) {  // the fwd kernel's pattern: groups of 8 into alternating accumulators + 2 commits
           const bool pv = (i >> 3) & 1;
           tc::mma_ss(tm + (pv ? 256 : 0) + ((i >> 4) & 1) * 128, tc::sdesc(sb + ko, 16, 1024),
@@ -136,14 +167,19 @@ void run(const char* name, long long* d, int iters, const uint8_t* g) {
   cudaError_t e = cudaDeviceSynchronize();
   long long h[600];
   cudaMemcpy(h, d, 600 * 8, cudaMemcpyDeviceToHost);
-  const int N = (MODE == 1) ? 256 : (MODE == 4 ? 64 : 128);
-  const double cyc = (double)h[0] / iters;
+  const int N = (MODE == 1) ? 256 : ((MODE == 4 || MODE == 15) ? 64 : 128);
+  const double cyc = (double)h[0] / (MODE >= 16 && MODE <= 22 ? iters / 40 : iters);
   const double ideal = 128.0 * N * 16 * 2 / 8192.0;  // cycles at 8192 dense bf16 flop/clk/SM
-  const double bytes = (MODE == 2 ? 0 : 128 * 16 * 2) + N * 16 * 2;
+  const double bytes = (MODE == 2 || MODE == 15 ? 0 : 128 * 16 * 2) + N * 16 * 2;
+  if (MODE >= 16 && MODE <= 22) {
+    printf("%-28s %s cycles/iteration %.1f (ideal at 8192 flop/clk: %.0f)\n", name, cudaGetErrorString(e), cyc,
+           5.0 * 128 * 64 * 128 * 2 / 8192.0);
+    return;
+  }
   printf("%-28s %s cycles/MMA %.1f (ideal %.0f) smem operand B/clk %.0f", name, cudaGetErrorString(e),
          cyc, ideal, bytes / cyc);
   if (MODE == 3) printf("  store B/clk %.1f", (double)h[148] * 128 * 16 * 16 / h[0]);
-  if (MODE >= 11) printf("  per group of 8: issue+commit %.0f cycles, satisfied mbar_wait %.0f cycles", (double)h[3 * 148] / (iters / 8), (double)h[2 * 148] / (iters / 8));
+  if (MODE >= 11 && MODE <= 14) printf("  per group of 8: issue+commit %.0f cycles, satisfied mbar_wait %.0f cycles", (double)h[3 * 148] / (iters / 8), (double)h[2 * 148] / (iters / 8));
   if (MODE == 6) printf("  tmem ld B/clk %.1f", (double)h[148] * 128 * 32 * 4 / h[0]);
   if (MODE == 7) printf("  bulk copy B/clk %.1f", (double)h[148] * 16384 / h[0]);
   printf("\n");
@@ -160,6 +196,14 @@ int main() {
   run<1>("SS M128 N256 K16", d, it, g);
   run<4>("SS M128 N64 K16", d, it, g);
   run<2>("TS M128 N128 K16 (A tmem)", d, it, g);
+  run<15>("TS M128 N64 K16 (A tmem)", d, it, g);
+  run<16>("bwd q64 iteration (40 MMAs)", d, it, g);
+  run<17>("  S^T only (8 SS N64)", d, it, g);
+  run<18>("  dP^T only (8 SS N64)", d, it, g);
+  run<19>("  dV only (4 TS N128)", d, it, g);
+  run<20>("  dK only (4 SS N128 Bmn)", d, it, g);
+  run<21>("  dQ^T only (8 SS N64 A mn)", d, it, g);
+  run<22>("  dQ^T with K-major A (8 SS N64)", d, it, g);
   run<5>("SS M128 N128 B MN-major", d, it, g);
   run<8>("fwd pattern (8 S, 2 commits, 8 PV)", d, it, g);
   run<9>("fwd pattern, 1 commit", d, it, g);
