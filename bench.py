@@ -174,6 +174,8 @@ def main():
     ap.add_argument("--family", default="tcgen05", choices=["tcgen05", "mma", "tcgen05_pp"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-groups", type=int, default=0,
+                    help="kv-head groups of the pipelined host step (0 = library default)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args, args.config)
@@ -261,33 +263,36 @@ def main():
     C.check(C.lib().spattn_profile_read(kms, kn))
     tokens_per_s = L / (ms / 1000.0)
 
-    # e2e through the public API with host buffers: H2D of q, k, v, dout from pinned memory,
-    # fwd + bwd, D2H of dq, dk, dv (the step's result) inside the timed region
+    # e2e through the C-ABI with HOST buffers (spattn_step_host): the H2D of q, k, v, dout
+    # from pinned memory, fwd + bwd, and the D2H of dq, dk, dv (the step's result) are all
+    # inside the timed region; the library pipelines the copies against the kernels over
+    # kv-head groups
     e2e = None
     if not args.no_e2e:
         hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, do))
         hdq, hdk, hdv = (torch.empty_like(x, device="cpu").pin_memory() for x in (dq, dk, dv))
+
+        def host_step():
+            C.check(C.lib().spattn_step_host(
+                ctx, eid, ctypes.byref(cfg), ctypes.byref(lay), 1, hq.data_ptr(), hk.data_ptr(),
+                hv.data_ptr(), hdo.data_ptr(), None, None, hdq.data_ptr(), hdk.data_ptr(),
+                hdv.data_ptr(), None, 0, args.e2e_groups))
+
         for _ in range(2):
-            for src, dst in ((hq, q), (hk, k), (hv, v), (hdo, do)):
-                dst.copy_(src, non_blocking=True)
-            step(*ptrs)
-            for src, dst in ((dq, hdq), (dk, hdk), (dv, hdv)):
-                dst.copy_(src, non_blocking=True)
+            host_step()
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            for src, dst in ((hq, q), (hk, k), (hv, v), (hdo, do)):
-                dst.copy_(src, non_blocking=True)
-            step(*ptrs)
-            for src, dst in ((dq, hdq), (dk, hdk), (dv, hdv)):
-                dst.copy_(src, non_blocking=True)
+            host_step()
         ev1.record(stream)
         barrier()
         ems = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
         h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hdo))
         d2h = sum(x.numel() * x.element_size() for x in (hdq, hdk, hdv))
         e2e = {"value": L / (ems / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ems}
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems,
+               "api": "spattn_step_host (C ABI, pinned host buffers)",
+               "head_groups": args.e2e_groups or C.lib().spattn_pick_step_groups(eid, ctypes.byref(cfg), sp)}
 
     burst, sustained, hbm, src = peaks()
     # algorithmic flops of this rank's attention kernels per step (reference counters:

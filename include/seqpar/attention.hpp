@@ -76,6 +76,17 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& saved, const Device
                                    const DeviceTensor& dq, const DeviceTensor& dk,
                                    const DeviceTensor& dv);
 
+// One fwd+bwd step of the layer on HOST buffers (host_step.cpp): the reference's
+// run_attention_engine + tape.backward on host tensors, with the H2D / D2H traffic of
+// independent kv-head groups overlapped with compute. All buffers are [bs, local_len, heads,
+// dim] bf16 (lse fp32 [bs, local_len, heads]); out / lse may be null. groups <= 0 picks the
+// largest of 8, 4, 2, 1 the engine's head constraints allow (pick_step_groups).
+void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig& cfg,
+                             const ShardLayout& layout, int64_t bs, const void* hq, const void* hk,
+                             const void* hv, const void* hdout, void* hout, float* hlse, void* hdq,
+                             void* hdk, void* hdv, const Documents* docs, int groups);
+int pick_step_groups(Engine e, const AttentionConfig& cfg, int sp);
+
 // rope_apply (tensor.cpp:548-607) on a bf16 [bs, len, heads, dim] device tensor (inverse:
 // the backward's rotation, tensor.cpp:589-600); out may alias x.
 void rope_apply(cudaStream_t s, int64_t bs, int64_t len, int64_t heads, int dim, const void* x,

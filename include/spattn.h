@@ -133,6 +133,19 @@ int spattn_bwd(spattn_ctx* ctx, spattn_saved* saved, const void* dout, void* dq,
                void* dv);
 void spattn_saved_free(spattn_saved* saved);
 
+/* One training step (fwd + bwd) of the layer on HOST buffers (pinned for full overlap):
+ * run_attention_engine + the tape backward on host tensors, as the reference runs them
+ * (attention.cpp:526-574). The step is pipelined over `groups` independent kv-head groups
+ * (0 = auto) so the H2D of q/k/v/dout and the D2H of dq/dk/dv overlap the attention kernels.
+ * Shapes as spattn_fwd; out and lse may be NULL. Returns when the host results are written. */
+int spattn_step_host(spattn_ctx* ctx, int engine, const spattn_config* cfg,
+                     const spattn_layout* layout, int64_t bs, const void* q, const void* k,
+                     const void* v, const void* dout, void* out, float* lse, void* dq, void* dk,
+                     void* dv, const int64_t* doc_lens, int n_docs, int groups);
+
+/* The head-group count spattn_step_host uses when groups = 0. */
+int spattn_pick_step_groups(int engine, const spattn_config* cfg, int sp);
+
 /* Loopback group drivers: one call runs every rank on its own thread (arrays of world
  * pointers), returning when all ranks' streams are idle. */
 int spattn_fabric_fwd(spattn_fabric* f, int engine, const spattn_config* cfg,

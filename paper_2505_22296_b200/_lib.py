@@ -29,6 +29,7 @@ EXPORTS = [
     "spattn_shard_rows", "spattn_gather_rows", "spattn_launch_count", "spattn_profile_enable",
     "spattn_profile_read", "spattn_selftest_umma", "spattn_plan_heads", "spattn_plan_problems",
     "spattn_debug_bwd_trace", "spattn_fwd_rope", "spattn_fabric_fwd_rope", "spattn_rope_apply",
+    "spattn_step_host", "spattn_pick_step_groups",
 ]
 
 
@@ -115,6 +116,8 @@ def lib() -> ctypes.CDLL:
                                    ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                                    ctypes.POINTER(_vp), _i64p, _i32, ctypes.POINTER(_i64p),
                                    ctypes.c_double, ctypes.POINTER(_vp)],
+        "spattn_pick_step_groups": [_i32, cfgp, _i32],
+        "spattn_step_host": [_vp, _i32, cfgp, layp, _i64] + [_vp] * 9 + [_i64p, _i32, _i32],
         "spattn_rope_apply": [_vp, _i64, _i64, _i32, _i32, _vp, _i64p, ctypes.c_double, _i32, _vp],
         "spattn_fabric_bwd": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                               ctypes.POINTER(_vp), ctypes.POINTER(_vp)],

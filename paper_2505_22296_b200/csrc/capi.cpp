@@ -466,3 +466,26 @@ extern "C" int spattn_rope_apply(void* stream, int64_t bs, int64_t len, int head
                        std::vector<int64_t>(position_ids, position_ids + len), base, inverse != 0, out);
   });
 }
+
+extern "C" int spattn_step_host(spattn_ctx* ctx, int engine, const spattn_config* cfg,
+                                const spattn_layout* layout, int64_t bs, const void* q,
+                                const void* k, const void* v, const void* dout, void* out,
+                                float* lse, void* dq, void* dk, void* dv, const int64_t* doc_lens,
+                                int n_docs, int groups) {
+  return guard([&] {
+    const auto c = make_cfg(cfg);
+    const auto L = make_layout(layout);
+    (void)views(c, L, bs, q, k, v, out ? out : dq);  // shape / config validation
+    const auto D = docs_of(doc_lens, n_docs);
+    seqpar::run_attention_step_host(*ctx->rc, make_engine(engine), c, L, bs, q, k, v, dout, out, lse,
+                                    dq, dk, dv, D.get(), groups);
+  });
+}
+
+extern "C" int spattn_pick_step_groups(int engine, const spattn_config* cfg, int sp) {
+  try {
+    return seqpar::pick_step_groups(make_engine(engine), make_cfg(cfg), sp);
+  } catch (...) {
+    return 1;
+  }
+}

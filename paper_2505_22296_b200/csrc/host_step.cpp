@@ -1,0 +1,165 @@
+// One training step of the SP attention layer on HOST buffers — the reference's
+// run_attention_engine + tape.backward on host tensors (attention.cpp:526-574, the tape
+// closures :236-258 / :290-339; the reference keeps every tensor in host memory) — with the
+// host<->device traffic overlapped with compute.
+//
+// Attention heads are independent, so the step is cut into `groups` kv-head groups (each a
+// valid engine call on heads/groups query heads and kv_heads/groups kv heads, the same math on
+// a head subset). Three streams pipeline them: the H2D of group g+1 (pitched copies out of the
+// [bs, len, heads, dim] host rows) and the D2H of group g-1 run on copy streams while group g's
+// forward + backward run on the context's compute stream. Double-buffered device slots.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "seqpar/attention.hpp"
+
+namespace seqpar {
+namespace {
+
+#define HS_CUDA(x)                                                                            \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess) throw StateError(std::string("CUDA: ") + cudaGetErrorString(e_) + \
+                                            " at " #x);                                       \
+  } while (0)
+
+struct Slot {
+  void *q = nullptr, *k = nullptr, *v = nullptr, *dout = nullptr, *out = nullptr;
+  void *dq = nullptr, *dk = nullptr, *dv = nullptr;
+  float* lse = nullptr;
+  cudaEvent_t loaded = nullptr, computed = nullptr, drained = nullptr;
+};
+
+bool group_ok(Engine e, const AttentionConfig& c, int sp, int ng) {
+  const int H = c.heads, Hkv = c.kv_heads > 0 ? c.kv_heads : c.heads;
+  if (ng < 1 || H % ng || Hkv % ng) return false;
+  const int hg = H / ng;
+  switch (e) {
+    case Engine::ulysses: return hg % sp == 0;
+    case Engine::dummy_head:  // no extra dummy heads: groups pad exactly as the whole would
+      return static_cast<int64_t>((hg + sp - 1) / sp) * sp * ng == static_cast<int64_t>((H + sp - 1) / sp) * sp;
+    case Engine::xtuner: return ng == 1;
+    case Engine::usp: return c.ulysses_degree > 0 && hg % c.ulysses_degree == 0;
+    default: return true;
+  }
+}
+
+}  // namespace
+
+int pick_step_groups(Engine e, const AttentionConfig& c, int sp) {
+  for (int ng : {8, 4, 2})
+    if (group_ok(e, c, sp, ng)) return ng;
+  return 1;
+}
+
+void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig& cfg,
+                             const ShardLayout& layout, int64_t bs, const void* hq, const void* hk,
+                             const void* hv, const void* hdout, void* hout, float* hlse, void* hdq,
+                             void* hdk, void* hdv, const Documents* docs, int groups) {
+  const int H = cfg.heads, Hkv = cfg.kv_heads > 0 ? cfg.kv_heads : cfg.heads, d = cfg.head_dim;
+  const int sp = layout.sp;
+  const int ng = groups > 0 ? groups : pick_step_groups(engine, cfg, sp);
+  if (!group_ok(engine, cfg, sp, ng))
+    throw ConfigError("host step: " + std::to_string(ng) + " head groups do not split heads=" +
+                      std::to_string(H) + ", kv_heads=" + std::to_string(Hkv) + " for engine " +
+                      engine_name(engine) + " at sp=" + std::to_string(sp));
+  if (!hq || !hk || !hv || !hdout || !hdq || !hdk || !hdv) throw ShapeError("host step: null buffer");
+  const int64_t lloc = layout.local_len();
+  const int64_t rows = bs * lloc;
+  const int hg = H / ng, kg = Hkv / ng;
+  AttentionConfig gc = cfg;
+  gc.heads = hg;
+  gc.kv_heads = kg;
+  const size_t qb = static_cast<size_t>(rows * hg * d * 2), kb = static_cast<size_t>(rows * kg * d * 2);
+  const size_t qpitch = static_cast<size_t>(H) * d * 2, kpitch = static_cast<size_t>(Hkv) * d * 2;
+  const size_t qw = static_cast<size_t>(hg) * d * 2, kw = static_cast<size_t>(kg) * d * 2;
+
+  cudaStream_t cs = ctx.stream, up = nullptr, down = nullptr;
+  HS_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+  HS_CUDA(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+  const int nslots = std::min(ng, 2);
+  std::vector<Slot> slots(static_cast<size_t>(nslots));
+  auto cleanup = [&] {
+    for (auto& s : slots) {
+      for (void* p : {s.q, s.k, s.v, s.dout, s.out, s.dq, s.dk, s.dv, static_cast<void*>(s.lse)})
+        if (p) cudaFreeAsync(p, cs);
+      for (cudaEvent_t e : {s.loaded, s.computed, s.drained})
+        if (e) cudaEventDestroy(e);
+    }
+    cudaStreamSynchronize(up);
+    cudaStreamSynchronize(down);
+    cudaStreamDestroy(up);
+    cudaStreamDestroy(down);
+  };
+  try {
+    for (auto& s : slots) {
+      for (void** p : {&s.q, &s.dout, &s.out, &s.dq}) HS_CUDA(cudaMallocAsync(p, qb, cs));
+      for (void** p : {&s.k, &s.v, &s.dk, &s.dv}) HS_CUDA(cudaMallocAsync(p, kb, cs));
+      HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s.lse), static_cast<size_t>(rows * hg * 4), cs));
+      for (cudaEvent_t* e : {&s.loaded, &s.computed, &s.drained})
+        HS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    // slots allocated on the compute stream must exist before the copy streams touch them
+    cudaEvent_t ready;
+    HS_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    HS_CUDA(cudaEventRecord(ready, cs));
+    HS_CUDA(cudaStreamWaitEvent(up, ready, 0));
+    HS_CUDA(cudaStreamWaitEvent(down, ready, 0));
+    cudaEventDestroy(ready);
+
+    auto h2d = [&](void* dst, const void* src, size_t col_bytes, size_t width, size_t pitch) {
+      HS_CUDA(cudaMemcpy2DAsync(dst, width, static_cast<const char*>(src) + col_bytes, pitch, width,
+                                static_cast<size_t>(rows), cudaMemcpyHostToDevice, up));
+    };
+    auto d2h = [&](void* dst, const void* src, size_t col_bytes, size_t width, size_t pitch) {
+      HS_CUDA(cudaMemcpy2DAsync(static_cast<char*>(dst) + col_bytes, pitch, src, width, width,
+                                static_cast<size_t>(rows), cudaMemcpyDeviceToHost, down));
+    };
+    auto load = [&](int g) {
+      Slot& s = slots[static_cast<size_t>(g % nslots)];
+      if (g >= nslots) HS_CUDA(cudaStreamWaitEvent(up, s.drained, 0));  // slot's last use done
+      h2d(s.q, hq, g * qw, qw, qpitch);
+      h2d(s.k, hk, g * kw, kw, kpitch);
+      h2d(s.v, hv, g * kw, kw, kpitch);
+      h2d(s.dout, hdout, g * qw, qw, qpitch);
+      HS_CUDA(cudaEventRecord(s.loaded, up));
+    };
+    load(0);
+    for (int g = 0; g < ng; ++g) {
+      if (g + 1 < ng) load(g + 1);
+      Slot& s = slots[static_cast<size_t>(g % nslots)];
+      HS_CUDA(cudaStreamWaitEvent(cs, s.loaded, 0));
+      const DeviceTensor tq{s.q, bs, lloc, hg, d}, tk{s.k, bs, lloc, kg, d}, tv{s.v, bs, lloc, kg, d};
+      const DeviceTensor to{s.out, bs, lloc, hg, d};
+      SavedPtr saved = run_attention_engine(ctx, engine, gc, layout, tq, tk, tv, to, s.lse, docs);
+      run_attention_engine_backward(ctx, *saved, DeviceTensor{s.dout, bs, lloc, hg, d},
+                                    DeviceTensor{s.dq, bs, lloc, hg, d}, DeviceTensor{s.dk, bs, lloc, kg, d},
+                                    DeviceTensor{s.dv, bs, lloc, kg, d});
+      saved.reset();
+      HS_CUDA(cudaEventRecord(s.computed, cs));
+      HS_CUDA(cudaStreamWaitEvent(down, s.computed, 0));
+      d2h(hdq, s.dq, g * qw, qw, qpitch);
+      d2h(hdk, s.dk, g * kw, kw, kpitch);
+      d2h(hdv, s.dv, g * kw, kw, kpitch);
+      if (hout) d2h(hout, s.out, g * qw, qw, qpitch);
+      if (hlse)
+        HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(hlse) + static_cast<size_t>(g) * hg * 4,
+                                  static_cast<size_t>(H) * 4, s.lse, static_cast<size_t>(hg) * 4,
+                                  static_cast<size_t>(hg) * 4, static_cast<size_t>(rows),
+                                  cudaMemcpyDeviceToHost, down));
+      HS_CUDA(cudaEventRecord(s.drained, down));
+    }
+    // the step completes on the compute stream (callers time / synchronise it)
+    HS_CUDA(cudaStreamWaitEvent(cs, slots[static_cast<size_t>((ng - 1) % nslots)].drained, 0));
+    if (nslots > 1) HS_CUDA(cudaStreamWaitEvent(cs, slots[static_cast<size_t>((ng - 2) % nslots)].drained, 0));
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
+}  // namespace seqpar

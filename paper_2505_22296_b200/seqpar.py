@@ -436,6 +436,47 @@ class RankContext:
         return out
 
 
+def attention_step_host(engine: str, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                        dout: torch.Tensor, rank_ctx: Optional["RankContext"] = None,
+                        seq_len: Optional[int] = None, layout: str = "auto", causal: bool = True,
+                        ulysses_degree: int = 0, ring_degree: int = 0,
+                        docs: Optional[Sequence[int]] = None, groups: int = 0,
+                        want_out: bool = False):
+    """One fwd+bwd step of the layer on HOST (CPU, ideally pinned) bf16 tensors of this rank's
+    shard — run_attention_engine + the tape backward as the reference runs them on host
+    tensors — with the H2D/D2H copies pipelined against the kernels over kv-head groups
+    (spattn_step_host). Returns (dq, dk, dv) or (dq, dk, dv, out, lse) CPU tensors."""
+    for t in (q, k, v, dout):
+        if t.is_cuda or t.dtype != torch.bfloat16:
+            raise ShapeError("attention_step_host: q, k, v, dout must be bf16 CPU tensors")
+    bs, lloc, H, d = q.shape
+    Hkv = k.shape[2]
+    sp = rank_ctx.sp if rank_ctx is not None else 1
+    mode, lay = _layout_for(layout, engine, seq_len or lloc * sp, sp, ulysses_degree, ring_degree)
+    cfg = C.make_config(H, Hkv, d, causal, ulysses_degree, ring_degree)
+    if rank_ctx is None:
+        fab = Fabric(1)
+        h = fab.ctxs[0]
+    else:
+        fab, h = None, rank_ctx._h
+    C.check(C.lib().spattn_ctx_set_stream(h, _stream()))
+    pin = lambda t: t.contiguous() if t.is_pinned() else t.contiguous().pin_memory()  # noqa: E731
+    q, k, v, dout = (pin(t) for t in (q, k, v, dout))
+    dq, dk, dv = (torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (q, k, v))
+    out = torch.empty(q.shape, dtype=q.dtype).pin_memory() if want_out else None
+    lse = torch.empty(q.shape[:3], dtype=torch.float32).pin_memory() if want_out else None
+    nd = 0 if docs is None else len(docs)
+    darr = None if docs is None else (ctypes.c_int64 * nd)(*docs)
+    C.check(C.lib().spattn_step_host(
+        h, C.engine_id(engine), ctypes.byref(cfg), ctypes.byref(lay), bs, q.data_ptr(),
+        k.data_ptr(), v.data_ptr(), dout.data_ptr(), out.data_ptr() if want_out else None,
+        lse.data_ptr() if want_out else None, dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), darr, nd,
+        groups))
+    torch.cuda.current_stream().synchronize()
+    del fab
+    return (dq, dk, dv, out, lse) if want_out else (dq, dk, dv)
+
+
 class _RankEngine(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, rc, engine, cfg, lay, docs, pos=None):

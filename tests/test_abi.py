@@ -63,3 +63,14 @@ def test_errors_map_to_value_error():
         P.shard_positions("bogus", 16, 2, 0)
     msg = C.lib().spattn_last_error().decode()
     assert msg  # thread-local message of the last failing call
+
+
+def test_binding_arity_matches_header():
+    """Every ctypes binding declares as many arguments as the C prototype has parameters."""
+    text = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "spattn.h")).read(), flags=re.S)
+    L = C.lib()
+    for m in re.finditer(r"\b(spattn_\w+)\s*\(([^)]*)\)\s*;", text):
+        name, params = m.group(1), m.group(2).strip()
+        n = 0 if params in ("", "void") else params.count(",") + 1
+        at = getattr(L, name).argtypes
+        assert at is None or len(at) == n, (name, n, len(at))

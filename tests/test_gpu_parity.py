@@ -214,3 +214,24 @@ def test_native_bytes_closed_form(P):
     got_r = P.measure_engine_bytes("ring", L, H, Hkv, d, sp)
     Xkv = X * Hkv * d
     assert got_r == (sp - 1) * 2 * Xkv * 2 + sp * (2 * Xkv * 2 + 2 * Xkv * 4)
+
+
+@pytest.mark.parametrize("L,H,Hkv,d,groups", [(256, 8, 4, 128, 0), (256, 8, 4, 64, 2),
+                                              (192, 4, 2, 128, 1), (320, 8, 8, 64, 4)])
+def test_host_step_matches_oracle(P, L, H, Hkv, d, groups):
+    """spattn_step_host: host buffers in, host gradients out, copies pipelined over kv-head
+    groups — the same math as the device path."""
+    P.set_kernel_family("tcgen05")
+    q, k, v, R = parity_inputs(500 + L + groups, L, H, Hkv, d)
+    cpu = lambda x: torch.from_numpy(x).to(torch.bfloat16)  # noqa: E731
+    dq, dk, dv, out, lse = P.attention_step_host("oracle", cpu(q), cpu(k), cpu(v), cpu(R),
+                                                 groups=groups, want_out=True)
+    res = {"out": np_(out), "lse": np_(lse), "dq": np_(dq), "dk": np_(dk), "dv": np_(dv)}
+    check_all(res, oracle_all(q, k, v, R), torch_ref(q, k, v, R))
+
+
+def test_host_step_ulysses_loopback_rejects_bad_groups(P):
+    q = torch.zeros(1, 64, 6, 64, dtype=torch.bfloat16)
+    k = torch.zeros(1, 64, 3, 64, dtype=torch.bfloat16)
+    with pytest.raises(P.ConfigError):
+        P.attention_step_host("oracle", q, k, k, q, groups=4)
