@@ -142,6 +142,13 @@ class LoopbackFabric {
 // One process per GPU; NCCL loaded at run time (libnccl.so.2, the copy torch already mapped).
 // `unique_id` is the 128-byte ncclUniqueId rank 0 created (spattn_nccl_unique_id) and the
 // launcher broadcast.
+// replicate_packing_mask (partition.cpp:222-227) over broadcast_bytes (comm.cpp:526-545):
+// group index 0 supplies the neat-packing mask (other ranks pass anything, e.g. empty); every
+// member returns the root's bytes. The mask is replicated, not split. Counted
+// as one broadcast of size*(g-1)/g bytes per rank, as the reference counts it.
+std::vector<uint8_t> replicate_packing_mask(RankCtx& ctx, const CommGroup& group,
+                                            const std::vector<uint8_t>& mask);
+
 std::unique_ptr<Transport> make_nccl_transport(int rank, int world, const void* unique_id,
                                                int device);
 void nccl_unique_id(void* out128);

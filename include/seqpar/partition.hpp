@@ -55,6 +55,37 @@ int64_t dummy_head_bytes(int64_t bs, int64_t len, int64_t heads, int64_t head_di
 int64_t xtuner_bytes(int64_t bs, int64_t len, int64_t heads, int64_t head_dim, int sp);
 int64_t usp_bytes(int64_t bs, int64_t len, int64_t heads, int64_t head_dim, int u, int r);
 
+// ---- batches, padding and neat-packing metadata (partition.hpp:92-125, partition.cpp:164-227)
+constexpr int64_t kIgnoreLabel = -100;
+constexpr int64_t kNoImage = -1;
+constexpr int64_t kNoSegment = -1;
+
+struct TrainBatch {  // partition.hpp:96-105
+  std::vector<int64_t> tokens;
+  std::vector<int64_t> labels;        // kIgnoreLabel marks unsupervised slots
+  std::vector<int64_t> position_ids;  // [0..len) before sharding
+  std::vector<int64_t> segment_ids;   // optional (empty when absent)
+  std::vector<int64_t> image_map;     // optional; kNoImage for text positions
+  int64_t len() const { return static_cast<int64_t>(tokens.size()); }
+  void validate() const;  // partition.cpp:164-177
+};
+
+// partition.cpp:202-215: extends every field to pad_length(len, sp, cutoff, pad_to_cutoff)
+// with its sentinel (pad_token, kIgnoreLabel, iota positions, kNoSegment, kNoImage).
+TrainBatch pad_batch(const TrainBatch& batch, int sp, int64_t pad_token, int64_t cutoff_len,
+                     bool pad_to_cutoff = false);
+// partition.cpp:217-220 / :124-139: the layout's rows of any per-position int64 field
+std::vector<int64_t> shard(const std::vector<int64_t>& values, const ShardLayout& layout, int index);
+std::vector<int64_t> split_position_map(const std::vector<int64_t>& image_map,
+                                        const ShardLayout& layout, int index);
+
+// B200 bridge from the packed batch to the varlen kernels (the reference keeps segment ids
+// but never wires them into attention, model.cpp:339-351): consecutive runs of equal segment
+// ids become documents (a kNoSegment tail — pad_batch padding — is one more document, so real
+// tokens never attend to padding), and rope position ids restart at 0 in every document.
+std::vector<int64_t> documents_from_segments(const std::vector<int64_t>& segment_ids);
+std::vector<int64_t> document_position_ids(const std::vector<int64_t>& doc_lens);
+
 // Contiguous position runs of a position list: rows [row0, row0+n) hold positions
 // [pos0, pos0+n). The kernels work on runs instead of per-row position arrays.
 struct PosRun {

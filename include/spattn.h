@@ -63,6 +63,32 @@ int spattn_pick_xtuner_insp(int heads, int sp, int head_dim, int* out);
 int spattn_reference_bytes(int engine, int64_t bs, int64_t len, int64_t heads, int64_t head_dim,
                            int sp, int u, int r, int64_t* out);
 
+/* ---- batches, padding and neat-packing metadata (partition.hpp:92-125) ---- */
+/* pad_batch (partition.cpp:202-215): every field extended to *out_len = pad_length(len, sp,
+ * cutoff_len, pad_to_cutoff) entries with its sentinel (pad_token, -100, iota, -1, -1).
+ * segment_ids / image_map may be NULL (then their outputs are untouched); out arrays hold
+ * *out_len entries (query pad_length first). */
+int spattn_pad_batch(const int64_t* tokens, const int64_t* labels, const int64_t* position_ids,
+                     const int64_t* segment_ids, const int64_t* image_map, int64_t len, int sp,
+                     int64_t pad_token, int64_t cutoff_len, int pad_to_cutoff, int64_t* out_len,
+                     int64_t* out_tokens, int64_t* out_labels, int64_t* out_position_ids,
+                     int64_t* out_segment_ids, int64_t* out_image_map);
+/* split_position_map / shard (partition.cpp:217-220, :124-139) of a per-position int64 field:
+ * out holds global_len/sp entries */
+int spattn_split_position_map(const spattn_layout* layout, int index, const int64_t* values,
+                              int64_t* out);
+/* Neat-packing bridge to the varlen kernels: runs of equal segment ids -> document lengths
+ * (a -1 padding tail is one more document); ConfigError when an id is not one run. */
+int spattn_documents_from_segments(const int64_t* segment_ids, int64_t len, int64_t* doc_lens,
+                                   int max_docs, int* n_docs);
+/* replicate_packing_mask (partition.cpp:222-227): group index 0's bytes to every member over
+ * the context's transport; out holds cap bytes, *out_len receives the mask length. */
+int spattn_replicate_packing_mask(spattn_ctx* ctx, const uint8_t* mask, int64_t len, uint8_t* out,
+                                  int64_t cap, int64_t* out_len);
+int spattn_fabric_replicate_packing_mask(spattn_fabric* f, const uint8_t* const* masks,
+                                         const int64_t* lens, uint8_t* const* outs, int64_t cap,
+                                         int64_t* out_lens);
+
 /* Host planners of the engines (no GPU): per-member head windows of the Ulysses
  * head<->sequence moves (query heads [q_lo, q_lo+q_n), kv heads [kv_lo, kv_lo+kv_n); dummy
  * heads are virtual), and the attention problems two position lists reduce to: rows of 6

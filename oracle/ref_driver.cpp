@@ -9,6 +9,9 @@
 //       sharded run gathered to global order (mirrors report.cpp:95-133) + per-rank bytes
 //   ref_driver bench <engine> <sp> <L> <heads> <kv> <dim> <steps>
 //       wall time of fwd+bwd of run_attention_engine, one thread per rank (comm.cpp:197-222)
+//   ref_driver batch <len> <sp> <cutoff> <pad_to_cutoff> <seed>
+//       pad_batch (partition.cpp:202-215) of a random packed batch, split_position_map of its
+//       image map over zigzag(sp), replicate_packing_mask over sp ranks: JSON on stdout
 //   ref_driver rope <L> <heads> <dim> <pos_scale> <pos_offset> <seed> <out.bin>
 //       rope_apply (tensor.cpp:548-607) of x ~ U(-2,2) at ids i*scale+offset, loss sum(y*R)
 //   ref_driver rope_engine <engine> <sp> <L> <heads> <kv> <dim> <u> <r> <pos_scale>
@@ -169,6 +172,60 @@ int engine(int argc, char** argv, int64_t rope_scale = 0, int64_t rope_offset = 
   return 0;
 }
 
+void put_json(const char* name, const std::vector<int64_t>& v, bool last = false) {
+  std::printf("\"%s\": [", name);
+  for (size_t i = 0; i < v.size(); ++i) std::printf("%s%lld", i ? ", " : "", static_cast<long long>(v[i]));
+  std::printf("]%s", last ? "" : ", ");
+}
+
+int batch(int argc, char** argv) {
+  if (argc != 7) return 2;
+  const int64_t len = std::atoll(argv[2]);
+  const int sp = std::atoi(argv[3]);
+  const int64_t cutoff = std::atoll(argv[4]);
+  const bool to_cutoff = std::atoi(argv[5]) != 0;
+  Rng rng(std::strtoull(argv[6], nullptr, 10));
+  TrainBatch b;
+  int64_t seg = 0, left = 0;
+  for (int64_t i = 0; i < len; ++i) {
+    if (left == 0) left = rng.uniform_int(1, 9), ++seg;
+    --left;
+    b.tokens.push_back(rng.uniform_int(0, 1000));
+    b.labels.push_back(rng.uniform_int(0, 3) == 0 ? kIgnoreLabel : b.tokens.back());
+    b.position_ids.push_back(i);
+    b.segment_ids.push_back(seg - 1);
+    b.image_map.push_back(rng.uniform_int(0, 2) == 0 ? rng.uniform_int(0, 50) : kNoImage);
+  }
+  TrainBatch p = pad_batch(b, sp, /*pad_token=*/7, cutoff, to_cutoff);
+  std::printf("{");
+  put_json("tokens", b.tokens), put_json("labels", b.labels), put_json("segment_ids", b.segment_ids);
+  put_json("image_map", b.image_map);
+  put_json("p_tokens", p.tokens), put_json("p_labels", p.labels), put_json("p_position_ids", p.position_ids);
+  put_json("p_segment_ids", p.segment_ids), put_json("p_image_map", p.image_map);
+  const ShardLayout z = ShardLayout::make_zigzag(p.len(), sp);
+  std::printf("\"split_image_map\": [");
+  for (int i = 0; i < sp; ++i) {
+    const auto s = split_position_map(p.image_map, z, i);
+    std::printf("%s[", i ? ", " : "");
+    for (size_t j = 0; j < s.size(); ++j) std::printf("%s%lld", j ? ", " : "", static_cast<long long>(s[j]));
+    std::printf("]");
+  }
+  std::printf("], ");
+  CommFabric fabric(sp, sp, SchedulerKind::threaded);
+  std::vector<std::vector<uint8_t>> got(static_cast<size_t>(sp));
+  fabric.run([&](RankCtx& ctx) {
+    std::vector<uint8_t> mask;
+    if (ctx.rank == 0)
+      for (int64_t i = 0; i < p.len(); ++i) mask.push_back(static_cast<uint8_t>(p.segment_ids[static_cast<size_t>(i)] & 0xff));
+    got[static_cast<size_t>(ctx.rank)] = replicate_packing_mask(ctx, ctx.sp_group, mask);
+  });
+  std::vector<int64_t> mask0(got[0].begin(), got[0].end()), bc;
+  for (int r = 0; r < sp; ++r) bc.push_back(fabric.stats(r, Primitive::broadcast).bytes);
+  put_json("mask", mask0), put_json("broadcast_bytes", bc, true);
+  std::printf("}\n");
+  return 0;
+}
+
 int rope(int argc, char** argv) {
   if (argc != 9) return 2;
   const int64_t L = std::atoll(argv[2]);
@@ -258,6 +315,7 @@ int main(int argc, char** argv) {
     else if (mode == "engine") rc = engine(argc, argv);
     else if (mode == "bench") rc = bench(argc, argv);
     else if (mode == "rope") rc = rope(argc, argv);
+    else if (mode == "batch") rc = batch(argc, argv);
     else if (mode == "rope_engine") rc = rope_engine(argc, argv);
     if (rc == 2) std::fprintf(stderr, "bad arguments for %s\n", mode.c_str());
     return rc;

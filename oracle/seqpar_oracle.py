@@ -381,6 +381,40 @@ def varlen_attention_fwd_bwd(q, k, v, dout, doc_lens: Sequence[int], causal=True
     return {"out": out, "lse": lse, "dq": dq, "dk": dk, "dv": dv}
 
 
+IGNORE_LABEL, NO_IMAGE, NO_SEGMENT = -100, -1, -1  # partition.hpp:92-94
+
+
+def pad_batch(tokens, labels, position_ids, segment_ids, image_map, sp, pad_token, cutoff_len,
+              pad_to_cutoff=False):
+    """pad_batch (partition.cpp:202-215): fields extended to pad_length with their sentinels;
+    position ids become iota; absent (empty) segment_ids / image_map stay absent."""
+    n = len(tokens)
+    if n == 0:
+        raise ConfigError("batch has no tokens")
+    t = pad_length(n, sp, cutoff_len, pad_to_cutoff)
+    ext = lambda xs, fill: list(xs) + [fill] * (t - len(xs)) if len(xs) else []  # noqa: E731
+    return (ext(tokens, pad_token), ext(labels, IGNORE_LABEL), list(range(t)),
+            ext(segment_ids, NO_SEGMENT), ext(image_map, NO_IMAGE))
+
+
+def documents_from_segments(segment_ids):
+    """Runs of equal segment ids -> document lengths (the B200 varlen bridge; the reference
+    never consumes segment ids in attention, model.cpp:339-351)."""
+    docs, seen, i = [], set(), 0
+    seg = list(segment_ids)
+    while i < len(seg):
+        j = i + 1
+        while j < len(seg) and seg[j] == seg[i]:
+            j += 1
+        if seg[i] != NO_SEGMENT:
+            if seg[i] in seen:
+                raise ConfigError(f"segment id {seg[i]} is not one contiguous run")
+            seen.add(seg[i])
+        docs.append(j - i)
+        i = j
+    return docs
+
+
 ROPE_BASE = 10000.0  # kRopeBase (tensor.hpp:141-144)
 
 

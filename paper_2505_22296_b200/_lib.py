@@ -29,7 +29,9 @@ EXPORTS = [
     "spattn_shard_rows", "spattn_gather_rows", "spattn_launch_count", "spattn_profile_enable",
     "spattn_profile_read", "spattn_selftest_umma", "spattn_plan_heads", "spattn_plan_problems",
     "spattn_debug_bwd_trace", "spattn_fwd_rope", "spattn_fabric_fwd_rope", "spattn_rope_apply",
-    "spattn_step_host", "spattn_pick_step_groups",
+    "spattn_step_host", "spattn_pick_step_groups", "spattn_pad_batch",
+    "spattn_split_position_map", "spattn_documents_from_segments", "spattn_replicate_packing_mask",
+    "spattn_fabric_replicate_packing_mask",
 ]
 
 
@@ -117,6 +119,12 @@ def lib() -> ctypes.CDLL:
                                    ctypes.POINTER(_vp), _i64p, _i32, ctypes.POINTER(_i64p),
                                    ctypes.c_double, ctypes.POINTER(_vp)],
         "spattn_pick_step_groups": [_i32, cfgp, _i32],
+        "spattn_pad_batch": [_i64p] * 5 + [_i64, _i32, _i64, _i64, _i32] + [_i64p] * 6,
+        "spattn_split_position_map": [layp, _i32, _i64p, _i64p],
+        "spattn_documents_from_segments": [_i64p, _i64, _i64p, _i32, ctypes.POINTER(ctypes.c_int)],
+        "spattn_replicate_packing_mask": [_vp, _vp, _i64, _vp, _i64, _i64p],
+        "spattn_fabric_replicate_packing_mask": [_vp, ctypes.POINTER(_vp), _i64p, ctypes.POINTER(_vp),
+                                                 _i64, _i64p],
         "spattn_step_host": [_vp, _i32, cfgp, layp, _i64] + [_vp] * 9 + [_i64p, _i32, _i32],
         "spattn_rope_apply": [_vp, _i64, _i64, _i32, _i32, _vp, _i64p, ctypes.c_double, _i32, _vp],
         "spattn_fabric_bwd": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),

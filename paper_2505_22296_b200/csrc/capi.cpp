@@ -489,3 +489,81 @@ extern "C" int spattn_pick_step_groups(int engine, const spattn_config* cfg, int
     return 1;
   }
 }
+
+extern "C" int spattn_pad_batch(const int64_t* tokens, const int64_t* labels,
+                                const int64_t* position_ids, const int64_t* segment_ids,
+                                const int64_t* image_map, int64_t len, int sp, int64_t pad_token,
+                                int64_t cutoff_len, int pad_to_cutoff, int64_t* out_len,
+                                int64_t* out_tokens, int64_t* out_labels,
+                                int64_t* out_position_ids, int64_t* out_segment_ids,
+                                int64_t* out_image_map) {
+  return guard([&] {
+    if (len < 0) throw seqpar::ConfigError("pad_batch: negative length");
+    auto vec = [&](const int64_t* p) {
+      return p ? std::vector<int64_t>(p, p + len) : std::vector<int64_t>();
+    };
+    seqpar::TrainBatch b;
+    b.tokens = vec(tokens), b.labels = vec(labels), b.position_ids = vec(position_ids);
+    b.segment_ids = vec(segment_ids), b.image_map = vec(image_map);
+    const auto p = seqpar::pad_batch(b, sp, pad_token, cutoff_len, pad_to_cutoff != 0);
+    *out_len = p.len();
+    auto put = [](const std::vector<int64_t>& v, int64_t* o) {
+      if (o && !v.empty()) std::memcpy(o, v.data(), v.size() * sizeof(int64_t));
+    };
+    put(p.tokens, out_tokens), put(p.labels, out_labels), put(p.position_ids, out_position_ids);
+    put(p.segment_ids, out_segment_ids), put(p.image_map, out_image_map);
+  });
+}
+
+extern "C" int spattn_split_position_map(const spattn_layout* layout, int index,
+                                         const int64_t* values, int64_t* out) {
+  return guard([&] {
+    const auto L = make_layout(layout);
+    const auto v = seqpar::split_position_map(
+        std::vector<int64_t>(values, values + L.global_len), L, index);
+    std::memcpy(out, v.data(), v.size() * sizeof(int64_t));
+  });
+}
+
+extern "C" int spattn_documents_from_segments(const int64_t* segment_ids, int64_t len,
+                                              int64_t* doc_lens, int max_docs, int* n_docs) {
+  return guard([&] {
+    const auto d = seqpar::documents_from_segments(std::vector<int64_t>(segment_ids, segment_ids + len));
+    if (static_cast<int>(d.size()) > max_docs)
+      throw seqpar::ShapeError("documents_from_segments: " + std::to_string(d.size()) +
+                               " documents exceed the output capacity " + std::to_string(max_docs));
+    std::memcpy(doc_lens, d.data(), d.size() * sizeof(int64_t));
+    *n_docs = static_cast<int>(d.size());
+  });
+}
+
+namespace {
+void copy_mask(const std::vector<uint8_t>& m, uint8_t* out, int64_t cap, int64_t* out_len) {
+  if (static_cast<int64_t>(m.size()) > cap)
+    throw seqpar::ShapeError("packing mask of " + std::to_string(m.size()) +
+                             " bytes exceeds the output capacity " + std::to_string(cap));
+  if (!m.empty()) std::memcpy(out, m.data(), m.size());
+  *out_len = static_cast<int64_t>(m.size());
+}
+}  // namespace
+
+extern "C" int spattn_replicate_packing_mask(spattn_ctx* ctx, const uint8_t* mask, int64_t len,
+                                             uint8_t* out, int64_t cap, int64_t* out_len) {
+  return guard([&] {
+    const std::vector<uint8_t> m = mask ? std::vector<uint8_t>(mask, mask + len) : std::vector<uint8_t>();
+    copy_mask(seqpar::replicate_packing_mask(*ctx->rc, ctx->rc->sp_group, m), out, cap, out_len);
+  });
+}
+
+extern "C" int spattn_fabric_replicate_packing_mask(spattn_fabric* f, const uint8_t* const* masks,
+                                                    const int64_t* lens, uint8_t* const* outs,
+                                                    int64_t cap, int64_t* out_lens) {
+  return guard([&] {
+    f->f->run([&](seqpar::RankCtx& rc) {
+      const size_t r = static_cast<size_t>(rc.rank);
+      const std::vector<uint8_t> m =
+          masks && masks[r] ? std::vector<uint8_t>(masks[r], masks[r] + lens[r]) : std::vector<uint8_t>();
+      copy_mask(seqpar::replicate_packing_mask(rc, rc.sp_group, m), outs[r], cap, &out_lens[r]);
+    });
+  });
+}

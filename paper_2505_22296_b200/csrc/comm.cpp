@@ -321,4 +321,50 @@ void nccl_unique_id(void* out128) {
   std::memcpy(out128, &id, sizeof(id));
 }
 
+std::vector<uint8_t> replicate_packing_mask(RankCtx& ctx, const CommGroup& group,
+                                            const std::vector<uint8_t>& mask) {
+  const int g = group.size();
+  const int me = group.index_of(ctx.rank);
+  cudaStream_t s = ctx.stream;
+  if (g == 1) {
+    ctx.count(Primitive::broadcast, 0);
+    return mask;
+  }
+  // the root's size first (members do not know it), then the payload; both staged in device
+  // memory so the NCCL transport can carry them
+  int64_t* dsize = nullptr;
+  SP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dsize), sizeof(int64_t), s));
+  int64_t n = me == 0 ? static_cast<int64_t>(mask.size()) : 0;
+  if (me == 0) SP_CUDA(cudaMemcpyAsync(dsize, &n, sizeof(n), cudaMemcpyHostToDevice, s));
+  std::vector<Msg> sends, recvs;
+  if (me == 0) {
+    for (int j = 1; j < g; ++j) sends.push_back({j, dsize, sizeof(int64_t)});
+  } else {
+    recvs.push_back({0, dsize, sizeof(int64_t)});
+  }
+  ctx.transport->send_recv(group, ctx.rank, sends, recvs, s);
+  SP_CUDA(cudaMemcpyAsync(&n, dsize, sizeof(n), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  SP_CUDA(cudaFreeAsync(dsize, s));
+  std::vector<uint8_t> out(static_cast<size_t>(n));
+  if (n > 0) {
+    void* buf = nullptr;
+    SP_CUDA(cudaMallocAsync(&buf, static_cast<size_t>(n), s));
+    if (me == 0) SP_CUDA(cudaMemcpyAsync(buf, mask.data(), static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
+    sends.clear();
+    recvs.clear();
+    if (me == 0) {
+      for (int j = 1; j < g; ++j) sends.push_back({j, buf, static_cast<size_t>(n)});
+    } else {
+      recvs.push_back({0, buf, static_cast<size_t>(n)});
+    }
+    ctx.transport->send_recv(group, ctx.rank, sends, recvs, s);
+    SP_CUDA(cudaMemcpyAsync(out.data(), buf, static_cast<size_t>(n), cudaMemcpyDeviceToHost, s));
+    SP_CUDA(cudaFreeAsync(buf, s));
+    SP_CUDA(cudaStreamSynchronize(s));
+  }
+  ctx.count(Primitive::broadcast, n * (g - 1) / g);
+  return out;
+}
+
 }  // namespace seqpar

@@ -184,4 +184,71 @@ std::vector<PosRun> position_runs(const std::vector<int64_t>& p) {
   return runs;
 }
 
+// ------------------------------------------------------------------ batches and packing
+void TrainBatch::validate() const {
+  const size_t n = tokens.size();
+  if (n == 0) throw ConfigError("batch has no tokens");
+  if (labels.size() != n) throw ConfigError("batch labels length does not match tokens");
+  if (position_ids.size() != n) throw ConfigError("batch position_ids length does not match tokens");
+  if (!segment_ids.empty() && segment_ids.size() != n)
+    throw ConfigError("batch segment_ids length does not match tokens");
+  if (!image_map.empty() && image_map.size() != n)
+    throw ConfigError("batch image_map length does not match tokens");
+}
+
+TrainBatch pad_batch(const TrainBatch& batch, int sp, int64_t pad_token, int64_t cutoff_len,
+                     bool pad_to_cutoff) {
+  batch.validate();
+  const int64_t target = pad_length(batch.len(), sp, cutoff_len, pad_to_cutoff);
+  const size_t t = static_cast<size_t>(target);
+  TrainBatch out = batch;
+  out.tokens.resize(t, pad_token);
+  out.labels.resize(t, kIgnoreLabel);
+  out.position_ids.resize(t);
+  for (size_t i = 0; i < t; ++i) out.position_ids[i] = static_cast<int64_t>(i);
+  if (!out.segment_ids.empty()) out.segment_ids.resize(t, kNoSegment);
+  if (!out.image_map.empty()) out.image_map.resize(t, kNoImage);
+  return out;
+}
+
+std::vector<int64_t> shard(const std::vector<int64_t>& values, const ShardLayout& layout, int index) {
+  if (static_cast<int64_t>(values.size()) != layout.global_len)
+    throw ShapeError("shard: " + std::to_string(values.size()) + " values for a layout of " +
+                     std::to_string(layout.global_len));
+  std::vector<int64_t> out;
+  for (int64_t p : layout.positions_of(index)) out.push_back(values[static_cast<size_t>(p)]);
+  return out;
+}
+
+std::vector<int64_t> split_position_map(const std::vector<int64_t>& image_map,
+                                        const ShardLayout& layout, int index) {
+  return shard(image_map, layout, index);
+}
+
+std::vector<int64_t> documents_from_segments(const std::vector<int64_t>& seg) {
+  std::vector<int64_t> docs, seen;
+  for (size_t i = 0; i < seg.size();) {
+    size_t j = i + 1;
+    while (j < seg.size() && seg[j] == seg[i]) ++j;
+    if (seg[i] != kNoSegment) {
+      if (std::find(seen.begin(), seen.end(), seg[i]) != seen.end())
+        throw ConfigError("segment id " + std::to_string(seg[i]) +
+                          " is not one contiguous run; a packed document must be contiguous");
+      seen.push_back(seg[i]);
+    }
+    docs.push_back(static_cast<int64_t>(j - i));
+    i = j;
+  }
+  return docs;
+}
+
+std::vector<int64_t> document_position_ids(const std::vector<int64_t>& doc_lens) {
+  std::vector<int64_t> ids;
+  for (int64_t n : doc_lens) {
+    if (n <= 0) throw ConfigError("documents: lengths must be positive");
+    for (int64_t i = 0; i < n; ++i) ids.push_back(i);
+  }
+  return ids;
+}
+
 }  // namespace seqpar

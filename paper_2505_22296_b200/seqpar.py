@@ -8,6 +8,7 @@ Everything here calls libspattn.so through its C ABI (``_lib``); there is no CPU
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 import weakref
 from typing import Optional, Sequence
 
@@ -110,6 +111,85 @@ def plan_problems(qpos, kpos, causal: bool = True, docs=None, max_problems: int 
     return [tuple(out[6 * i:6 * i + 6]) for i in range(n.value)], pairs[0]
 
 
+# ------------------------------------------------ batches, padding, neat-packing metadata
+IGNORE_LABEL, NO_IMAGE, NO_SEGMENT = -100, -1, -1  # kIgnoreLabel / kNoImage / kNoSegment
+
+
+@dataclasses.dataclass
+class TrainBatch:
+    """TrainBatch (reference partition.hpp:96-105): one packed sequence."""
+    tokens: list
+    labels: list
+    position_ids: list
+    segment_ids: list = dataclasses.field(default_factory=list)
+    image_map: list = dataclasses.field(default_factory=list)
+
+    def __len__(self):
+        return len(self.tokens)
+
+    def validate(self) -> None:  # partition.cpp:164-177
+        n = len(self.tokens)
+        if n == 0:
+            raise ConfigError("batch has no tokens")
+        if len(self.labels) != n:
+            raise ConfigError("batch labels length does not match tokens")
+        if len(self.position_ids) != n:
+            raise ConfigError("batch position_ids length does not match tokens")
+        if self.segment_ids and len(self.segment_ids) != n:
+            raise ConfigError("batch segment_ids length does not match tokens")
+        if self.image_map and len(self.image_map) != n:
+            raise ConfigError("batch image_map length does not match tokens")
+
+
+def pad_batch(batch: TrainBatch, sp: int, pad_token: int, cutoff_len: int,
+              pad_to_cutoff: bool = False) -> TrainBatch:
+    """pad_batch (partition.cpp:202-215): every field extended to pad_length(len, sp, ...)."""
+    batch.validate()
+    n = len(batch)
+    target = pad_length(n, sp, cutoff_len, pad_to_cutoff)
+    arr = lambda xs: _i64_array(xs) if xs else None  # noqa: E731
+    outs = [_i64(max(1, target)) for _ in range(5)]
+    out_len = _i64()
+    C.check(C.lib().spattn_pad_batch(arr(batch.tokens), arr(batch.labels), arr(batch.position_ids),
+                                     arr(batch.segment_ids), arr(batch.image_map), n, sp, pad_token,
+                                     cutoff_len, int(pad_to_cutoff), out_len, *outs))
+    t = out_len[0]
+    return TrainBatch(list(outs[0][:t]), list(outs[1][:t]), list(outs[2][:t]),
+                      list(outs[3][:t]) if batch.segment_ids else [],
+                      list(outs[4][:t]) if batch.image_map else [])
+
+
+def split_position_map(image_map: Sequence[int], mode: str, sp: int, index: int,
+                       ulysses_degree: int = 0, ring_degree: int = 0) -> list[int]:
+    """split_position_map (partition.cpp:217-220): the shard's entries of a per-position map."""
+    lay = C.make_layout(mode, len(image_map), sp, ulysses_degree, ring_degree)
+    n = len(image_map) // sp if sp > 0 else 0
+    out = _i64(max(1, n))
+    C.check(C.lib().spattn_split_position_map(ctypes.byref(lay), index, _i64_array(image_map), out))
+    return list(out[:n])
+
+
+def documents_from_segments(segment_ids: Sequence[int]) -> list[int]:
+    """Neat-packing segment ids -> document lengths for the varlen kernels (``docs=``): runs of
+    equal ids are documents, a -1 padding tail is one more document."""
+    n = len(segment_ids)
+    out = _i64(max(1, n))
+    nd = ctypes.c_int()
+    C.check(C.lib().spattn_documents_from_segments(_i64_array(segment_ids), n, out, max(1, n),
+                                                   ctypes.byref(nd)))
+    return list(out[:nd.value])
+
+
+def document_position_ids(doc_lens: Sequence[int]) -> list[int]:
+    """Per-document reset position ids (rope ids of a neat-packed sequence)."""
+    ids = []
+    for n in doc_lens:
+        if n <= 0:
+            raise ConfigError("documents: lengths must be positive")
+        ids.extend(range(n))
+    return ids
+
+
 def set_kernel_family(name: str) -> None:
     """'tcgen05' (default where supported), 'mma' or 'tcgen05_pp' (two-tile forward)."""
     C.check(C.lib().spattn_set_kernel_family({"tcgen05": 0, "mma": 1, "tcgen05_pp": 2}[name]))
@@ -198,6 +278,19 @@ class Fabric:
             C.check(C.lib().spattn_ctx_stats(self.ctxs[rank], i, calls, nbytes))
             out[name] = (calls[0], nbytes[0])
         return out
+
+    def replicate_packing_mask(self, masks: Sequence[Optional[bytes]]) -> list[bytes]:
+        """replicate_packing_mask (partition.cpp:222-227) on every rank: rank 0's bytes
+        everywhere (counted as one broadcast)."""
+        cap = max([len(m) for m in masks if m] + [1])
+        bufs = [ctypes.create_string_buffer(m or b"", max(1, len(m or b""))) for m in masks]
+        outs = [ctypes.create_string_buffer(cap) for _ in masks]
+        lens = _i64_array([len(m or b"") for m in masks])
+        out_lens = _i64(len(masks))
+        C.check(C.lib().spattn_fabric_replicate_packing_mask(
+            self._h, C.ptr_array([ctypes.addressof(b) for b in bufs]), lens,
+            C.ptr_array([ctypes.addressof(o) for o in outs]), cap, out_lens))
+        return [o.raw[:out_lens[i]] for i, o in enumerate(outs)]
 
     def total_bytes(self, rank: int) -> int:
         return sum(b for _, b in self.stats(rank).values())
@@ -426,6 +519,16 @@ class RankContext:
         self._h = h
         self.rank, self.world = rank, world
         self._fin = weakref.finalize(self, C.lib().spattn_ctx_destroy, h)
+
+    def replicate_packing_mask(self, mask: Optional[bytes], max_len: int) -> bytes:
+        """replicate_packing_mask (partition.cpp:222-227) over NCCL: group index 0 supplies
+        the mask, every rank returns it; ``max_len`` bounds the result buffer."""
+        m = mask or b""
+        buf = ctypes.create_string_buffer(m, max(1, len(m)))
+        out = ctypes.create_string_buffer(max(1, max_len))
+        n = _i64()
+        C.check(C.lib().spattn_replicate_packing_mask(self._h, buf, len(m), out, max_len, n))
+        return out.raw[:n[0]]
 
     def stats(self) -> dict:
         out = {}

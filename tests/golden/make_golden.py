@@ -105,6 +105,28 @@ def make_rope(tmp):
     print("wrote", os.path.join(HERE, "reference_rope.npz"))
 
 
+BATCH_CASES = [
+    # len, sp, cutoff_len, pad_to_cutoff, seed
+    (13, 2, 512, 0, 3), (37, 4, 1024, 0, 5), (50, 2, 256, 1, 7), (64, 8, 64, 0, 11),
+    (5, 1, 64, 0, 13), (100, 4, 128, 1, 17),
+]
+
+
+def make_batch():
+    """pad_batch / split_position_map / replicate_packing_mask of the unmodified reference ->
+    tests/golden/reference_batch.json."""
+    out = []
+    for ln, sp, cut, to_cut, seed in BATCH_CASES:
+        r = subprocess.run([DRIVER, "batch", str(ln), str(sp), str(cut), str(to_cut), str(seed)],
+                           check=True, capture_output=True, text=True)
+        rec = json.loads(r.stdout)
+        rec["args"] = [ln, sp, cut, to_cut, seed]
+        out.append(rec)
+    with open(os.path.join(HERE, "reference_batch.json"), "w") as f:
+        json.dump(out, f)
+    print("wrote", os.path.join(HERE, "reference_batch.json"))
+
+
 def main():
     if not os.path.exists(DRIVER):
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
@@ -187,6 +209,9 @@ def main():
 if __name__ == "__main__":
     if sys.argv[1:] == ["rope"]:
         make_rope(tempfile.mkdtemp())
+    elif sys.argv[1:] == ["batch"]:
+        make_batch()
     else:
         main()
         make_rope(tempfile.mkdtemp())
+        make_batch()
