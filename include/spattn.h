@@ -89,6 +89,27 @@ int spattn_fabric_replicate_packing_mask(spattn_fabric* f, const uint8_t* const*
                                          const int64_t* lens, uint8_t* const* outs, int64_t cap,
                                          int64_t* out_lens);
 
+/* ---- the step after the model: log-probs and sharded loss reductions (losses.cpp) ---- */
+/* sequence_logprob_per_position (losses.cpp:20-72): logits [T, V] of dtype 0 fp32 / 1 bf16 /
+ * 2 fp64,
+ * device labels [T] int64 (-100 = ignored); out / lse device fp64 [T]. */
+int spattn_logprob_fwd(void* stream, const void* logits, int dtype, int64_t T, int64_t V,
+                       const int64_t* labels, double* out, double* lse);
+/* its tape backward: dlogits (= or +=) g_t * (onehot(label_t) - softmax(row_t)) */
+int spattn_logprob_bwd(void* stream, const void* logits, int dtype, int64_t T, int64_t V,
+                       const int64_t* labels, const double* lse, const double* g, void* dlogits,
+                       int accumulate);
+/* ExactSum (exact_sum.hpp): 35 uint64 limbs, 2240-bit two's complement in units of 2^-1074.
+ * _device adds n device doubles, _host n host doubles; limbs accumulate (+=). */
+int spattn_exact_sum_device(void* stream, const double* values, int64_t n, uint64_t* limbs);
+int spattn_exact_sum_host(const double* values, int64_t n, uint64_t* limbs);
+int spattn_exact_merge(uint64_t* acc, const uint64_t* other);
+int spattn_exact_round(const uint64_t* limbs, double* out);
+/* group reductions of the context's SP group (comm.cpp:339-353, :504-524), in place */
+int spattn_exact_sum_all_reduce(spattn_ctx* ctx, uint64_t* limbs);
+int spattn_all_reduce_count(spattn_ctx* ctx, int64_t* n);
+int spattn_all_reduce_values(spattn_ctx* ctx, double* values, int64_t n);
+
 /* Host planners of the engines (no GPU): per-member head windows of the Ulysses
  * head<->sequence moves (query heads [q_lo, q_lo+q_n), kv heads [kv_lo, kv_lo+kv_n); dummy
  * heads are virtual), and the attention problems two position lists reduce to: rows of 6

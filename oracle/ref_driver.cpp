@@ -12,6 +12,10 @@
 //   ref_driver batch <len> <sp> <cutoff> <pad_to_cutoff> <seed>
 //       pad_batch (partition.cpp:202-215) of a random packed batch, split_position_map of its
 //       image map over zigzag(sp), replicate_packing_mask over sp ranks: JSON on stdout
+//   ref_driver loss
+//       sequence_logprob_per_position, sft_loss_sharded and dpo_loss_sharded / the wrong-order
+//       DPO (losses.cpp) on the reference's own test inputs (tests/test_losses.cpp:150-266)
+//       over sp in {1, 2, 4}: JSON on stdout
 //   ref_driver rope <L> <heads> <dim> <pos_scale> <pos_offset> <seed> <out.bin>
 //       rope_apply (tensor.cpp:548-607) of x ~ U(-2,2) at ids i*scale+offset, loss sum(y*R)
 //   ref_driver rope_engine <engine> <sp> <L> <heads> <kv> <dim> <u> <r> <pos_scale>
@@ -29,6 +33,7 @@
 
 #include "seqpar/attention.hpp"
 #include "seqpar/comm.hpp"
+#include "seqpar/losses.hpp"
 #include "seqpar/partition.hpp"
 #include "seqpar/report.hpp"
 #include "seqpar/tensor.hpp"
@@ -226,6 +231,102 @@ int batch(int argc, char** argv) {
   return 0;
 }
 
+std::vector<double> rvals(int64_t n, uint64_t seed, double lo = -2.0, double hi = 2.0) {
+  Rng rng(seed);
+  std::vector<double> out(static_cast<size_t>(n));
+  for (double& v : out) v = rng.uniform_range(lo, hi);
+  return out;
+}
+
+void put_jd(const char* name, const std::vector<double>& v, bool last = false) {
+  std::printf("\"%s\": [", name);
+  for (size_t i = 0; i < v.size(); ++i) std::printf("%s%.17g", i ? ", " : "", v[i]);
+  std::printf("]%s", last ? "" : ", ");
+}
+
+int loss(int argc, char**) {
+  if (argc != 2) return 2;
+  const int64_t T = 32, V = 11;
+  const auto logits = rvals(T * V, 29);
+  std::vector<int64_t> labels(static_cast<size_t>(T));
+  Rng lr(31);
+  for (auto& l : labels) l = lr.uniform() < 0.25 ? kIgnoreLabel : lr.uniform_int(0, V - 1);
+  // one SFT run: loss and the logits gradient gathered to global order
+  auto sft = [&](const ShardLayout& layout, ReduceMode mode, bool per_rank, std::vector<double>* grad) {
+    const int sp = layout.sp;
+    CommFabric fabric(sp, sp, SchedulerKind::threaded);
+    std::vector<double> losses(static_cast<size_t>(sp));
+    std::vector<std::vector<double>> grads(static_cast<size_t>(sp));
+    fabric.run([&](RankCtx& ctx) {
+      const int idx = ctx.sp_group.index_of(ctx.rank);
+      Tensor lg = Tensor::from({layout.local_len(), V}, shard_rows(logits, V, layout, idx), true);
+      std::vector<int64_t> lab = shard(labels, layout, idx);
+      Tape tape;
+      TapeScope sc(&tape);
+      Tensor l = sft_loss_sharded(ctx, ctx.sp_group, lg, lab, mode, per_rank);
+      tape.backward(l);
+      losses[static_cast<size_t>(idx)] = l.scalar_value();
+      grads[static_cast<size_t>(idx)].assign(lg.grad().begin(), lg.grad().end());
+    });
+    if (grad) *grad = gather_rows(grads, V, layout);
+    return losses[0];
+  };
+  std::printf("{");
+  put_jd("logits", logits);
+  put_json("labels", labels);
+  {
+    Tensor lg = Tensor::from({T, V}, logits, false);
+    Tensor pp = sequence_logprob_per_position(lg, labels);
+    put_jd("per_pos", std::vector<double>(pp.values().begin(), pp.values().end()));
+  }
+  std::vector<double> g1, g4a, g4p;
+  std::vector<double> sft_losses{sft(ShardLayout::make_naive(T, 1), ReduceMode::grad_aware, false, &g1)};
+  for (int sp : {2, 4}) {
+    sft_losses.push_back(sft(ShardLayout::make_naive(T, sp), ReduceMode::grad_aware, false, nullptr));
+    sft_losses.push_back(sft(ShardLayout::make_zigzag(T, sp), ReduceMode::grad_aware, false, nullptr));
+  }
+  sft(ShardLayout::make_naive(T, 4), ReduceMode::grad_aware, false, &g4a);
+  sft(ShardLayout::make_naive(T, 4), ReduceMode::plain, false, &g4p);
+  put_jd("sft_losses", sft_losses);  // sp1, naive2, zigzag2, naive4, zigzag4
+  put_jd("sft_per_rank_mean_sp2", {sft(ShardLayout::make_naive(T, 2), ReduceMode::grad_aware, true, nullptr)});
+  put_jd("sft_grad_sp1", g1), put_jd("sft_grad_sp4_aware", g4a), put_jd("sft_grad_sp4_plain", g4p);
+  // DPO (tests/test_losses.cpp:224-266)
+  const int64_t TD = 24;
+  const auto pc = rvals(TD, 53, -1.0, 0.0), pr = rvals(TD, 59, -2.0, -0.5), rc = rvals(TD, 61, -1.2, -0.1),
+             rr = rvals(TD, 67, -1.8, -0.4);
+  auto dpo = [&](const ShardLayout& layout, bool wrong, std::vector<double>* gpc) {
+    const int sp = layout.sp;
+    CommFabric fabric(sp, sp, SchedulerKind::threaded);
+    std::vector<double> losses(static_cast<size_t>(sp));
+    std::vector<std::vector<double>> grads(static_cast<size_t>(sp));
+    fabric.run([&](RankCtx& ctx) {
+      const int idx = ctx.sp_group.index_of(ctx.rank);
+      auto t = [&](const std::vector<double>& full, bool rg) {
+        return Tensor::from({layout.local_len()}, shard(full, layout, idx), rg);
+      };
+      Tensor a = t(pc, true), b = t(pr, true), c = t(rc, false), d = t(rr, false);
+      Tape tape;
+      TapeScope sc(&tape);
+      Tensor l = wrong ? wrong_order_dpo_loss(ctx, ctx.sp_group, a, b, c, d, kDpoBetaDefault)
+                       : dpo_loss_sharded(ctx, ctx.sp_group, a, b, c, d, kDpoBetaDefault);
+      tape.backward(l);
+      losses[static_cast<size_t>(idx)] = l.scalar_value();
+      grads[static_cast<size_t>(idx)].assign(a.grad().begin(), a.grad().end());
+    });
+    if (gpc) *gpc = gather_rows(grads, 1, layout);
+    return losses[0];
+  };
+  std::vector<double> gd1, gd2;
+  std::vector<double> dl{dpo(ShardLayout::make_naive(TD, 1), false, &gd1), dpo(ShardLayout::make_naive(TD, 2), false, &gd2),
+                         dpo(ShardLayout::make_zigzag(TD, 4), false, nullptr)};
+  put_jd("pc", pc), put_jd("pr", pr), put_jd("rc", rc), put_jd("rr", rr);
+  put_jd("dpo_losses", dl);  // sp1, naive2, zigzag4
+  put_jd("dpo_wrong_sp2", {dpo(ShardLayout::make_naive(TD, 2), true, nullptr)});
+  put_jd("dpo_grad_pc_sp1", gd1), put_jd("dpo_grad_pc_sp2", gd2, true);
+  std::printf("}\n");
+  return 0;
+}
+
 int rope(int argc, char** argv) {
   if (argc != 9) return 2;
   const int64_t L = std::atoll(argv[2]);
@@ -316,6 +417,7 @@ int main(int argc, char** argv) {
     else if (mode == "bench") rc = bench(argc, argv);
     else if (mode == "rope") rc = rope(argc, argv);
     else if (mode == "batch") rc = batch(argc, argv);
+    else if (mode == "loss") rc = loss(argc, argv);
     else if (mode == "rope_engine") rc = rope_engine(argc, argv);
     if (rc == 2) std::fprintf(stderr, "bad arguments for %s\n", mode.c_str());
     return rc;

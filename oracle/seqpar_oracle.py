@@ -415,6 +415,44 @@ def documents_from_segments(segment_ids):
     return docs
 
 
+def logprob_per_position(logits, labels):
+    """sequence_logprob_per_position (losses.cpp:20-50): row[label] - (m + log(sum exp(row - m)))
+    in f64, 0 for ignored labels."""
+    logits = np.asarray(logits, dtype=np.float64)
+    out = np.zeros(logits.shape[0])
+    for t, lab in enumerate(labels):
+        if lab == IGNORE_LABEL:
+            continue
+        row = logits[t]
+        m = row.max()
+        out[t] = row[lab] - (m + math.log(float(np.sum(np.exp(row - m)))))
+    return out
+
+
+def exact_sum(values) -> float:
+    """ExactSum (exact_sum.hpp) rounds the exact sum once to nearest-even: math.fsum's contract."""
+    return math.fsum(float(v) for v in np.asarray(values, dtype=np.float64).ravel())
+
+
+def sft_loss(per_pos, labels) -> float:
+    """sft_loss_sharded's value (losses.cpp:104-119, default weighting): -exact_sum / N_global,
+    independent of the sharding."""
+    n = sum(1 for lab in labels if lab != IGNORE_LABEL)
+    if n == 0:
+        raise ConfigError("sft loss: no supervised positions in the group")
+    return exact_sum(per_pos) * (-1.0 / n)
+
+
+def softplus(x: float) -> float:  # tensor.cpp:211-213
+    return math.log1p(math.exp(-abs(x))) + max(x, 0.0)
+
+
+def dpo_loss(pc, pr, rc, rr, beta=0.1) -> float:
+    """dpo_loss_sharded's value (losses.cpp:121-135)."""
+    margin = (exact_sum(pc) - exact_sum(pr)) - (exact_sum(rc) - exact_sum(rr))
+    return softplus(margin * -beta)
+
+
 ROPE_BASE = 10000.0  # kRopeBase (tensor.hpp:141-144)
 
 

@@ -31,7 +31,9 @@ EXPORTS = [
     "spattn_debug_bwd_trace", "spattn_fwd_rope", "spattn_fabric_fwd_rope", "spattn_rope_apply",
     "spattn_step_host", "spattn_pick_step_groups", "spattn_pad_batch",
     "spattn_split_position_map", "spattn_documents_from_segments", "spattn_replicate_packing_mask",
-    "spattn_fabric_replicate_packing_mask",
+    "spattn_fabric_replicate_packing_mask", "spattn_logprob_fwd", "spattn_logprob_bwd",
+    "spattn_exact_sum_device", "spattn_exact_sum_host", "spattn_exact_merge", "spattn_exact_round",
+    "spattn_exact_sum_all_reduce", "spattn_all_reduce_count", "spattn_all_reduce_values",
 ]
 
 
@@ -119,6 +121,15 @@ def lib() -> ctypes.CDLL:
                                    ctypes.POINTER(_vp), _i64p, _i32, ctypes.POINTER(_i64p),
                                    ctypes.c_double, ctypes.POINTER(_vp)],
         "spattn_pick_step_groups": [_i32, cfgp, _i32],
+        "spattn_logprob_fwd": [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp],
+        "spattn_logprob_bwd": [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _i32],
+        "spattn_exact_sum_device": [_vp, _vp, _i64, _vp],
+        "spattn_exact_sum_host": [_vp, _i64, _vp],
+        "spattn_exact_merge": [_vp, _vp],
+        "spattn_exact_round": [_vp, ctypes.POINTER(ctypes.c_double)],
+        "spattn_exact_sum_all_reduce": [_vp, _vp],
+        "spattn_all_reduce_count": [_vp, _i64p],
+        "spattn_all_reduce_values": [_vp, _vp, _i64],
         "spattn_pad_batch": [_i64p] * 5 + [_i64, _i32, _i64, _i64, _i32] + [_i64p] * 6,
         "spattn_split_position_map": [layp, _i32, _i64p, _i64p],
         "spattn_documents_from_segments": [_i64p, _i64, _i64p, _i32, ctypes.POINTER(ctypes.c_int)],

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "seqpar/attention.hpp"
+#include "seqpar/losses.hpp"
 #include "spattn.h"
 #include "spattn_internal.h"
 
@@ -565,5 +566,71 @@ extern "C" int spattn_fabric_replicate_packing_mask(spattn_fabric* f, const uint
           masks && masks[r] ? std::vector<uint8_t>(masks[r], masks[r] + lens[r]) : std::vector<uint8_t>();
       copy_mask(seqpar::replicate_packing_mask(rc, rc.sp_group, m), outs[r], cap, &out_lens[r]);
     });
+  });
+}
+
+// ------------------------------------------------------------------------------- losses
+namespace {
+seqpar::ExactSum limbs_in(const uint64_t* l) {
+  std::array<uint64_t, seqpar::ExactSum::kLimbs> a{};
+  std::memcpy(a.data(), l, sizeof(a));
+  return seqpar::ExactSum::from_limbs(a);
+}
+void limbs_out(const seqpar::ExactSum& s, uint64_t* l) {
+  std::memcpy(l, s.limbs().data(), sizeof(uint64_t) * seqpar::ExactSum::kLimbs);
+}
+}  // namespace
+
+extern "C" int spattn_logprob_fwd(void* stream, const void* logits, int dtype, int64_t T, int64_t V,
+                                  const int64_t* labels, double* out, double* lse) {
+  return guard([&] {
+    seqpar::logprob_forward(static_cast<cudaStream_t>(stream), logits, dtype, T, V, labels, out, lse);
+  });
+}
+extern "C" int spattn_logprob_bwd(void* stream, const void* logits, int dtype, int64_t T, int64_t V,
+                                  const int64_t* labels, const double* lse, const double* g,
+                                  void* dlogits, int accumulate) {
+  return guard([&] {
+    seqpar::logprob_backward(static_cast<cudaStream_t>(stream), logits, dtype, T, V, labels, lse, g,
+                             dlogits, accumulate != 0);
+  });
+}
+extern "C" int spattn_exact_sum_device(void* stream, const double* values, int64_t n, uint64_t* limbs) {
+  return guard([&] {
+    auto acc = limbs_in(limbs);
+    acc.merge(seqpar::exact_sum_device(values, n, static_cast<cudaStream_t>(stream)));
+    limbs_out(acc, limbs);
+  });
+}
+extern "C" int spattn_exact_sum_host(const double* values, int64_t n, uint64_t* limbs) {
+  return guard([&] {
+    auto acc = limbs_in(limbs);
+    for (int64_t i = 0; i < n; ++i) acc.add(values[i]);
+    limbs_out(acc, limbs);
+  });
+}
+extern "C" int spattn_exact_merge(uint64_t* acc, const uint64_t* other) {
+  return guard([&] {
+    auto a = limbs_in(acc);
+    a.merge(limbs_in(other));
+    limbs_out(a, acc);
+  });
+}
+extern "C" int spattn_exact_round(const uint64_t* limbs, double* out) {
+  return guard([&] { *out = limbs_in(limbs).round_to_double(); });
+}
+extern "C" int spattn_exact_sum_all_reduce(spattn_ctx* ctx, uint64_t* limbs) {
+  return guard([&] {
+    limbs_out(seqpar::exact_sum_all_reduce(*ctx->rc, ctx->rc->sp_group, limbs_in(limbs)), limbs);
+  });
+}
+extern "C" int spattn_all_reduce_count(spattn_ctx* ctx, int64_t* n) {
+  return guard([&] { *n = seqpar::all_reduce_count(*ctx->rc, ctx->rc->sp_group, *n); });
+}
+extern "C" int spattn_all_reduce_values(spattn_ctx* ctx, double* values, int64_t n) {
+  return guard([&] {
+    const auto r = seqpar::all_reduce_values(*ctx->rc, ctx->rc->sp_group,
+                                             std::vector<double>(values, values + n));
+    std::memcpy(values, r.data(), static_cast<size_t>(n) * sizeof(double));
   });
 }

@@ -127,6 +127,15 @@ def make_batch():
     print("wrote", os.path.join(HERE, "reference_batch.json"))
 
 
+def make_loss():
+    """sequence_logprob_per_position / sft_loss_sharded / dpo_loss_sharded of the unmodified
+    reference on its own test inputs -> tests/golden/reference_loss.json."""
+    r = subprocess.run([DRIVER, "loss"], check=True, capture_output=True, text=True)
+    with open(os.path.join(HERE, "reference_loss.json"), "w") as f:
+        f.write(r.stdout)
+    print("wrote", os.path.join(HERE, "reference_loss.json"))
+
+
 def main():
     if not os.path.exists(DRIVER):
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
@@ -211,7 +220,10 @@ if __name__ == "__main__":
         make_rope(tempfile.mkdtemp())
     elif sys.argv[1:] == ["batch"]:
         make_batch()
+    elif sys.argv[1:] == ["loss"]:
+        make_loss()
     else:
         main()
         make_rope(tempfile.mkdtemp())
         make_batch()
+        make_loss()
