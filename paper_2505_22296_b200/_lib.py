@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspattn.so")
+# SPATTN_LIB (development A/B builds) names another build of the library inside the package
+LIB_PATH = os.path.join(_HERE, os.environ.get("SPATTN_LIB", "libspattn.so"))
 
 OK, ERR_CONFIG, ERR_SHAPE, ERR_STATE, ERR_PEER = range(5)
 ENGINES = ["oracle", "ulysses", "dummy_head", "xtuner", "ring", "usp"]

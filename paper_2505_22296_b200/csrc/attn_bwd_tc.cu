@@ -25,15 +25,22 @@ namespace {
 
 constexpr int D = 128;
 constexpr int BQ = 64;
-constexpr int NST = 3;                      // Q/dO pipeline stages
+#ifndef BWD_NST
+#define BWD_NST 3
+#endif
+#ifndef BWD_NSTG
+#define BWD_NSTG 1
+#endif
+constexpr int NST = BWD_NST;                // Q/dO pipeline stages
+constexpr int NSTG = BWD_NSTG;              // dQ staging slots per drain warp
 constexpr int KV_TILE = 128 * D * 2;        // 32 KB (two 16 KB column blocks)
 constexpr int Q_TILE = BQ * D * 2;          // 16 KB (two 8 KB column blocks)
 constexpr int K_OFF = 0, V_OFF = KV_TILE;
 constexpr int Q_OFF = 2 * KV_TILE;          // NST x Q tile
 constexpr int DO_OFF = Q_OFF + NST * Q_TILE;
 constexpr int DS_OFF = DO_OFF + NST * Q_TILE;    // 2 x [128 keys x 64 queries] bf16 (16 KB each)
-constexpr int STG_OFF = DS_OFF + 2 * 16384;      // 4 warps x [64 queries x 32 fp32] (8 KB each)
-constexpr int LD_OFF = STG_OFF + 4 * 8192;       // lse*log2e, delta: [NST][64] each
+constexpr int STG_OFF = DS_OFF + 2 * 16384;      // 4 warps x NSTG x [64 queries x 32 fp32] (8 KB)
+constexpr int LD_OFF = STG_OFF + 4 * NSTG * 8192;  // lse*log2e, delta: [NST][64] each
 constexpr int BAR_OFF = LD_OFF + 2 * NST * 64 * 4;
 
 enum {
@@ -260,7 +267,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         tc::commit(bar(E_SF + b));
         TR(2, it);
-        if (it >= 2) {  // dQ^T of it-2 (same columns) must be drained
+        if (it >= 2 && !(a.debug & 64)) {  // dQ^T of it-2 (same columns) must be drained (debug 64: skip, wrong dq)
           tc::mbar_wait(bar(E_DQF + b), ((it - 2) >> 1) & 1);
           tc::fence_after();
         }
@@ -373,7 +380,7 @@ __global__ void __launch_bounds__(384, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 120;\n");
     const int w = warp - 4, lane = threadIdx.x % 32;
     const uint32_t lane_base = (uint32_t)(w * 32) << 16;
-    const uint32_t stg = sStg + w * 8192;  // [64 queries x 32 fp32], 128B-swizzled rows
+    const uint32_t stg0 = sStg + w * NSTG * 8192;  // NSTG x [64 queries x 32 fp32], 128B-swizzled rows
     for (int it = 0; it < T; ++it) {
       const int b = it & 1;
       const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * BQ;
@@ -389,7 +396,8 @@ __global__ void __launch_bounds__(384, 1)
       if (w == 0 && lane == 0) TR(12, it);
       // (per-lane red.global.add.f32 from registers measured 1.8x slower than this staging)
       if (a.debug & 32) continue;  // profiling: no dQ staging / reduce (wrong dq)
-      if (lane == 0) tc::bulk_wait_read<0>();  // the slot's previous reduce has read it
+      const uint32_t stg = stg0 + (it % NSTG) * 8192;
+      if (lane == 0) tc::bulk_wait_read<NSTG - 1>();  // the slot's previous reduce has read it
       __syncwarp();
 #pragma unroll
       for (int qq = 0; qq < BQ; ++qq) {
