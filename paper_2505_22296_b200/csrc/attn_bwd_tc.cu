@@ -66,10 +66,12 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 // and dS = P (dP - delta), both packed to bf16 pairs (attention.cpp:199-209). Packed fp32x2
 // math; one pair in four takes the FMA-pipe exp2 so MUFU and FMA finish together. MASK (only
 // for tiles crossing the causal diagonal or the row end) zeroes queries outside [ilo, ihi).
+// dS is produced already multiplied by the softmax scale (dl2 holds -delta*scale): the dQ and
+// dK accumulators then need no rescaling (dS scale = scale * P (dP - delta)).
 template <bool MASK, bool PACKED, bool POLY>
 __device__ __forceinline__ void grad_chunk(const uint32_t (&rs)[32], const uint32_t (&rp)[32], const float2* nl2,
-                                           const float2* dl2, uint64_t sl2x2, int ilo, int ihi, uint32_t (&wp)[16],
-                                           uint32_t (&wd)[16]) {
+                                           const float2* dl2, uint64_t sl2x2, uint64_t sc2, int ilo, int ihi,
+                                           uint32_t (&wp)[16], uint32_t (&wd)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const float2 nl = nl2[i], dl = dl2[i];
@@ -94,10 +96,12 @@ __device__ __forceinline__ void grad_chunk(const uint32_t (&rs)[32], const uint3
     if (PACKED) {
       const float2 dsv = f2_unpack(f2_mul(
           f2_pack(pp.x, pp.y),
-          f2_sub(f2_pack(__uint_as_float(rp[2 * i]), __uint_as_float(rp[2 * i + 1])), f2_pack(dl.x, dl.y))));
+          f2_fma(f2_pack(__uint_as_float(rp[2 * i]), __uint_as_float(rp[2 * i + 1])), sc2, f2_pack(dl.x, dl.y))));
       wd[i] = pack_bf16(dsv.x, dsv.y);
     } else {
-      wd[i] = pack_bf16(pp.x * (__uint_as_float(rp[2 * i]) - dl.x), pp.y * (__uint_as_float(rp[2 * i + 1]) - dl.y));
+      const float sc = f2_unpack(sc2).x;
+      wd[i] = pack_bf16(pp.x * fmaf(__uint_as_float(rp[2 * i]), sc, dl.x),
+                        pp.y * fmaf(__uint_as_float(rp[2 * i + 1]), sc, dl.y));
     }
   }
 }
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           sL[st * 64 + lane + 32 * k] = pl[k] == -INFINITY ? -INFINITY : -pl[k] * kLog2e;
-          sDl[st * 64 + lane + 32 * k] = pd[k];
+          sDl[st * 64 + lane + 32 * k] = -pd[k] * a.scale;  // dS is stored pre-scaled
         }
         if (it + 1 < T) fetch(it + 1);
         tc::mbar_arrive(bar(E_QF + st));  // release: the stores above are visible to waiters
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(384, 1)
       }
       const float2* lse2 = reinterpret_cast<const float2*>(sL + lb);   // -lse*log2e per query
       const float2* dl2 = reinterpret_cast<const float2*>(sDl + lb);   // delta per query
-      const uint64_t sl2x2 = f2_pack(sl2, sl2);
+      const uint64_t sl2x2 = f2_pack(sl2, sl2), sc2 = f2_pack(a.scale, a.scale);
       constexpr bool PK = SV & 2, PO = SV & 8;
 #pragma unroll
       for (int cc = 0; cc < BQ / 32; ++cc) {
@@ -339,9 +343,9 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) wp[i] = rs[cc][i] ^ rp[cc][i], wd[i] = rs[cc][i + 16] ^ rp[cc][i + 16];
         } else if ((SV & 4) && full) {
-          grad_chunk<false, PK, PO>(rs[cc], rp[cc], lse2 + cc * 16, dl2 + cc * 16, sl2x2, 0, 0, wp, wd);
+          grad_chunk<false, PK, PO>(rs[cc], rp[cc], lse2 + cc * 16, dl2 + cc * 16, sl2x2, sc2, 0, 0, wp, wd);
         } else {
-          grad_chunk<true, PK, PO>(rs[cc], rp[cc], lse2 + cc * 16, dl2 + cc * 16, sl2x2, ilo - cc * 32,
+          grad_chunk<true, PK, PO>(rs[cc], rp[cc], lse2 + cc * 16, dl2 + cc * 16, sl2x2, sc2, ilo - cc * 32,
                                    ihi - cc * 32, wp, wd);
         }
         tc::tmem_st16(tmem + lane_base + 64 * b + cc * 16, wp);
@@ -402,7 +406,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int qq = 0; qq < BQ; ++qq) {
         const uint32_t addr = tc::sw128(stg, qq, lane >> 2) + (lane & 3) * 4;
-        asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(addr), "f"(__uint_as_float(r[qq >> 5][qq & 31]) * a.scale));
+        asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(addr), "f"(__uint_as_float(r[qq >> 5][qq & 31])));
       }
       tc::fence_proxy_async();
       __syncwarp();
@@ -426,9 +430,8 @@ __global__ void __launch_bounds__(384, 1)
         if (c < P.nk) {
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            red_add_v4(dk + cc * 32 + 4 * i, __uint_as_float(r[4 * i]) * a.scale,
-                       __uint_as_float(r[4 * i + 1]) * a.scale, __uint_as_float(r[4 * i + 2]) * a.scale,
-                       __uint_as_float(r[4 * i + 3]) * a.scale);
+            red_add_v4(dk + cc * 32 + 4 * i, __uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                       __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
         }
       }
     }
