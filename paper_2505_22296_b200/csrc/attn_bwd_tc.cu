@@ -398,7 +398,9 @@ __global__ void __launch_bounds__(384, 1)
       tc::fence_before();
       tc::mbar_arrive(bar(E_DQF + b));
       if (w == 0 && lane == 0) TR(12, it);
-      // (per-lane red.global.add.f32 from registers measured 1.8x slower than this staging)
+      // (per-lane red.global.add.f32 from registers measured 1.8x slower than this staging, and
+      // a quad-transpose via shuffles + red.global.add.v4.f32 1.6x slower: 3620 vs 2229 cycles
+      // per iteration — the L2 atomics, not the smem traffic, would bound it)
       if (a.debug & 32) continue;  // profiling: no dQ staging / reduce (wrong dq)
       const uint32_t stg = stg0 + (it % NSTG) * 8192;
       if (lane == 0) tc::bulk_wait_read<NSTG - 1>();  // the slot's previous reduce has read it
