@@ -235,3 +235,40 @@ def test_host_step_ulysses_loopback_rejects_bad_groups(P):
     k = torch.zeros(1, 64, 3, 64, dtype=torch.bfloat16)
     with pytest.raises(P.ConfigError):
         P.attention_step_host("oracle", q, k, k, q, groups=4)
+
+
+@pytest.mark.parametrize("engine,sp,H,Hkv", [("ulysses", 2, 8, 4), ("dummy_head", 4, 6, 2),
+                                             ("ring", 2, 4, 2)])
+def test_host_step_sharded_on_loopback_ranks(P, engine, sp, H, Hkv):
+    """spattn_step_host on every rank of a loopback group (one thread per rank): the kv-head
+    group split must respect each engine's head constraints and still match the oracle."""
+    import threading
+    import types
+
+    P.set_kernel_family("tcgen05")
+    L, d = 256, 64
+    q, k, v, R = parity_inputs(700 + sp + H, L, H, Hkv, d)
+    mode = "zigzag" if engine == "ring" else "naive"
+    fab = P.Fabric(sp)
+    shard = lambda x, i: P.shard_rows(to_dev(x), mode, sp, i).cpu()  # noqa: E731
+    res, errs = [None] * sp, []
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            rc = types.SimpleNamespace(sp=sp, _h=fab.ctxs[r])
+            res[r] = P.attention_step_host(engine, shard(q, r), shard(k, r), shard(v, r),
+                                           shard(R, r), rank_ctx=rc, seq_len=L, want_out=True)
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(sp)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    gather = lambda i: P.gather_rows([res[r][i].cuda() for r in range(sp)], mode, sp)  # noqa: E731
+    got = {"dq": np_(gather(0)), "dk": np_(gather(1)), "dv": np_(gather(2)), "out": np_(gather(3))}
+    orc, ref = oracle_all(q, k, v, R), torch_ref(q, k, v, R)
+    check_all(got, orc, ref, keys=("out", "dq", "dk", "dv"))
