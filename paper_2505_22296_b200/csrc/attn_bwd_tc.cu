@@ -31,7 +31,19 @@ constexpr int BQ = 64;
 #ifndef BWD_NSTG
 #define BWD_NSTG 1
 #endif
+#ifndef BWD_SMW
+#define BWD_SMW 4
+#endif
 constexpr int NST = BWD_NST;                // Q/dO pipeline stages
+// Softmax-gradient warps: 4 (one per TMEM lane quadrant, 64 queries per thread) or 8 (two per
+// quadrant, 32 queries each: two warps per SMSP hide each other's latency chains).
+constexpr int NSMW = BWD_SMW;
+constexpr int DRAIN0 = NSMW;               // first of the 4 dQ drain warps
+constexpr int PRODW = DRAIN0 + 4, TALLOCW = PRODW + 1, MMAW = PRODW + 3;
+constexpr int NTHREADS = (PRODW + 4) * 32;
+// registers per thread: softmax / drain / control, sum over warps <= 2048
+constexpr int REG_SM = NSMW == 4 ? 232 : 160, REG_DQ = NSMW == 4 ? 120 : 96, REG_CTL = NSMW == 4 ? 152 : 96;
+static_assert(NSMW * REG_SM + 4 * REG_DQ + 4 * REG_CTL <= 2048, "register budget");
 constexpr int NSTG = BWD_NSTG;              // dQ staging slots per drain warp
 constexpr int KV_TILE = 128 * D * 2;        // 32 KB (two 16 KB column blocks)
 constexpr int Q_TILE = BQ * D * 2;          // 16 KB (two 8 KB column blocks)
@@ -109,7 +121,7 @@ __device__ __forceinline__ void grad_chunk(const uint32_t (&rs)[32], const uint3
 // SV: softmax-loop variant bits (A/B builds, SPATTN_BWD_SV): 1 prefetch chunk 1's TMEM loads,
 // 2 packed fp32x2 math, 4 separate full / masked code paths, 8 FMA-pipe exp2 for 1 pair in 4
 template <int SV>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(NTHREADS, 1)
     attn_bwd_tc_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                            const __grid_constant__ CUtensorMap tmDQ, BwdArgs a, ProblemSet ps) {
@@ -158,23 +170,23 @@ __global__ void __launch_bounds__(384, 1)
       const bool many = (i >= E_PR && i < E_PR + 2) || (i >= E_DQF && i < E_DQF + 2);
       // a stage is full after the TMA bytes and the producer warp's 32 lse/delta stores
       const bool stage = i >= E_QF && i < E_QF + NST;
-      tc::mbar_init(bar(i), many ? 128 : stage ? 33 : 1);
+      const bool pr = i >= E_PR && i < E_PR + 2;
+      tc::mbar_init(bar(i), pr ? 32 * NSMW : many ? 128 : stage ? 33 : 1);
     }
     tc::fence_barrier_init();
   }
-  if (warp == 9) tc::tmem_alloc<512>(smem_u32(tmem_slot));
+  if (warp == TALLOCW) tc::tmem_alloc<512>(smem_u32(tmem_slot));
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tDV = tmem + 256, tDK = tmem + 384;
-  // per SMSP: 232 (softmax) + 120 (dQ) + 152 (control) <= 512 registers per thread slot
-  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 152;\n");
+  if (warp >= PRODW) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_CTL));
 
   // Roles. The scheduler favours the highest warp id, so the single-thread MMA issuer is the
   // last warp and the producer sits above the math warps: warps 0-3 softmax-gradient, 4-7 dQ
   // drain, 8 TMA producer, 9 TMEM allocator, 11 MMA issuer.
-  if (warp == 8) {
+  if (warp == PRODW) {
     // ------------------------------------------------------------------ TMA producer
     // lane 0 issues the TMA loads; all 32 lanes stage this tile's lse/delta (2 query rows each)
     // into the stage's smem slot and arrive on the stage barrier, so the softmax warpgroup
@@ -227,7 +239,7 @@ __global__ void __launch_bounds__(384, 1)
         tc::mbar_arrive(bar(E_QF + st));  // release: the stores above are visible to waiters
       }
     }
-  } else if (warp == 11) {
+  } else if (warp == MMAW) {
     // ---------------------------------------------------------------------- MMA issuer
     if (tc::elect_one() && T > 0) {
       constexpr uint32_t id_s = tc::idesc_bf16(128, BQ, false, false);  // S^T, dP^T
@@ -289,18 +301,20 @@ __global__ void __launch_bounds__(384, 1)
       tail(T - 1);
       tc::commit(bar(E_FIN));
     }
-  } else if (warp < 4) {
+  } else if (warp < NSMW) {
     // ----------------------------------------------- softmax-gradient warpgroup (lane = key)
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
-    const int t = threadIdx.x;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_SM));
+    const int t = (warp & 3) * 32 + (threadIdx.x & 31);  // key row within the tile == TMEM lane
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    // query chunks of 32 this warp owns: both (4 warps) or chunk warp/4 (8 warps)
+    const int cc_lo = NSMW == 8 ? warp >> 2 : 0, cc_hi = NSMW == 8 ? cc_lo + 1 : 2;
     const float sl2 = a.scale * kLog2e;
     const int c = n0 + t;
     for (int it = 0; it < T; ++it) {
       const int b = it & 1;
       const int m0 = m_begin + (it % nqt) * BQ;
       const int lb = (it % NST) * 64;  // this tile's lse/delta slot (complete once S^T is)
-      if (t == 0) TR(8, it);
+      if (warp == 0 && t == 0) TR(8, it);
       int ilo = 0, ihi = min(BQ, P.nq - m0);
       if (c >= P.nk) ihi = 0;
       if (P.causal) ilo = max(0, c - P.off - m0);
@@ -309,17 +323,17 @@ __global__ void __launch_bounds__(384, 1)
       tc::mbar_wait(bar(E_DPF + b), (it >> 1) & 1);
       if (it >= 2) tc::mbar_wait(bar(E_MD + b), ((it - 2) >> 1) & 1);  // dS^T_b read by dK/dQ
       tc::fence_after();
-      if (t == 0) TR(9, it);
+      if (warp == 0 && t == 0) TR(9, it);
       const uint32_t ds = sdS + b * 16384;
       // both 32-query chunks of S^T / dP^T are loaded up front; chunk 1's loads fly while
       // chunk 0 is computed (one TMEM round trip per tile instead of two)
       uint32_t rs[2][32], rp[2][32];
-      tc::tmem_ld32(tmem + lane_base + 64 * b, rs[0]);
-      tc::tmem_ld32(tmem + lane_base + 128 + 64 * b, rp[0]);
+      tc::tmem_ld32(tmem + lane_base + 64 * b + cc_lo * 32, rs[cc_lo]);
+      tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + cc_lo * 32, rp[cc_lo]);
       tc::tmem_wait_ld();
-      tc::reg_fence(rs[0]);
-      tc::reg_fence(rp[0]);
-      if (SV & 1) {
+      tc::reg_fence(rs[cc_lo]);
+      tc::reg_fence(rp[cc_lo]);
+      if ((SV & 1) && NSMW == 4) {
         tc::tmem_ld32(tmem + lane_base + 64 * b + 32, rs[1]);
         tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, rp[1]);
       }
@@ -328,8 +342,8 @@ __global__ void __launch_bounds__(384, 1)
       const uint64_t sl2x2 = f2_pack(sl2, sl2), sc2 = f2_pack(a.scale, a.scale);
       constexpr bool PK = SV & 2, PO = SV & 8;
 #pragma unroll
-      for (int cc = 0; cc < BQ / 32; ++cc) {
-        if (cc == 1) {
+      for (int cc = cc_lo; cc < cc_hi; ++cc) {
+        if (NSMW == 4 && cc == 1) {
           if (!(SV & 1)) {
             tc::tmem_ld32(tmem + lane_base + 64 * b + 32, rs[1]);
             tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, rp[1]);
@@ -360,14 +374,16 @@ __global__ void __launch_bounds__(384, 1)
       tc::fence_proxy_async();
       tc::fence_before();
       tc::mbar_arrive(bar(E_PR + b));
-      if (t == 0) TR(10, it);
+      if (warp == 0 && t == 0) TR(10, it);
     }
     if (T > 0) {  // dV epilogue
       tc::mbar_wait(bar(E_FIN), 0);
       tc::fence_after();
       float* dv = a.dv_acc + (int64_t)(P.k_row0 + c) * a.dkv_row_stride + kvh * D;
+      constexpr int NC = D / 32 / (NSMW / 4);  // 32-column chunks of dV per warp
 #pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) {
+      for (int ci = 0; ci < NC; ++ci) {
+        const int cc = (NSMW == 8 ? (warp >> 2) * NC : 0) + ci;
         uint32_t r[32];
         tc::tmem_ld32(tDV + lane_base + cc * 32, r);
         tc::tmem_wait_ld();
@@ -379,10 +395,10 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= DRAIN0 && warp < DRAIN0 + 4) {
     // ------------------------------------------- dQ warpgroup (lane = head-dim index)
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 120;\n");
-    const int w = warp - 4, lane = threadIdx.x % 32;
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_DQ));
+    const int w = warp - DRAIN0, lane = threadIdx.x % 32;
     const uint32_t lane_base = (uint32_t)(w * 32) << 16;
     const uint32_t stg0 = sStg + w * NSTG * 8192;  // NSTG x [64 queries x 32 fp32], 128B-swizzled rows
     for (int it = 0; it < T; ++it) {
@@ -440,7 +456,7 @@ __global__ void __launch_bounds__(384, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 9) tc::tmem_dealloc<512>(tmem);
+  if (warp == TALLOCW) tc::tmem_dealloc<512>(tmem);
 }
 
 int max_rows(const ProblemSet& ps, bool q) {
@@ -484,7 +500,7 @@ void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t
   auto launch = [&](auto kern) {
     static std::once_flag once;
     std::call_once(once, [&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM); });
-    kern<<<dim3(tiles * a.hm.hkv), 384, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
+    kern<<<dim3(tiles * a.hm.hkv), NTHREADS, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
   };
   switch (sv) {
     case 0: launch(attn_bwd_tc_q64_kernel<0>); break;
