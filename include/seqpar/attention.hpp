@@ -131,7 +131,8 @@ std::vector<std::array<int, 6>> plan_problems(const std::vector<int64_t>& qpos,
                                               const Documents* docs, int64_t* pairs);
 
 // Which attention kernel family the engines launch.
-enum class KernelFamily { tcgen05, mma, tcgen05_pp };  // tcgen05_pp: two-tile ping-pong forward
+// tcgen05_pp: two-tile ping-pong forward; tcgen05_pair: CTA-pair (cta_group::2) forward for d=128
+enum class KernelFamily { tcgen05, mma, tcgen05_pp, tcgen05_pair };
 void set_kernel_family(KernelFamily f);
 KernelFamily kernel_family();
 

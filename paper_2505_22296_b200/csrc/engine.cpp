@@ -255,11 +255,17 @@ void launch_add_tasks_f32(const CopyTaskSet& ts, cudaStream_t s);
 bool tc_fwd_pp_supported(const FwdArgs& a);
 void launch_attn_fwd_tc_pp(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s);
 
+bool tc_fwd_pair_supported(const FwdArgs& a);
+void launch_attn_fwd_pair(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s);
+
 void launch_attn_fwd(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
   // the 1-tile kernel measures faster; the two-tile ping-pong forward is a selectable family
   const bool use_pp = seqpar::kernel_family() == seqpar::KernelFamily::tcgen05_pp || getenv("SPATTN_FWD_PP");
+  const bool pair = seqpar::kernel_family() == seqpar::KernelFamily::tcgen05_pair || getenv("SPATTN_FWD_PAIR");
   if (use_pp && tc_fwd_pp_supported(a))
     launch_attn_fwd_tc_pp(a, ps, s);
+  else if (pair && seqpar::kernel_family() != seqpar::KernelFamily::mma && tc_fwd_pair_supported(a))
+    launch_attn_fwd_pair(a, ps, s);
   else if (seqpar::kernel_family() != seqpar::KernelFamily::mma && tc_fwd_supported(a))
     launch_attn_fwd_tc(a, ps, s);
   else

@@ -31,7 +31,7 @@ def rel(a, b):
 
 @pytest.mark.parametrize("L,H,Hkv,d,causal", [(2048, 8, 2, 128, True), (1536, 4, 4, 64, True),
                                               (1024, 4, 1, 128, False), (1920, 6, 2, 64, True)])
-@pytest.mark.parametrize("family", ["tcgen05", "mma", "tcgen05_pp"])
+@pytest.mark.parametrize("family", ["tcgen05", "mma", "tcgen05_pp", "tcgen05_pair"])
 def test_multi_tile_attention_vs_torch(L, H, Hkv, d, causal, family):
     import paper_2505_22296_b200 as P
 
