@@ -33,15 +33,21 @@ constexpr int Q_TILE = 128 * D * 2;   // 32 KB: this CTA's 128 query rows
 constexpr int KH = 64 * D * 2;        // 16 KB: half a key tile (64 keys x 128 dims, 2 column blocks)
 constexpr int VH = 128 * 64 * 2;      // 16 KB: half a value tile (128 keys x 64 dims)
 constexpr int P_TILE = 128 * 128 * 2; // 32 KB
+#ifndef FWD_PAIR_KST
+#define FWD_PAIR_KST 3
+#endif
+constexpr int KST = FWD_PAIR_KST;          // K / V pipeline stages (the half tiles leave room for 3)
 constexpr int Q_OFF = 0;
-constexpr int K_OFF = Q_OFF + Q_TILE;      // 2 stages
-constexpr int V_OFF = K_OFF + 2 * KH;      // 2 stages
-constexpr int P_OFF = V_OFF + 2 * VH;      // 2 buffers
+constexpr int K_OFF = Q_OFF + Q_TILE;
+constexpr int V_OFF = K_OFF + KST * KH;
+constexpr int P_OFF = V_OFF + KST * VH;    // 2 buffers
 constexpr int BAR_OFF = P_OFF + 2 * P_TILE;
+static_assert(BAR_OFF + 256 + 2 * 2 * 128 * 4 <= 227 * 1024, "shared memory");
 constexpr int XCH_OFF = BAR_OFF + 256;
 constexpr int SMEM = XCH_OFF + 2 * 2 * 128 * 4;
 
-enum Bar { B_Q = 0, B_KF = 1, B_VF = 3, B_SF = 5, B_SFREE = 7, B_PF = 9, B_PV = 11, B_N = 13 };
+enum Bar { B_Q = 0, B_KF = 1, B_VF = B_KF + KST, B_SF = B_VF + KST, B_SFREE = B_SF + 2, B_PF = B_SFREE + 2,
+           B_PV = B_PF + 2, B_N = B_PV + 2 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(352, 1)
     attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -99,8 +105,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(352, 1)
       for (int b = 0; b < 2; ++b)
         tc::tma_load_2d_pair(sQ + b * 16384, &tmQ, h * D + b * 64, P.q_row0 + m0, lbar(B_Q));
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        if (j >= 2) tc::mbar_wait(bar(B_SF + st), ((j - 2) >> 1) & 1);  // S(j-2) read the stage
+        const int st = j % KST;
+        if (j >= KST) tc::mbar_wait(bar(B_SF + ((j - KST) & 1)), ((j - KST) >> 1) & 1);  // S(j-KST) read it
         if (leader) tc::mbar_expect_tx(bar(B_KF + st), 2 * KH);
         for (int b = 0; b < 2; ++b)
           tc::tma_load_2d_pair(sK + st * KH + b * 8192, &tmK, kvh * D + b * 64, P.k_row0 + j * 128 + 64 * rank,
@@ -112,8 +118,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(352, 1)
     if (tc::elect_one() && n_tiles > 0) {
       tc::tma_prefetch(&tmV);
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        if (j >= 2) tc::mbar_wait(bar(B_PV + st), ((j - 2) >> 1) & 1);  // PV(j-2) read the stage
+        const int st = j % KST;
+        if (j >= KST) tc::mbar_wait(bar(B_PV + ((j - KST) & 1)), ((j - KST) >> 1) & 1);  // PV(j-KST) read it
         if (leader) tc::mbar_expect_tx(bar(B_VF + st), 2 * VH);
         tc::tma_load_2d_pair(sV + st * VH, &tmV, kvh * D + 64 * rank, P.k_row0 + j * 128, lbar(B_VF + st));
       }
@@ -123,11 +129,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(352, 1)
       constexpr uint32_t id_s = tc::idesc_bf16(256, 128, false, false);
       constexpr uint32_t id_o = tc::idesc_bf16(256, D, false, true);
       auto issue_s = [&](int j) {
-        const int st = j & 1;
-        tc::mbar_wait(bar(B_KF + st), (j >> 1) & 1);
+        const int st = j & 1, ks_ = j % KST;
+        tc::mbar_wait(bar(B_KF + ks_), (j / KST) & 1);
         if (j >= 2) tc::mbar_wait(bar(B_SFREE + st), ((j - 2) >> 1) & 1);
         tc::fence_after();
-        const uint32_t kbase = sK + st * KH;
+        const uint32_t kbase = sK + ks_ * KH;
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t qo = (ks >> 2) * 16384 + (ks & 3) * 32, ko = (ks >> 2) * 8192 + (ks & 3) * 32;
@@ -137,11 +143,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(352, 1)
         tc::commit_pair(bar(B_SF + st), 0x3);
       };
       auto issue_pv = [&](int i) {
-        const int st = i & 1;
+        const int st = i & 1, vs = i % KST;
         tc::mbar_wait(bar(B_PF + st), (i >> 1) & 1);
-        tc::mbar_wait(bar(B_VF + st), (i >> 1) & 1);
+        tc::mbar_wait(bar(B_VF + vs), (i / KST) & 1);
         tc::fence_after();
-        const uint32_t pbase = sP + st * P_TILE, vbase = sV + st * VH;
+        const uint32_t pbase = sP + st * P_TILE, vbase = sV + vs * VH;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;
