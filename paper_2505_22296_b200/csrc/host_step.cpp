@@ -83,14 +83,15 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
   const int nslots = std::min(ng, 2);
   std::vector<Slot> slots(static_cast<size_t>(nslots));
   auto cleanup = [&] {
+    // copies in flight (also on an error path) finish before the slots go back to the pool
+    cudaStreamSynchronize(up);
+    cudaStreamSynchronize(down);
     for (auto& s : slots) {
       for (void* p : {s.q, s.k, s.v, s.dout, s.out, s.dq, s.dk, s.dv, static_cast<void*>(s.lse)})
         if (p) cudaFreeAsync(p, cs);
       for (cudaEvent_t e : {s.loaded, s.computed, s.drained})
         if (e) cudaEventDestroy(e);
     }
-    cudaStreamSynchronize(up);
-    cudaStreamSynchronize(down);
     cudaStreamDestroy(up);
     cudaStreamDestroy(down);
   };
