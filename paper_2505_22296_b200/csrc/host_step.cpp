@@ -30,7 +30,7 @@ struct Slot {
   void *q = nullptr, *k = nullptr, *v = nullptr, *dout = nullptr, *out = nullptr;
   void *dq = nullptr, *dk = nullptr, *dv = nullptr;
   float* lse = nullptr;
-  cudaEvent_t loaded = nullptr, computed = nullptr, drained = nullptr;
+  cudaEvent_t loaded = nullptr, dout_loaded = nullptr, computed = nullptr, drained = nullptr;
 };
 
 bool group_ok(Engine e, const AttentionConfig& c, int sp, int ng) {
@@ -77,30 +77,38 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
   const size_t qpitch = static_cast<size_t>(H) * d * 2, kpitch = static_cast<size_t>(Hkv) * d * 2;
   const size_t qw = static_cast<size_t>(hg) * d * 2, kw = static_cast<size_t>(kg) * d * 2;
 
-  cudaStream_t cs = ctx.stream, up = nullptr, down = nullptr;
+  // Single-device steps alternate groups over two compute streams so one group's backward tail
+  // overlaps the next group's forward; with collectives (sp > 1) one stream keeps every rank's
+  // NCCL calls in the same order.
+  cudaStream_t cs = ctx.stream, cs2 = nullptr, up = nullptr, down = nullptr;
+  const bool dual = sp == 1 && ng > 1;
   HS_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
   HS_CUDA(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
-  const int nslots = std::min(ng, 2);
+  if (dual) HS_CUDA(cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking));
+  const int nslots = std::min(ng, dual ? 4 : 2);
   std::vector<Slot> slots(static_cast<size_t>(nslots));
   auto cleanup = [&] {
     // copies in flight (also on an error path) finish before the slots go back to the pool
     cudaStreamSynchronize(up);
     cudaStreamSynchronize(down);
+    if (cs2) cudaStreamSynchronize(cs2);
+    ctx.stream = cs;
     for (auto& s : slots) {
       for (void* p : {s.q, s.k, s.v, s.dout, s.out, s.dq, s.dk, s.dv, static_cast<void*>(s.lse)})
         if (p) cudaFreeAsync(p, cs);
-      for (cudaEvent_t e : {s.loaded, s.computed, s.drained})
+      for (cudaEvent_t e : {s.loaded, s.dout_loaded, s.computed, s.drained})
         if (e) cudaEventDestroy(e);
     }
     cudaStreamDestroy(up);
     cudaStreamDestroy(down);
+    if (cs2) cudaStreamDestroy(cs2);
   };
   try {
     for (auto& s : slots) {
       for (void** p : {&s.q, &s.dout, &s.out, &s.dq}) HS_CUDA(cudaMallocAsync(p, qb, cs));
       for (void** p : {&s.k, &s.v, &s.dk, &s.dv}) HS_CUDA(cudaMallocAsync(p, kb, cs));
       HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s.lse), static_cast<size_t>(rows * hg * 4), cs));
-      for (cudaEvent_t* e : {&s.loaded, &s.computed, &s.drained})
+      for (cudaEvent_t* e : {&s.loaded, &s.dout_loaded, &s.computed, &s.drained})
         HS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
     // slots allocated on the compute stream must exist before the copy streams touch them
@@ -109,6 +117,7 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
     HS_CUDA(cudaEventRecord(ready, cs));
     HS_CUDA(cudaStreamWaitEvent(up, ready, 0));
     HS_CUDA(cudaStreamWaitEvent(down, ready, 0));
+    if (cs2) HS_CUDA(cudaStreamWaitEvent(cs2, ready, 0));
     cudaEventDestroy(ready);
 
     auto h2d = [&](void* dst, const void* src, size_t col_bytes, size_t width, size_t pitch) {
@@ -125,22 +134,27 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
       h2d(s.q, hq, g * qw, qw, qpitch);
       h2d(s.k, hk, g * kw, kw, kpitch);
       h2d(s.v, hv, g * kw, kw, kpitch);
+      HS_CUDA(cudaEventRecord(s.loaded, up));  // the forward starts while dout is in flight
       h2d(s.dout, hdout, g * qw, qw, qpitch);
-      HS_CUDA(cudaEventRecord(s.loaded, up));
+      HS_CUDA(cudaEventRecord(s.dout_loaded, up));
     };
     load(0);
     for (int g = 0; g < ng; ++g) {
       if (g + 1 < ng) load(g + 1);
       Slot& s = slots[static_cast<size_t>(g % nslots)];
-      HS_CUDA(cudaStreamWaitEvent(cs, s.loaded, 0));
+      cudaStream_t gs = (dual && (g & 1)) ? cs2 : cs;
+      ctx.stream = gs;
+      HS_CUDA(cudaStreamWaitEvent(gs, s.loaded, 0));
       const DeviceTensor tq{s.q, bs, lloc, hg, d}, tk{s.k, bs, lloc, kg, d}, tv{s.v, bs, lloc, kg, d};
       const DeviceTensor to{s.out, bs, lloc, hg, d};
       SavedPtr saved = run_attention_engine(ctx, engine, gc, layout, tq, tk, tv, to, s.lse, docs);
+      HS_CUDA(cudaStreamWaitEvent(gs, s.dout_loaded, 0));
       run_attention_engine_backward(ctx, *saved, DeviceTensor{s.dout, bs, lloc, hg, d},
                                     DeviceTensor{s.dq, bs, lloc, hg, d}, DeviceTensor{s.dk, bs, lloc, kg, d},
                                     DeviceTensor{s.dv, bs, lloc, kg, d});
       saved.reset();
-      HS_CUDA(cudaEventRecord(s.computed, cs));
+      ctx.stream = cs;
+      HS_CUDA(cudaEventRecord(s.computed, gs));
       HS_CUDA(cudaStreamWaitEvent(down, s.computed, 0));
       d2h(hdq, s.dq, g * qw, qw, qpitch);
       d2h(hdk, s.dk, g * kw, kw, kpitch);
@@ -154,8 +168,8 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
       HS_CUDA(cudaEventRecord(s.drained, down));
     }
     // the step completes on the compute stream (callers time / synchronise it)
-    HS_CUDA(cudaStreamWaitEvent(cs, slots[static_cast<size_t>((ng - 1) % nslots)].drained, 0));
-    if (nslots > 1) HS_CUDA(cudaStreamWaitEvent(cs, slots[static_cast<size_t>((ng - 2) % nslots)].drained, 0));
+    for (int g = std::max(0, ng - nslots); g < ng; ++g)
+      HS_CUDA(cudaStreamWaitEvent(cs, slots[static_cast<size_t>(g % nslots)].drained, 0));
   } catch (...) {
     cleanup();
     throw;
