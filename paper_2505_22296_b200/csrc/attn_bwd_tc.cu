@@ -256,10 +256,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int kk = 0; kk < BQ / 16; ++kk)
           tc::mma_ts(tDV, tmem + 64 * b + kk * 8, tc::sdesc(dO + kk * 2048, 8192, 1024), id_kv,
                      (i > 0 || kk > 0) ? 1u : 0u);
+        if constexpr ((SV & 64) != 0) {
+          // dS^T also sits in TMEM (the dead upper half of the S^T buffer): dK is a TS MMA and
+          // reads no A operand from shared memory
 #pragma unroll
-        for (int kk = 0; kk < BQ / 16; ++kk)
-          tc::mma_ss(tDK, tc::sdesc(ds + kk * 32, 16, 1024), tc::sdesc(q + kk * 2048, 8192, 1024), id_kv,
-                     (i > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BQ / 16; ++kk)
+            tc::mma_ts(tDK, tmem + 64 * b + 32 + kk * 8, tc::sdesc(q + kk * 2048, 8192, 1024), id_kv,
+                       (i > 0 || kk > 0) ? 1u : 0u);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < BQ / 16; ++kk)
+            tc::mma_ss(tDK, tc::sdesc(ds + kk * 32, 16, 1024), tc::sdesc(q + kk * 2048, 8192, 1024), id_kv,
+                       (i > 0 || kk > 0) ? 1u : 0u);
+        }
         tc::commit(bar(E_QE + st));
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
@@ -341,6 +350,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const float2* dl2 = reinterpret_cast<const float2*>(sDl + lb);   // delta per query
       const uint64_t sl2x2 = f2_pack(sl2, sl2), sc2 = f2_pack(a.scale, a.scale);
       constexpr bool PK = SV & 2, PO = SV & 8;
+      uint32_t wds[16];  // (SV & 64) chunk 0's dS^T, parked until chunk 1's S^T is out of TMEM
 #pragma unroll
       for (int cc = cc_lo; cc < cc_hi; ++cc) {
         if (NSMW == 4 && cc == 1) {
@@ -351,6 +361,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tc::tmem_wait_ld();
           tc::reg_fence(rs[1]);
           tc::reg_fence(rp[1]);
+          if constexpr ((SV & 64) != 0) tc::tmem_st16(tmem + lane_base + 64 * b + 32, wds);
         }
         uint32_t wp[16], wd[16];
         if (a.debug & 16) {  // profiling: no softmax-gradient math (wrong results)
@@ -363,6 +374,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                    ihi - cc * 32, wp, wd);
         }
         tc::tmem_st16(tmem + lane_base + 64 * b + cc * 16, wp);
+        if constexpr ((SV & 64) != 0) {
+          if (cc == 0) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) wds[i] = wd[i];
+          } else {
+            tc::tmem_st16(tmem + lane_base + 64 * b + 48, wd);
+          }
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t addr = tc::sw128(ds, t, cc * 4 + k);
@@ -496,7 +515,7 @@ void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t
     cudaGetLastError();
     return;
   }
-  static const int sv = getenv("SPATTN_BWD_SV") ? atoi(getenv("SPATTN_BWD_SV")) : 0;
+  static const int sv = getenv("SPATTN_BWD_SV") ? atoi(getenv("SPATTN_BWD_SV")) : 64;
   auto launch = [&](auto kern) {
     static std::once_flag once;
     std::call_once(once, [&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM); });
@@ -509,7 +528,8 @@ void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t
     case 7: launch(attn_bwd_tc_q64_kernel<7>); break;
     case 15: launch(attn_bwd_tc_q64_kernel<15>); break;
     case 11: launch(attn_bwd_tc_q64_kernel<11>); break;
-    default: launch(attn_bwd_tc_q64_kernel<0>); break;
+    case 64: launch(attn_bwd_tc_q64_kernel<64>); break;
+    default: launch(attn_bwd_tc_q64_kernel<64>); break;
   }
   note_launch();
 }
