@@ -207,8 +207,18 @@ struct FwdLayout {
 // so the next K load overlaps the current softmax instead of waiting for PV.
 enum FwdBar { B_Q = 0, B_KF = 1, B_VF = 3, B_SF = 5, B_SFREE = 7, B_PF = 9, B_PV = 11, B_N = 13 };
 
+#ifndef SPATTN_FWD_DUAL_ISSUE
+#define SPATTN_FWD_DUAL_ISSUE 0
+#endif
+// SPATTN_FWD_DUAL_ISSUE=1: two MMA issuers (warps 10 and 11), one per softmax stream (the
+// streams touch disjoint S / O accumulators, P buffers and K / V stages). It cuts a stream's
+// wait for its next S from 765 to 111 cycles, but the two softmax warps of an SMSP then overlap
+// their exp phases on the shared MUFU (16/clk/SM) and the tile period stays at ~1590 cycles
+// (1564 with one issuer), so the single issuer is the default.
+constexpr int kFwdThreads = SPATTN_FWD_DUAL_ISSUE ? 384 : 352;
+
 template <int D>
-__global__ void __launch_bounds__(352, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, FwdArgs a, ProblemSet ps) {
   using Lay = FwdLayout<D>;
@@ -287,7 +297,7 @@ __global__ void __launch_bounds__(352, 1)
                           bar(B_VF + st));
       }
     }
-  } else if (warp == 10) {
+  } else if (warp == 10 || (SPATTN_FWD_DUAL_ISSUE && warp == 11)) {
     if (tc::elect_one()) {
       constexpr uint32_t id_s = tc::idesc_bf16(128, 128, false, false);
       constexpr uint32_t id_o = tc::idesc_bf16(128, D, false, true);
@@ -330,14 +340,26 @@ __global__ void __launch_bounds__(352, 1)
       };
       // order S0 S1 | S2 PV0 | S3 PV1 | ...: S(j+2) only needs group j&1 to have read S(j) out of
       // TMEM (early in its softmax), so it runs while that softmax is still computing P(j)
-      if (n_tiles > 0) {
-        tc::mbar_wait(bar(B_Q), 0);
-        issue_s(0);
-      }
-      if (n_tiles > 1) issue_s(1);
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 2 < n_tiles) issue_s(j + 2);
-        issue_pv(j);
+      if (SPATTN_FWD_DUAL_ISSUE) {
+        const int g = warp - 10;  // this issuer's stream: key tiles j = g (mod 2)
+        if (n_tiles > g) {
+          tc::mbar_wait(bar(B_Q), 0);
+          issue_s(g);
+        }
+        for (int j = g; j < n_tiles; j += 2) {
+          if (j + 2 < n_tiles) issue_s(j + 2);
+          issue_pv(j);
+        }
+      } else {
+        if (n_tiles > 0) {
+          tc::mbar_wait(bar(B_Q), 0);
+          issue_s(0);
+        }
+        if (n_tiles > 1) issue_s(1);
+        for (int j = 0; j < n_tiles; ++j) {
+          if (j + 2 < n_tiles) issue_s(j + 2);
+          issue_pv(j);
+        }
       }
     }
   } else if (warp < 8) {
@@ -561,7 +583,7 @@ void launch_fwd_tc_d(const FwdArgs& a, const ProblemSet& in, cudaStream_t s) {
     cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          FwdLayout<D>::SMEM);
   });
-  attn_fwd_tc_kernel<D><<<dim3(tiles, a.hm.hq), 352, FwdLayout<D>::SMEM, s>>>(tq, tk, tv, a, ps);
+  attn_fwd_tc_kernel<D><<<dim3(tiles, a.hm.hq), kFwdThreads, FwdLayout<D>::SMEM, s>>>(tq, tk, tv, a, ps);
   note_launch();
 }
 
