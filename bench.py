@@ -247,6 +247,7 @@ def main():
         step(*ptrs)
     barrier()
     n0 = C.lib().spattn_launch_count()
+    C.check(C.lib().spattn_ctx_reset_stats(ctx))
     C.check(C.lib().spattn_profile_enable(1))
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clocks:
@@ -258,6 +259,12 @@ def main():
         barrier()
     C.check(C.lib().spattn_profile_enable(0))
     launches = (C.lib().spattn_launch_count() - n0) / args.steps
+    step_bytes = 0  # send-side bytes per rank per step (all_to_all + p2p + ...), library counters
+    for prim in range(len(C.PRIMITIVES)):
+        calls_, bytes_ = ctypes.c_int64(), ctypes.c_int64()
+        C.check(C.lib().spattn_ctx_stats(ctx, prim, ctypes.byref(calls_), ctypes.byref(bytes_)))
+        step_bytes += bytes_.value
+    step_bytes /= args.steps
     ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
     kms, kn = (ctypes.c_double * 2)(), (ctypes.c_int64 * 2)()
     C.check(C.lib().spattn_profile_read(kms, kn))
@@ -292,6 +299,32 @@ def main():
         return {"value": L / (ems / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ems,
                 "api": "spattn_step_host (C ABI, pinned host buffers)", "head_groups": groups}
+
+    # the metric's second half at N>1: all-to-all NVLink GB/s of this library's collective
+    # (one q-shaped sequence->head exchange, send-side bytes per rank / device time, max over ranks)
+    comm = None
+    if world > 1:
+        try:
+            a2a_out = torch.empty(1, lloc * world, heads // world, d, device="cuda", dtype=torch.bfloat16)
+
+            def a2a():
+                C.check(C.lib().spattn_all_to_all(ctx, q.data_ptr(), a2a_out.data_ptr(), 1, lloc, heads, d, 2,
+                                                  2, 1))
+
+            for _ in range(3):
+                a2a()
+            barrier()
+            ev0.record(stream)
+            for _ in range(10):
+                a2a()
+            ev1.record(stream)
+            barrier()
+            cms = max_over_ranks(ev0.elapsed_time(ev1)) / 10
+            sent = q.numel() * 2 * (world - 1) / world
+            comm = {"a2a_bytes_per_rank": sent, "a2a_ms": cms, "a2a_gbs": sent / (cms / 1e3) / 1e9,
+                    "step_bytes_per_rank": step_bytes}
+        except Exception as ex:  # noqa: BLE001
+            comm = {"error": str(ex)[:200]}
 
     e2e = None
     if not args.no_e2e:
@@ -350,6 +383,8 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if comm:
+        line["comm"] = comm
     if world == 1 and not args.no_cpu_baseline:
         try:
             cb = cpu_reference_sample(heads, kv, d, L)

@@ -209,6 +209,10 @@ int spattn_fabric_fwd_rope(spattn_fabric* f, int engine, const spattn_config* cf
                            spattn_saved** saved);
 int spattn_fabric_bwd(spattn_fabric* f, spattn_saved* const* saved, const void* const* dout,
                       void* const* dq, void* const* dk, void* const* dv);
+/* all_to_all (comm.cpp:357-379) over a rank context's SP group (NCCL: every rank calls it);
+ * device [bs, len, heads, dim] tensors of elem_bytes each, on the context's stream */
+int spattn_all_to_all(spattn_ctx* ctx, const void* local, void* out, int64_t bs, int64_t len,
+                      int64_t heads, int64_t dim, int elem_bytes, int scatter_dim, int gather_dim);
 /* all_to_all (comm.cpp:357-379) on [bs, len, heads, dim] tensors of elem_bytes each */
 int spattn_fabric_all_to_all(spattn_fabric* f, const void* const* local, void* const* out,
                              int64_t bs, int64_t len, int64_t heads, int64_t dim, int elem_bytes,

@@ -415,6 +415,14 @@ int spattn_fabric_all_to_all(spattn_fabric* f, const void* const* local, void* c
   });
 }
 
+int spattn_all_to_all(spattn_ctx* ctx, const void* local, void* out, int64_t bs, int64_t len,
+                      int64_t heads, int64_t dim, int elem_bytes, int scatter_dim, int gather_dim) {
+  return guard([&] {
+    seqpar::all_to_all(*ctx->rc, ctx->rc->sp_group, local, bs, len, heads, dim, elem_bytes, scatter_dim,
+                       gather_dim, out);
+  });
+}
+
 int spattn_block_fwd(void* stream, int64_t bs, int heads, int kv_heads, int dim, const void* q,
                      const int64_t* qpos, int64_t lq, const void* k, const void* v,
                      const int64_t* kpos, int64_t lk, int causal, double scale, float* acc_out,

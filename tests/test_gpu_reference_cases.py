@@ -89,3 +89,37 @@ def test_local_position_ids_corrupt_the_rotary_phases(P):
     single = run(P, "oracle", q, k, v, R, 1, layout="naive", position_ids=list(range(L)))
     for key in ("out", "lse"):
         assert np.max(np.abs(glob[key] - single[key])) <= 2e-2 * max(1.0, np.max(np.abs(single[key]))), key
+
+
+def test_rank_all_to_all_matches_fabric_driver(P):
+    """spattn_all_to_all on each rank's context (one thread per rank, the call an NCCL rank makes)
+    equals the fabric's group driver and the reference's a2a semantics (comm.cpp:278-321)."""
+    import threading
+
+    import torch
+
+    from paper_2505_22296_b200 import _lib as C
+
+    sp, L, H, d = 4, 64, 8, 16
+    fab = P.Fabric(sp)
+    xs = [torch.randn(1, L, H, d, device="cuda").bfloat16() for _ in range(sp)]
+    want = fab.all_to_all(xs, 2, 1)
+    outs = [torch.empty_like(w) for w in want]
+    torch.cuda.synchronize()
+    errs = []
+
+    def rank(r):
+        try:
+            C.check(C.lib().spattn_all_to_all(fab.ctxs[r], xs[r].data_ptr(), outs[r].data_ptr(), 1, L, H, d, 2, 2, 1))
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(sp)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=60)
+    torch.cuda.synchronize()
+    assert not errs, errs
+    for a, b in zip(outs, want):
+        assert torch.equal(a, b)
