@@ -399,16 +399,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int i = 0; i < 128; ++i) x[i] = i <= lim ? x[i] : -INFINITY;
       }
-      // max over raw scores (sl2 > 0); four independent chains
-      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#ifndef SPATTN_FWD_MAX_CHAINS
+#define SPATTN_FWD_MAX_CHAINS 4
+#endif
+      // max over raw scores (sl2 > 0); independent 3-input-max chains, then a tree
+      constexpr int NCH = SPATTN_FWD_MAX_CHAINS;
+      float mx[NCH];
 #pragma unroll
-      for (int i = 0; i < 128; i += 8) {
-        mx[0] = fmaxf(mx[0], fmaxf(x[i], x[i + 1]));
-        mx[1] = fmaxf(mx[1], fmaxf(x[i + 2], x[i + 3]));
-        mx[2] = fmaxf(mx[2], fmaxf(x[i + 4], x[i + 5]));
-        mx[3] = fmaxf(mx[3], fmaxf(x[i + 6], x[i + 7]));
+      for (int c = 0; c < NCH; ++c) mx[c] = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 128; i += 2 * NCH) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) mx[c] = fmaxf(mx[c], fmaxf(x[i + 2 * c], x[i + 2 * c + 1]));
       }
-      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sl2;
+#pragma unroll
+      for (int w = NCH / 2; w > 0; w /= 2) {
+#pragma unroll
+        for (int c = 0; c < w; ++c) mx[c] = fmaxf(mx[c], mx[c + w]);
+      }
+      const float mt = mx[0] * sl2;
       if (row == 0) FTR(9, j);
       if (it == 0) {
         m_run = mt;
