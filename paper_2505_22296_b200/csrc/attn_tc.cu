@@ -207,6 +207,13 @@ struct FwdLayout {
 // so the next K load overlaps the current softmax instead of waiting for PV.
 enum FwdBar { B_Q = 0, B_KF = 1, B_VF = 3, B_SF = 5, B_SFREE = 7, B_PF = 9, B_PV = 11, B_N = 13 };
 
+#ifndef SPATTN_FWD_P_TMEM
+#define SPATTN_FWD_P_TMEM 0
+#endif
+// SPATTN_FWD_P_TMEM=1: P is written back over its own S columns in TMEM (bf16 pairs) and
+// O += P V is a TS MMA — no P tile in shared memory (the SS kernel moves 224 KB of smem per
+// tile: 128 KB operand reads, 64 KB K/V TMA writes, 32 KB P stores). PV(j) must then precede
+// S(j+2) (which overwrites those columns), so the issue order is PV-first.
 #ifndef SPATTN_FWD_DUAL_ISSUE
 #define SPATTN_FWD_DUAL_ISSUE 0
 #endif
@@ -331,9 +338,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const uint32_t pbase = sP + st * Lay::P_TILE, vbase = sV + st * Lay::TILE;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;
-          tc::mma_ss(tO + st * D, tc::sdesc(pbase + aoff, 16, 1024),
-                     tc::sdesc(vbase + kk * 2048, 16384, 1024), id_o, (i > 1 || kk > 0) ? 1u : 0u);
+          if (SPATTN_FWD_P_TMEM) {
+            tc::mma_ts(tO + st * D, tmem + st * 128 + kk * 8, tc::sdesc(vbase + kk * 2048, 16384, 1024), id_o,
+                       (i > 1 || kk > 0) ? 1u : 0u);
+          } else {
+            const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;
+            tc::mma_ss(tO + st * D, tc::sdesc(pbase + aoff, 16, 1024),
+                       tc::sdesc(vbase + kk * 2048, 16384, 1024), id_o, (i > 1 || kk > 0) ? 1u : 0u);
+          }
         }
         tc::commit(bar(B_PV + st));  // also releases V stage st
         FTR(4, i);
@@ -347,8 +359,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           issue_s(g);
         }
         for (int j = g; j < n_tiles; j += 2) {
-          if (j + 2 < n_tiles) issue_s(j + 2);
+          if (!SPATTN_FWD_P_TMEM && j + 2 < n_tiles) issue_s(j + 2);
           issue_pv(j);
+          if (SPATTN_FWD_P_TMEM && j + 2 < n_tiles) issue_s(j + 2);
+        }
+      } else if (SPATTN_FWD_P_TMEM) {
+        if (n_tiles > 0) {
+          tc::mbar_wait(bar(B_Q), 0);
+          issue_s(0);
+        }
+        if (n_tiles > 1) issue_s(1);
+        for (int j = 0; j < n_tiles; ++j) {
+          issue_pv(j);  // reads P(j) from S buffer j&1 before S(j+2) overwrites it (pipe order)
+          if (j + 2 < n_tiles) issue_s(j + 2);
         }
       } else {
         if (n_tiles > 0) {
@@ -461,14 +484,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         rs2[e & 1] = f2_add(rs2[e & 1], f2_pack(pv.x, pv.y));
         pw[e] = pack_bf16(pv.x, pv.y);
       }
-      // P buffer g was last read by PV(j-2); the wait is usually already satisfied here
-      if (it > 0) tc::mbar_wait(bar(B_PV + g), (it - 1) & 1);
-      const uint32_t pbase = sP + g * Lay::P_TILE;
+      if (SPATTN_FWD_P_TMEM) {
+        // P(j) over the first 64 columns of this group's S buffer (its S values are in x[] now)
+        tc::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pw[0]));
+        tc::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pw[32]));
+        tc::tmem_wait_st();
+      } else {
+        // P buffer g was last read by PV(j-2); the wait is usually already satisfied here
+        if (it > 0) tc::mbar_wait(bar(B_PV + g), (it - 1) & 1);
+        const uint32_t pbase = sP + g * Lay::P_TILE;
 #pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {
-        const uint32_t addr = tc::sw128(pbase + (ch >> 3) * 16384, row, ch & 7);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(pw[4 * ch]),
-                     "r"(pw[4 * ch + 1]), "r"(pw[4 * ch + 2]), "r"(pw[4 * ch + 3]));
+        for (int ch = 0; ch < 16; ++ch) {
+          const uint32_t addr = tc::sw128(pbase + (ch >> 3) * 16384, row, ch & 7);
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(pw[4 * ch]),
+                       "r"(pw[4 * ch + 1]), "r"(pw[4 * ch + 2]), "r"(pw[4 * ch + 3]));
+        }
       }
       {
         const float2 r = f2_unpack(f2_add(rs2[0], rs2[1]));
