@@ -123,3 +123,26 @@ def test_rank_all_to_all_matches_fabric_driver(P):
     assert not errs, errs
     for a, b in zip(outs, want):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("engine,sp", [("ulysses", 2), ("ring", 2), ("dummy_head", 4)])
+def test_batched_varlen_with_rope(P, engine, sp):
+    """bs=2 neat-packed batches (the same document cut for every batch entry) with RoPE at
+    per-document reset ids, against the composed per-document oracle."""
+    import seqpar_oracle as O
+
+    docs = [100, 60, 96]
+    L = sum(docs)
+    H = 6 if engine == "dummy_head" else 4
+    q, k, v, R = parity_inputs(81 + sp, L, H, 2, 64, bs=2)
+    ids = P.document_position_ids(docs)
+    res = run(P, engine, q, k, v, R, sp, docs=docs, position_ids=ids)
+    qr, kr = O.rope_apply(q, ids), O.rope_apply(k, ids)
+    orc = O.varlen_attention_fwd_bwd(qr, kr, v, R, docs)
+    orc["dq"] = O.rope_apply(orc["dq"], ids, inverse=True)
+    orc["dk"] = O.rope_apply(orc["dk"], ids, inverse=True)
+    ref = torch_ref(O.bf16_round(qr), O.bf16_round(kr), v, R, docs=docs)
+    ref["dq"] = O.bf16_round(O.rope_apply(ref["dq"], ids, inverse=True))
+    ref["dk"] = O.bf16_round(O.rope_apply(ref["dk"], ids, inverse=True))
+    for key in ("out", "dq", "dk", "dv"):
+        assert_close(key, res[key], orc[key], ref[key])
