@@ -716,9 +716,19 @@ void plain_forward(RankCtx& ctx, const Local& L, int d, const std::vector<AttnPr
   a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
   a.hm = L.hm;
   if (L.hm.hq == 0) return;
-  // rows no problem covers (empty attention) carry out=0, lse=-inf (finalize_piece, :151-165)
-  SP_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(L.rows * L.q_stride * 2), ctx.stream));
-  spattn::launch_fill_f32(lse, -INFINITY, L.rows * L.hm.hq, ctx.stream);
+  // rows no problem covers (empty attention) carry out=0, lse=-inf (finalize_piece, :151-165);
+  // the kernels write every covered row (empty ones included), so the fill is only needed when
+  // some row is outside every problem
+  std::vector<std::pair<int64_t, int64_t>> iv;
+  for (const auto& p : probs) iv.emplace_back(p.q_row0, static_cast<int64_t>(p.q_row0) + p.nq);
+  std::sort(iv.begin(), iv.end());
+  int64_t reach = 0;
+  for (const auto& r : iv)
+    if (r.first <= reach) reach = std::max(reach, r.second);
+  if (reach < L.rows) {
+    SP_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(L.rows * L.q_stride * 2), ctx.stream));
+    spattn::launch_fill_f32(lse, -INFINITY, L.rows * L.hm.hq, ctx.stream);
+  }
   attention_forward(ctx.stream, a, probs, false);
 }
 
