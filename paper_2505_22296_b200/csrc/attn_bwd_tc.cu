@@ -69,6 +69,17 @@ enum {
 };
 constexpr int SMEM = BAR_OFF + E_N * 8 + 16;
 
+// 32 consecutive fp32 columns of one row -> 32 bf16 (4 x 16-byte stores)
+__device__ __forceinline__ void store_bf16x32(void* dst, const uint32_t (&r)[32]) {
+  uint4* o = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    o[i] = make_uint4(pack_bf16(__uint_as_float(r[8 * i]), __uint_as_float(r[8 * i + 1])),
+                      pack_bf16(__uint_as_float(r[8 * i + 2]), __uint_as_float(r[8 * i + 3])),
+                      pack_bf16(__uint_as_float(r[8 * i + 4]), __uint_as_float(r[8 * i + 5])),
+                      pack_bf16(__uint_as_float(r[8 * i + 6]), __uint_as_float(r[8 * i + 7])));
+}
+
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
@@ -397,24 +408,36 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc::mbar_arrive(bar(E_PR + b));
       if (warp == 0 && t == 0) TR(10, it);
     }
+    constexpr int NC = D / 32 / (NSMW / 4);  // 32-column chunks of dV per warp
+    const int cc0 = NSMW == 8 ? (warp >> 2) * NC : 0;
+    __nv_bfloat16* dvb = a.dv_bf16 ? reinterpret_cast<__nv_bfloat16*>(a.dv_bf16) +
+                                         (int64_t)(P.k_row0 + c) * a.dkv_bf16_row_stride + kvh * D
+                                   : nullptr;
     if (T > 0) {  // dV epilogue
       tc::mbar_wait(bar(E_FIN), 0);
       tc::fence_after();
       float* dv = a.dv_acc + (int64_t)(P.k_row0 + c) * a.dkv_row_stride + kvh * D;
-      constexpr int NC = D / 32 / (NSMW / 4);  // 32-column chunks of dV per warp
 #pragma unroll
       for (int ci = 0; ci < NC; ++ci) {
-        const int cc = (NSMW == 8 ? (warp >> 2) * NC : 0) + ci;
+        const int cc = cc0 + ci;
         uint32_t r[32];
         tc::tmem_ld32(tDV + lane_base + cc * 32, r);
         tc::tmem_wait_ld();
         if (c < P.nk) {
+          if (dvb) {
+            store_bf16x32(dvb + cc * 32, r);
+          } else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            red_add_v4(dv + cc * 32 + 4 * i, __uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                       __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+            for (int i = 0; i < 8; ++i)
+              red_add_v4(dv + cc * 32 + 4 * i, __uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                         __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+          }
         }
       }
+    } else if (dvb && c < P.nk) {  // no query sees this key tile: dV = 0
+      uint32_t z[32] = {};
+#pragma unroll
+      for (int ci = 0; ci < NC; ++ci) store_bf16x32(dvb + (cc0 + ci) * 32, z);
     }
   } else if (warp >= DRAIN0 && warp < DRAIN0 + 4) {
     // ------------------------------------------- dQ warpgroup (lane = head-dim index)
@@ -456,23 +479,34 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (w == 0 && lane == 0) TR(13, it);
     }
     if (lane == 0) tc::bulk_wait_read<0>();
+    const int ck = n0 + w * 32 + lane;
+    __nv_bfloat16* dkb = a.dk_bf16 ? reinterpret_cast<__nv_bfloat16*>(a.dk_bf16) +
+                                         (int64_t)(P.k_row0 + ck) * a.dkv_bf16_row_stride + kvh * D
+                                   : nullptr;
     if (T > 0) {  // dK epilogue (lane = key row)
       tc::mbar_wait(bar(E_FIN), 0);
       tc::fence_after();
-      const int c = n0 + w * 32 + lane;
-      float* dk = a.dk_acc + (int64_t)(P.k_row0 + c) * a.dkv_row_stride + kvh * D;
+      float* dk = a.dk_acc + (int64_t)(P.k_row0 + ck) * a.dkv_row_stride + kvh * D;
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t r[32];
         tc::tmem_ld32(tDK + lane_base + cc * 32, r);
         tc::tmem_wait_ld();
-        if (c < P.nk) {
+        if (ck < P.nk) {
+          if (dkb) {
+            store_bf16x32(dkb + cc * 32, r);
+          } else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            red_add_v4(dk + cc * 32 + 4 * i, __uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                       __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+            for (int i = 0; i < 8; ++i)
+              red_add_v4(dk + cc * 32 + 4 * i, __uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                         __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+          }
         }
       }
+    } else if (dkb && ck < P.nk) {  // no query sees this key tile: dK = 0
+      uint32_t z[32] = {};
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) store_bf16x32(dkb + cc * 32, z);
     }
   }
   tc::fence_before();

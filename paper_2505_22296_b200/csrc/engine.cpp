@@ -274,10 +274,16 @@ void launch_attn_fwd(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
 bool tc_bwd_q64_supported(const BwdArgs& a);
 void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
 
-void launch_attn_bwd(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
+// The backward launch picks the q64 tcgen05 kernel for these arguments (the only one that can
+// write dK / dV directly as bf16).
+bool bwd_uses_q64(const BwdArgs& a) {
   static const bool use_q64 = !getenv("SPATTN_BWD_Q128");
+  return seqpar::kernel_family() != seqpar::KernelFamily::mma && use_q64 && tc_bwd_q64_supported(a);
+}
+
+void launch_attn_bwd(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
   const bool tc = seqpar::kernel_family() != seqpar::KernelFamily::mma;
-  if (tc && use_q64 && tc_bwd_q64_supported(a))
+  if (bwd_uses_q64(a))
     launch_attn_bwd_tc_q64(a, ps, s);
   else if (tc && tc_bwd_supported(a))
     launch_attn_bwd_tc(a, ps, s);
@@ -732,10 +738,43 @@ void plain_forward(RankCtx& ctx, const Local& L, int d, const std::vector<AttnPr
   attention_forward(ctx.stream, a, probs, false);
 }
 
-void plain_backward(RankCtx& ctx, const Local& L, int d, const std::vector<AttnProblem>& probs,
+// True when every key row of the launch belongs to exactly one problem (disjoint key ranges that
+// cover all rows): each (key row, kv head) is then owned by a single backward CTA.
+bool keys_exclusive(const std::vector<AttnProblem>& probs, int64_t rows) {
+  std::vector<std::pair<int64_t, int64_t>> iv;
+  for (const auto& p : probs) iv.emplace_back(p.k_row0, static_cast<int64_t>(p.k_row0) + p.nk);
+  std::sort(iv.begin(), iv.end());
+  int64_t reach = 0;
+  for (const auto& r : iv) {
+    if (r.first != reach) return false;  // overlap or gap
+    reach = r.second;
+  }
+  return reach == rows;
+}
+
+// dK / dV can go straight to bf16 buffers: the q64 tcgen05 kernel runs for these local tensors
+// and every key row is owned by one problem.
+bool direct_dkv_ok(const Local& L, int d, const std::vector<AttnProblem>& probs, const void* dk_bf16,
+                   const void* dv_bf16) {
+  if (!dk_bf16 || !dv_bf16 || L.hm.hq == 0) return false;
+  spattn::BwdArgs probe{};
+  probe.d = d;
+  probe.q = L.q, probe.k = L.k, probe.v = L.v;
+  probe.dout = L.q, probe.dq_acc = reinterpret_cast<float*>(const_cast<void*>(L.q));  // alignment probe only
+  probe.q_row_stride = L.q_stride, probe.kv_row_stride = L.kv_stride, probe.o_row_stride = L.q_stride;
+  probe.dq_row_stride = L.q_stride, probe.dkv_row_stride = L.kv_stride;
+  return spattn::bwd_uses_q64(probe) && keys_exclusive(probs, L.rows) &&
+         reinterpret_cast<uintptr_t>(dk_bf16) % 16 == 0 && reinterpret_cast<uintptr_t>(dv_bf16) % 16 == 0 &&
+         (L.kv_stride * 2) % 16 == 0;
+}
+
+// Single-block backward (attention.cpp:236-258 closure). dk_bf16 / dv_bf16 (optional): when the
+// q64 tcgen05 kernel runs and the key rows are exclusive, dK / dV are written there as bf16
+// (dk / dv untouched) and true is returned; otherwise dk / dv (fp32, zeroed) receive them.
+bool plain_backward(RankCtx& ctx, const Local& L, int d, const std::vector<AttnProblem>& probs,
                     const void* out, const float* lse, const void* dout, float* dq, float* dk,
-                    float* dv) {
-  if (L.hm.hq == 0) return;
+                    float* dv, void* dk_bf16 = nullptr, void* dv_bf16 = nullptr) {
+  if (L.hm.hq == 0) return false;
   spattn::BwdArgs a{};
   a.q = L.q;
   a.k = L.k;
@@ -757,9 +796,16 @@ void plain_backward(RankCtx& ctx, const Local& L, int d, const std::vector<AttnP
   a.d = d;
   a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
   a.hm = L.hm;
+  const bool direct = direct_dkv_ok(L, d, probs, dk_bf16, dv_bf16) && spattn::bwd_uses_q64(a);
+  if (direct) {
+    a.dk_bf16 = dk_bf16;
+    a.dv_bf16 = dv_bf16;
+    a.dkv_bf16_row_stride = L.kv_stride;
+  }
   spattn::launch_attn_bwd_pre(a, static_cast<int>(L.rows), ctx.stream);
   check_launch();
   attention_backward(ctx.stream, a, probs);
+  return direct;
 }
 
 // ------------------------------------------------------------------------ ring attention
@@ -1252,16 +1298,23 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& S, const DeviceTens
     DevBuf dqa(static_cast<size_t>(rows * H * d * 4), s);
     dqa.zero();
     if (S.engine == Engine::oracle) {
-      DevBuf dka(static_cast<size_t>(rows * Hkv * d * 4), s), dva(static_cast<size_t>(rows * Hkv * d * 4), s);
-      dka.zero();
-      dva.zero();
       int64_t pairs = 0;
       for (const auto& p : S.plain_probs) pairs += admitted_pairs(p);
       ctx.add_flops(10 * d * pairs * H);
-      plain_backward(ctx, Lc, d, S.plain_probs, S.ro, S.lse, dout.data, dqa.as<float>(),
-                     dka.as<float>(), dva.as<float>());
-      spattn::launch_f32_to_bf16(dk.data, dka.as<float>(), 1.f, rows * Hkv * d, s);
-      spattn::launch_f32_to_bf16(dv.data, dva.as<float>(), 1.f, rows * Hkv * d, s);
+      // exclusive key rows: dK / dV straight to bf16 (no fp32 accumulators, fill or rounding)
+      if (direct_dkv_ok(Lc, d, S.plain_probs, dk.data, dv.data)) {
+        const bool direct = plain_backward(ctx, Lc, d, S.plain_probs, S.ro, S.lse, dout.data, dqa.as<float>(),
+                                           nullptr, nullptr, dk.data, dv.data);
+        if (!direct) throw StateError("backward: direct dK/dV path unexpectedly unavailable");
+      } else {
+        DevBuf dka(static_cast<size_t>(rows * Hkv * d * 4), s), dva(static_cast<size_t>(rows * Hkv * d * 4), s);
+        dka.zero();
+        dva.zero();
+        plain_backward(ctx, Lc, d, S.plain_probs, S.ro, S.lse, dout.data, dqa.as<float>(), dka.as<float>(),
+                       dva.as<float>());
+        spattn::launch_f32_to_bf16(dk.data, dka.as<float>(), 1.f, rows * Hkv * d, s);
+        spattn::launch_f32_to_bf16(dv.data, dva.as<float>(), 1.f, rows * Hkv * d, s);
+      }
     } else {
       ring_backward(ctx, S.ring_group, S.ring_runs, Lc, d, cfg.causal, bs, lloc, D, S.ro, S.lse,
                     dout.data, dqa.as<float>(), dk.data, dv.data, nullptr, nullptr);
@@ -1347,9 +1400,23 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& S, const DeviceTens
   MoveSpec mq = head_move(hp, false, bs, lloc, H, d, S.inner_runs, 2);
   DevBuf dog(static_cast<size_t>(bs * lg * nq * d * 2), s);
   move_forward(ctx, inner, mq, dout.data, dog.p, s);
-  DevBuf dqa(static_cast<size_t>(bs * lg * nq * d * 4), s), dka(static_cast<size_t>(bs * lg * nkv * d * 4), s),
-      dva(static_cast<size_t>(bs * lg * nkv * d * 4), s);
-  dqa.zero(), dka.zero(), dva.zero();
+  MoveSpec mkv = head_move(hp, true, bs, lloc, Hkv, d, S.inner_runs, 2);
+  const bool kv_overlap = windows_overlap(mkv.win);
+  // the gathered dK / dV go straight to bf16 when no other member shares their kv heads and the
+  // kernel owns every key row (no fp32 accumulators, fill or rounding pass)
+  DevBuf dkg, dvg;
+  if (!kv_overlap) {
+    dkg = DevBuf(static_cast<size_t>(bs * lg * nkv * d * 2), s);
+    dvg = DevBuf(static_cast<size_t>(bs * lg * nkv * d * 2), s);
+  }
+  const bool direct = !S.ring && !kv_overlap && direct_dkv_ok(Lc, d, S.plain_probs, dkg.p, dvg.p);
+  DevBuf dqa(static_cast<size_t>(bs * lg * nq * d * 4), s), dka, dva;
+  dqa.zero();
+  if (!direct) {
+    dka = DevBuf(static_cast<size_t>(bs * lg * nkv * d * 4), s);
+    dva = DevBuf(static_cast<size_t>(bs * lg * nkv * d * 4), s);
+    dka.zero(), dva.zero();
+  }
   if (S.ring) {
     ring_backward(ctx, S.ring_group, S.ring_runs, Lc, d, cfg.causal, bs, lg, D, S.ro, S.lse, dog.p,
                   dqa.as<float>(), nullptr, nullptr, dka.as<float>(), dva.as<float>());
@@ -1357,8 +1424,10 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& S, const DeviceTens
     int64_t pairs = 0;
     for (const auto& p : S.plain_probs) pairs += admitted_pairs(p);
     ctx.add_flops(10 * d * pairs * nq);
-    plain_backward(ctx, Lc, d, S.plain_probs, S.ro, S.lse, dog.p, dqa.as<float>(), dka.as<float>(),
-                   dva.as<float>());
+    const bool used = plain_backward(ctx, Lc, d, S.plain_probs, S.ro, S.lse, dog.p, dqa.as<float>(),
+                                     dka.as<float>(), dva.as<float>(), direct ? dkg.p : nullptr,
+                                     direct ? dvg.p : nullptr);
+    if (used != direct) throw StateError("backward: direct dK/dV decision changed between planning and launch");
   }
   DevBuf dqg(static_cast<size_t>(bs * lg * nq * d * 2), s);
   spattn::launch_f32_to_bf16(dqg.p, dqa.as<float>(), 1.f, bs * lg * nq * d, s);
@@ -1366,12 +1435,12 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& S, const DeviceTens
   const RopeMove rinv{S.rope_table, d, -1};
   const RopeMove* rbwd = S.rope_table ? &rinv : nullptr;
   move_reverse(ctx, inner, mq, dqg.p, dq.data, false, s, rbwd);
-  MoveSpec mkv = head_move(hp, true, bs, lloc, Hkv, d, S.inner_runs, 2);
   const int64_t rows = bs * lloc;
-  if (!windows_overlap(mkv.win)) {
-    DevBuf dkg(static_cast<size_t>(bs * lg * nkv * d * 2), s), dvg(static_cast<size_t>(bs * lg * nkv * d * 2), s);
-    spattn::launch_f32_to_bf16(dkg.p, dka.as<float>(), 1.f, bs * lg * nkv * d, s);
-    spattn::launch_f32_to_bf16(dvg.p, dva.as<float>(), 1.f, bs * lg * nkv * d, s);
+  if (!kv_overlap) {
+    if (!direct) {
+      spattn::launch_f32_to_bf16(dkg.p, dka.as<float>(), 1.f, bs * lg * nkv * d, s);
+      spattn::launch_f32_to_bf16(dvg.p, dva.as<float>(), 1.f, bs * lg * nkv * d, s);
+    }
     move_reverse(ctx, inner, mkv, dkg.p, dk.data, false, s, rbwd);
     move_reverse(ctx, inner, mkv, dvg.p, dv.data, false, s);
   } else {

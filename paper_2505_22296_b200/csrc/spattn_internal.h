@@ -67,6 +67,12 @@ struct BwdArgs {
   int d;
   float scale;
   HeadMap hm;
+  // optional: when every (key row, kv head) belongs to exactly one CTA of the launch (disjoint
+  // key ranges), the tcgen05 kernel writes dK / dV as bf16 here instead of adding into dk_acc /
+  // dv_acc (no zero fill, no atomics, no rounding pass); row stride in elements
+  void* dk_bf16 = nullptr;
+  void* dv_bf16 = nullptr;
+  int64_t dkv_bf16_row_stride = 0;
   int debug;  // profiling switches (SPATTN_DEBUG env): 1 skip dQ atomics, 2 skip dK/dV atomics
   long long* trace;  // profiling: per-iteration clock64 events of CTA (0,0), or null
 };
