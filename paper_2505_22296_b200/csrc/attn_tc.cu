@@ -205,7 +205,12 @@ struct FwdLayout {
 
 // K stage s is released by the S(j) completion barrier (B_SF), V stage s by the PV(j) one (B_PV),
 // so the next K load overlaps the current softmax instead of waiting for PV.
-enum FwdBar { B_Q = 0, B_KF = 1, B_VF = 3, B_SF = 5, B_SFREE = 7, B_PF = 9, B_PV = 11, B_N = 13 };
+// B_PH: the first half (keys 0-63) of P buffer st has been read by PV — the softmax of the
+// stream's next tile may overwrite it while PV still reads the second half.
+enum FwdBar { B_Q = 0, B_KF = 1, B_VF = 3, B_SF = 5, B_SFREE = 7, B_PF = 9, B_PV = 11, B_PH = 13, B_N = 15 };
+#ifndef SPATTN_FWD_PHALF
+#define SPATTN_FWD_PHALF 0
+#endif
 
 #ifndef SPATTN_FWD_P_TMEM
 #define SPATTN_FWD_P_TMEM 0
@@ -345,6 +350,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             const uint32_t aoff = (kk >> 2) * 16384 + (kk & 3) * 32;
             tc::mma_ss(tO + st * D, tc::sdesc(pbase + aoff, 16, 1024),
                        tc::sdesc(vbase + kk * 2048, 16384, 1024), id_o, (i > 1 || kk > 0) ? 1u : 0u);
+            if (SPATTN_FWD_PHALF && kk == 3) tc::commit(bar(B_PH + st));
           }
         }
         tc::commit(bar(B_PV + st));  // also releases V stage st
@@ -475,7 +481,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const float2 av = f2_unpack(f2_fma(f2_pack(x[2 * e], x[2 * e + 1]), sc2, nm2));
         // pairs in kFwdPolyPairs run on the FMA pipe instead of the MUFU (16/clk/SM)
         float2 pv;
+#ifdef SPATTN_FWD_PROBE_NOEXP
+        pv = av;  // profiling probe: no exponentials (wrong results)
+        if (false) {
+#else
         if ((kFwdPolyPairs >> (e & 3)) & 1) {
+#endif
           pv = poly_exp2x2(av.x, av.y);
         } else {
           pv.x = fast_exp2(av.x);
@@ -484,17 +495,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         rs2[e & 1] = f2_add(rs2[e & 1], f2_pack(pv.x, pv.y));
         pw[e] = pack_bf16(pv.x, pv.y);
       }
+#ifdef SPATTN_FWD_PROBE_NOSTORE
+      if (true) {  // profiling probe: P never written (wrong results)
+      } else
+#endif
       if (SPATTN_FWD_P_TMEM) {
         // P(j) over the first 64 columns of this group's S buffer (its S values are in x[] now)
         tc::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pw[0]));
         tc::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pw[32]));
         tc::tmem_wait_st();
       } else {
-        // P buffer g was last read by PV(j-2); the wait is usually already satisfied here
-        if (it > 0) tc::mbar_wait(bar(B_PV + g), (it - 1) & 1);
+        // P buffer g was last read by PV(j-2): each 64-key half is stored once PV(j-2) has read it
         const uint32_t pbase = sP + g * Lay::P_TILE;
 #pragma unroll
         for (int ch = 0; ch < 16; ++ch) {
+          if (it > 0 && ch == 0) tc::mbar_wait(bar(SPATTN_FWD_PHALF ? B_PH + g : B_PV + g), (it - 1) & 1);
+          if (SPATTN_FWD_PHALF && it > 0 && ch == 8) tc::mbar_wait(bar(B_PV + g), (it - 1) & 1);
           const uint32_t addr = tc::sw128(pbase + (ch >> 3) * 16384, row, ch & 7);
           asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(pw[4 * ch]),
                        "r"(pw[4 * ch + 1]), "r"(pw[4 * ch + 2]), "r"(pw[4 * ch + 3]));
