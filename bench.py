@@ -141,8 +141,8 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     vals, samples = [], []
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        pass
+    if args.warmup > 0:  # one untimed sample warms the page cache and the CPU frequency
+        cpu_reference_sample(heads, kv, d, L)
     for _ in range(args.steps):
         r = cpu_reference_sample(heads, kv, d, L)
         vals.append(r["value"])

@@ -239,9 +239,12 @@ def test_host_step_ulysses_loopback_rejects_bad_groups(P):
 
 @pytest.mark.parametrize("engine,sp,H,Hkv", [("ulysses", 2, 8, 4), ("dummy_head", 4, 6, 2),
                                              ("ring", 2, 4, 2)])
-def test_host_step_sharded_on_loopback_ranks(P, engine, sp, H, Hkv):
+@pytest.mark.parametrize("messages", [False, True])
+def test_host_step_sharded_on_loopback_ranks(P, engine, sp, H, Hkv, messages):
     """spattn_step_host on every rank of a loopback group (one thread per rank): the kv-head
-    group split must respect each engine's head constraints and still match the oracle."""
+    group split must respect each engine's head constraints and still match the oracle. With
+    ``messages`` every exchange goes through send/recv messages paired in NCCL's order (the path
+    an NCCL rank takes: no peer pointers)."""
     import threading
     import types
 
@@ -249,7 +252,7 @@ def test_host_step_sharded_on_loopback_ranks(P, engine, sp, H, Hkv):
     L, d = 256, 64
     q, k, v, R = parity_inputs(700 + sp + H, L, H, Hkv, d)
     mode = "zigzag" if engine == "ring" else "naive"
-    fab = P.Fabric(sp)
+    fab = P.Fabric(sp, force_messages=messages)
     shard = lambda x, i: P.shard_rows(to_dev(x), mode, sp, i).cpu()  # noqa: E731
     res, errs = [None] * sp, []
 
