@@ -151,6 +151,9 @@ int64_t spattn_launch_count(void);
 /* Profiling: per-iteration clock64 event trace of backward CTA (0,0) into a device buffer of
  * 16 int64 per iteration (NULL disables). */
 int spattn_debug_bwd_trace(void* device_buffer);
+/* Profiling: per-CTA globaltimer records of the forward kernel, 8 int64 per CTA (blockIdx.y-major):
+ * entry, first S in TMEM, main-loop end, exit (ns), n_tiles, smid (NULL disables). */
+int spattn_debug_fwd_cta_trace(void* device_buffer);
 int spattn_profile_enable(int on);
 int spattn_profile_read(double ms[2], int64_t n[2]);
 

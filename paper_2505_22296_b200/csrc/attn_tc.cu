@@ -169,6 +169,14 @@ int umma_selftest(cudaStream_t s, const void* A, const void* B, const void* Bmn,
 
 __device__ long long* g_fwd_trace = nullptr;  // profiling: per-tile clock64 events of CTA (0,0)
 void set_fwd_trace(void* p) { cudaMemcpyToSymbol(g_fwd_trace, &p, sizeof(p)); }
+// profiling: per-CTA globaltimer records [entry, first S in TMEM, loop end, exit, n_tiles, smid]
+__device__ long long* g_fwd_cta = nullptr;
+void set_fwd_cta_trace(void* p) { cudaMemcpyToSymbol(g_fwd_cta, &p, sizeof(p)); }
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // =================================================================================
 // Forward: one CTA = 128 query rows x one head of one problem. Warp roles:
@@ -260,6 +268,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   n_end = max(n_end, 0);
   const int n_tiles = (n_end + 127) / 128;
   long long* trace = (g_fwd_trace && blockIdx.x == 0 && blockIdx.y == 0) ? g_fwd_trace : nullptr;
+  long long* ctr = g_fwd_cta ? g_fwd_cta + 8 * ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (ctr && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    ctr[0] = gtimer();
+    ctr[4] = n_tiles;
+    ctr[5] = smid;
+  }
 #define FTR(slot, j) \
   if (trace) trace[(j) * 16 + (slot)] = clock64()
 
@@ -408,6 +424,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (row == 0) FTR(5, j);
       tc::mbar_wait(bar(B_SF + g), it & 1);
       if (row == 0) FTR(6, j);
+      if (ctr && j == 0 && threadIdx.x == 0) ctr[1] = gtimer();
       tc::fence_after();
       float x[128];
       {
@@ -526,6 +543,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tc::mbar_arrive(bar(B_PF + g));
       if (row == 0) FTR(7, j);
     }
+    if (ctr && threadIdx.x == 0) ctr[2] = gtimer();
     // ---- epilogue: merge the two streams; group g writes output columns [g*D/2, (g+1)*D/2)
     const bool valid = qa < P.nq;
     const int64_t grow = (int64_t)(P.q_row0 + qa);
@@ -610,6 +628,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc::fence_before();
   __syncthreads();
   if (warp == 9) tc::tmem_dealloc<512>(tmem);
+  if (ctr && threadIdx.x == 0) ctr[3] = gtimer();
 }
 
 int max_rows(const ProblemSet& ps, bool q) {

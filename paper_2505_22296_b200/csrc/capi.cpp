@@ -293,12 +293,22 @@ int spattn_selftest_umma(void* stream, const void* a, const void* b, const void*
 namespace spattn {
 void set_bwd_trace(void* p);
 void set_fwd_trace(void* p);
+void set_fwd_cta_trace(void* p);
+void set_pp_trace(void* p);
+void set_pp_cta_trace(void* p);
 }
 extern "C" {
 int spattn_debug_bwd_trace(void* device_buffer) {
   return guard([&] {
     spattn::set_bwd_trace(device_buffer);
     spattn::set_fwd_trace(device_buffer);
+    spattn::set_pp_trace(device_buffer);
+  });
+}
+int spattn_debug_fwd_cta_trace(void* device_buffer) {
+  return guard([&] {
+    spattn::set_fwd_cta_trace(device_buffer);
+    spattn::set_pp_cta_trace(device_buffer);
   });
 }
 
