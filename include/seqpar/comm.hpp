@@ -69,6 +69,9 @@ class Transport {
   // Grouped point-to-point messages on `stream` (all sends and receives in one group call).
   virtual void send_recv(const CommGroup& g, int my_rank, const std::vector<Msg>& sends,
                          const std::vector<Msg>& recvs, cudaStream_t stream) = 0;
+  // Diagnostics (collective over every rank of the transport): a message of `bytes` to this
+  // rank itself through every entry point the transport uses; throws on a mismatch.
+  virtual void self_test(int my_rank, size_t bytes, cudaStream_t stream);
 };
 
 // comm.hpp:63-82 RankCtx: this rank's transport, SP group, stream and counters.

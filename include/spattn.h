@@ -127,6 +127,10 @@ int spattn_nccl_unique_id(uint8_t out[128]);
 int spattn_ctx_create_nccl(int device, int rank, int world, int sp, const uint8_t unique_id[128],
                            spattn_ctx** out);
 int spattn_ctx_destroy(spattn_ctx* ctx);
+/* Diagnostics, collective over the context's transport: `bytes` sent by this rank to itself
+ * through every transport entry point (NCCL: CommSplit, grouped Send/Recv on the split and the
+ * world communicator, CommDestroy; loopback: send_recv). 0 when the bytes arrive intact. */
+int spattn_debug_transport_selftest(spattn_ctx* ctx, int64_t bytes);
 /* Loopback fabric: `world` ranks as threads sharing one device (CommFabric::run analog).
  * force_messages=1 routes collectives through the pack -> send/recv -> unpack path. */
 int spattn_fabric_create(int device, int world, int sp, int force_messages, spattn_fabric** out);

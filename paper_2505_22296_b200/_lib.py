@@ -29,7 +29,7 @@ EXPORTS = [
     "spattn_block_fwd", "spattn_block_finalize", "spattn_lse_merge", "spattn_block_bwd",
     "spattn_shard_rows", "spattn_gather_rows", "spattn_launch_count", "spattn_profile_enable",
     "spattn_profile_read", "spattn_selftest_umma", "spattn_plan_heads", "spattn_plan_problems",
-    "spattn_debug_bwd_trace", "spattn_debug_fwd_cta_trace", "spattn_fwd_rope", "spattn_fabric_fwd_rope", "spattn_rope_apply",
+    "spattn_debug_bwd_trace", "spattn_debug_fwd_cta_trace", "spattn_debug_transport_selftest", "spattn_fwd_rope", "spattn_fabric_fwd_rope", "spattn_rope_apply",
     "spattn_step_host", "spattn_pick_step_groups", "spattn_pad_batch",
     "spattn_split_position_map", "spattn_documents_from_segments", "spattn_replicate_packing_mask",
     "spattn_fabric_replicate_packing_mask", "spattn_logprob_fwd", "spattn_logprob_bwd",
@@ -154,6 +154,7 @@ def lib() -> ctypes.CDLL:
         "spattn_profile_enable": [_i32],
         "spattn_debug_bwd_trace": [_vp],
         "spattn_debug_fwd_cta_trace": [_vp],
+        "spattn_debug_transport_selftest": [_vp, ctypes.c_int64],
         "spattn_plan_heads": [_i32, _i32, _i32] + [ctypes.POINTER(ctypes.c_int32)] * 4,
         "spattn_plan_problems": [_i64p, _i64, _i64p, _i64, _i32, _i64p, _i32,
                                  ctypes.POINTER(ctypes.c_int32), _i32, ctypes.POINTER(ctypes.c_int),

@@ -190,6 +190,13 @@ int spattn_plan_problems(const int64_t* qpos, int64_t lq, const int64_t* kpos, i
   });
 }
 
+int spattn_debug_transport_selftest(spattn_ctx* ctx, int64_t bytes) {
+  return guard([&] {
+    if (!ctx || !ctx->rc || bytes <= 0) throw seqpar::ConfigError("transport self-test: bad arguments");
+    ctx->rc->transport->self_test(ctx->rc->rank, static_cast<size_t>(bytes), ctx->rc->stream);
+  });
+}
+
 int spattn_nccl_unique_id(uint8_t out[128]) {
   return guard([&] { seqpar::nccl_unique_id(out); });
 }

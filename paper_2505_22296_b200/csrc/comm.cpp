@@ -4,6 +4,8 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <functional>
+
 #include <cstring>
 #include <exception>
 #include <sstream>
@@ -207,6 +209,36 @@ void LoopbackFabric::run(const std::function<void(RankCtx&)>& body) {
     if (e) std::rethrow_exception(e);
 }
 
+namespace {
+// one self message on `c` (or through send_recv on the single-member group when c is null)
+void self_message(Transport& t, int my_rank, size_t bytes, cudaStream_t s,
+                  const std::function<void(void*, void*, size_t)>& send_self) {
+  void *a = nullptr, *b = nullptr;
+  SP_CUDA(cudaMallocAsync(&a, bytes, s));
+  SP_CUDA(cudaMallocAsync(&b, bytes, s));
+  SP_CUDA(cudaMemsetAsync(a, 0x5a, bytes, s));
+  SP_CUDA(cudaMemsetAsync(b, 0, bytes, s));
+  if (send_self) {
+    send_self(a, b, bytes);
+  } else {
+    CommGroup g;
+    g.ranks = {my_rank};
+    t.send_recv(g, my_rank, {{0, a, bytes}}, {{0, b, bytes}}, s);
+  }
+  std::vector<unsigned char> h(bytes);
+  SP_CUDA(cudaMemcpyAsync(h.data(), b, bytes, cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaFreeAsync(a, s));
+  SP_CUDA(cudaFreeAsync(b, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  for (unsigned char c : h)
+    if (c != 0x5a) throw StateError("transport self-test: received bytes differ from the sent ones");
+}
+}  // namespace
+
+void Transport::self_test(int my_rank, size_t bytes, cudaStream_t s) {
+  self_message(*this, my_rank, bytes, s, nullptr);
+}
+
 // ---------------------------------------------------------------------------------- NCCL
 namespace {
 
@@ -271,6 +303,22 @@ class NcclTransport : public Transport {
     throw StateError("NCCL transport has no peer-pointer path");
   }
   void release(const CommGroup&, int, cudaStream_t) override {}
+
+  // ncclCommSplit (collective: every rank calls it) + a grouped ncclSend/ncclRecv to itself on
+  // the split communicator and on the world one, then ncclCommDestroy of the split
+  void self_test(int my_rank, size_t bytes, cudaStream_t s) override {
+    ncclComm_t c = nullptr;
+    nccl_check(nccl().CommSplit(world_comm_, 7, my_rank, &c, nullptr), "CommSplit");
+    for (ncclComm_t comm : {c, world_comm_}) {
+      self_message(*this, my_rank, bytes, s, [&](void* a, void* b, size_t n) {
+        nccl_check(nccl().GroupStart(), "GroupStart");
+        nccl_check(nccl().Send(a, n, ncclUint8, my_rank, comm, s), "Send");
+        nccl_check(nccl().Recv(b, n, ncclUint8, my_rank, comm, s), "Recv");
+        nccl_check(nccl().GroupEnd(), "GroupEnd");
+      });
+    }
+    nccl_check(nccl().CommDestroy(c), "CommDestroy");
+  }
 
   void send_recv(const CommGroup& g, int, const std::vector<Msg>& sends,
                  const std::vector<Msg>& recvs, cudaStream_t s) override {

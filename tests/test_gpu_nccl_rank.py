@@ -44,3 +44,23 @@ def test_rank_context_module_matches_oracle(nccl_group, engine):
         assert_close(key, res[key], orc[key], ref[key])
     stats = rc.stats()
     assert all(b == 0 for _, b in stats.values())  # sp=1: nothing crosses NVLink
+
+
+def test_nccl_transport_entry_points(nccl_group):
+    """Every NCCL entry point the transport binds through dlopen (CommSplit, grouped Send/Recv on
+    the split and the world communicator, CommDestroy) on the real library: a self message."""
+    import paper_2505_22296_b200 as P
+    from paper_2505_22296_b200 import _lib as C
+
+    rc = P.RankContext()
+    for nbytes in (1, 4096, 3 << 20):
+        C.check(C.lib().spattn_debug_transport_selftest(rc._h, nbytes))
+
+
+@pytest.mark.parametrize("messages", [False, True])
+def test_loopback_transport_self_message(messages):
+    import paper_2505_22296_b200 as P
+    from paper_2505_22296_b200 import _lib as C
+
+    fab = P.Fabric(1, force_messages=messages)
+    C.check(C.lib().spattn_debug_transport_selftest(fab.ctxs[0], 1 << 16))
