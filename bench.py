@@ -33,6 +33,7 @@ CONFIGS = {
     "c3": (28, 4, 128, 65536, "dummy_head"),
     "c4": (32, 8, 128, 131072, "ring"),
 }
+MODEL_OF = {"c1": "reference parity-grid", "c2": "Llama-3-8B", "c3": "Qwen2.5-7B", "c4": "Llama-3-8B"}
 
 
 def peaks():
@@ -371,7 +372,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (torch.randn bf16, seeded)",
-        "config": {"workload": f"{args.config}: Llama-3-8B attention {heads}q/{kv}kv heads "
+        "config": {"workload": f"{args.config}: {MODEL_OF[args.config]} attention {heads}q/{kv}kv heads "
                                f"d={d} seq {L} causal bs 1", "engine": engine,
                    "parallelism": f"sp{world}", "global_batch": 1, "seq_len": L,
                    "kernel_family": args.family,
