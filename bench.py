@@ -364,6 +364,8 @@ def main():
     total_flops = 14 * d * causal_pairs(L) * heads
     layer_tflops = total_flops / (ms / 1e3) / 1e12
     if rank != 0:
+        torch.cuda.synchronize()
+        keep._fin()  # every rank releases its communicators while CUDA is still up
         if dist:
             dist.destroy_process_group()
         return
