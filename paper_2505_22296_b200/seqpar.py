@@ -567,9 +567,10 @@ def attention_step_host(engine: str, q: torch.Tensor, k: torch.Tensor, v: torch.
     C.check(C.lib().spattn_ctx_set_stream(h, _stream()))
     pin = lambda t: t.contiguous() if t.is_pinned() else t.contiguous().pin_memory()  # noqa: E731
     q, k, v, dout = (pin(t) for t in (q, k, v, dout))
-    dq, dk, dv = (torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (q, k, v))
-    out = torch.empty(q.shape, dtype=q.dtype).pin_memory() if want_out else None
-    lse = torch.empty(q.shape[:3], dtype=torch.float32).pin_memory() if want_out else None
+    # results land in pinned buffers (torch's caching host allocator reuses them across steps)
+    dq, dk, dv = (torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in (q, k, v))
+    out = torch.empty(q.shape, dtype=q.dtype, pin_memory=True) if want_out else None
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, pin_memory=True) if want_out else None
     nd = 0 if docs is None else len(docs)
     darr = None if docs is None else (ctypes.c_int64 * nd)(*docs)
     C.check(C.lib().spattn_step_host(
