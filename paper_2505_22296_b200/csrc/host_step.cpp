@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -120,11 +123,15 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
     if (cs2) HS_CUDA(cudaStreamWaitEvent(cs2, ready, 0));
     cudaEventDestroy(ready);
 
+    // profiling (wrong results): SPATTN_STEP_NOCOPY=1 skips H2D and D2H, 2 only D2H, 3 only H2D
+    static const int nocopy = getenv("SPATTN_STEP_NOCOPY") ? atoi(getenv("SPATTN_STEP_NOCOPY")) : 0;
     auto h2d = [&](void* dst, const void* src, size_t col_bytes, size_t width, size_t pitch) {
+      if (nocopy == 1 || nocopy == 3) return;
       HS_CUDA(cudaMemcpy2DAsync(dst, width, static_cast<const char*>(src) + col_bytes, pitch, width,
                                 static_cast<size_t>(rows), cudaMemcpyHostToDevice, up));
     };
     auto d2h = [&](void* dst, const void* src, size_t col_bytes, size_t width, size_t pitch) {
+      if (nocopy == 1 || nocopy == 2) return;
       HS_CUDA(cudaMemcpy2DAsync(static_cast<char*>(dst) + col_bytes, pitch, src, width, width,
                                 static_cast<size_t>(rows), cudaMemcpyDeviceToHost, down));
     };
@@ -138,13 +145,33 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
       h2d(s.dout, hdout, g * qw, qw, qpitch);
       HS_CUDA(cudaEventRecord(s.dout_loaded, up));
     };
-    load(0);
+    // profiling: SPATTN_STEP_TRACE=1 prints a per-group timeline (ms from the step start) to stderr
+    static const bool trace = getenv("SPATTN_STEP_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t st) -> int {
+      if (!trace) return -1;
+      cudaEvent_t e;
+      HS_CUDA(cudaEventCreate(&e));
+      HS_CUDA(cudaEventRecord(e, st));
+      tev.push_back(e);
+      return static_cast<int>(tev.size()) - 1;
+    };
+    std::vector<std::array<int, 6>> tl(static_cast<size_t>(ng), {-1, -1, -1, -1, -1, -1});
+    const int t0 = mark(cs);
+    if (trace) HS_CUDA(cudaStreamWaitEvent(up, tev[static_cast<size_t>(t0)], 0));
+    auto load_t = [&](int g) {
+      tl[static_cast<size_t>(g)][0] = mark(up);
+      load(g);
+      tl[static_cast<size_t>(g)][1] = mark(up);
+    };
+    load_t(0);
     for (int g = 0; g < ng; ++g) {
-      if (g + 1 < ng) load(g + 1);
+      if (g + 1 < ng) load_t(g + 1);
       Slot& s = slots[static_cast<size_t>(g % nslots)];
       cudaStream_t gs = (dual && (g & 1)) ? cs2 : cs;
       ctx.stream = gs;
       HS_CUDA(cudaStreamWaitEvent(gs, s.loaded, 0));
+      tl[static_cast<size_t>(g)][2] = mark(gs);
       const DeviceTensor tq{s.q, bs, lloc, hg, d}, tk{s.k, bs, lloc, kg, d}, tv{s.v, bs, lloc, kg, d};
       const DeviceTensor to{s.out, bs, lloc, hg, d};
       SavedPtr saved = run_attention_engine(ctx, engine, gc, layout, tq, tk, tv, to, s.lse, docs);
@@ -154,8 +181,10 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
                                     DeviceTensor{s.dv, bs, lloc, kg, d});
       saved.reset();
       ctx.stream = cs;
+      tl[static_cast<size_t>(g)][3] = mark(gs);
       HS_CUDA(cudaEventRecord(s.computed, gs));
       HS_CUDA(cudaStreamWaitEvent(down, s.computed, 0));
+      tl[static_cast<size_t>(g)][4] = mark(down);
       d2h(hdq, s.dq, g * qw, qw, qpitch);
       d2h(hdk, s.dk, g * kw, kw, kpitch);
       d2h(hdv, s.dv, g * kw, kw, kpitch);
@@ -166,6 +195,21 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
                                   static_cast<size_t>(hg) * 4, static_cast<size_t>(rows),
                                   cudaMemcpyDeviceToHost, down));
       HS_CUDA(cudaEventRecord(s.drained, down));
+      tl[static_cast<size_t>(g)][5] = mark(down);
+    }
+    if (trace) {
+      HS_CUDA(cudaDeviceSynchronize());
+      auto at = [&](int i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tev[static_cast<size_t>(t0)], tev[static_cast<size_t>(i)]);
+        return ms;
+      };
+      for (int g = 0; g < ng; ++g) {
+        const auto& r = tl[static_cast<size_t>(g)];
+        fprintf(stderr, "step group %d: H2D %.2f-%.2f  compute %.2f-%.2f  D2H %.2f-%.2f ms\n", g, at(r[0]),
+                at(r[1]), at(r[2]), at(r[3]), at(r[4]), at(r[5]));
+      }
+      for (cudaEvent_t e : tev) cudaEventDestroy(e);
     }
     // the step completes on the compute stream (callers time / synchronise it)
     for (int g = std::max(0, ng - nslots); g < ng; ++g)
