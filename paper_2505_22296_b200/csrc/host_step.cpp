@@ -84,7 +84,7 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
   // overlaps the next group's forward; with collectives (sp > 1) one stream keeps every rank's
   // NCCL calls in the same order.
   cudaStream_t cs = ctx.stream, cs2 = nullptr, up = nullptr, down = nullptr;
-  const bool dual = sp == 1 && ng > 1;
+  const bool dual = sp == 1 && ng > 1 && !getenv("SPATTN_STEP_SINGLE");  // (profiling switch)
   HS_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
   HS_CUDA(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
   if (dual) HS_CUDA(cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking));

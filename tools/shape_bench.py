@@ -17,12 +17,15 @@ g = torch.Generator(device="cuda").manual_seed(0)
 q = torch.randn(1, L, H, d, device="cuda", generator=g).bfloat16().requires_grad_(True)
 k = torch.randn(1, L, Hkv, d, device="cuda", generator=g).bfloat16().requires_grad_(True)
 v = torch.randn(1, L, Hkv, d, device="cuda", generator=g).bfloat16().requires_grad_(True)
+# random upstream gradient (a constant one toggles fewer bits and runs at higher clocks under
+# the power cap)
+dout = torch.randn(1, L, H, d, device="cuda", generator=g).bfloat16()
 for i in range(reps + 2):
     if i == 2:
         torch.cuda.synchronize()
         C.check(C.lib().spattn_profile_enable(1))
     out = P.oracle_attention(q, k, v)
-    out.backward(torch.ones_like(out))
+    out.backward(dout)
 torch.cuda.synchronize()
 C.check(C.lib().spattn_profile_enable(0))
 ms, n = (ctypes.c_double * 2)(), (ctypes.c_int64 * 2)()
