@@ -436,11 +436,18 @@ void move_forward(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
     if (G > 1) ctx.transport->release(g, ctx.rank, s);
     return;
   }
-  // message path: pack per destination -> grouped send/recv -> unpack per source
+  // message path: pack per destination -> grouped send/recv -> unpack per source. A source
+  // whose rows land as one contiguous block of y (bs 1, one run of all its rows, this member's
+  // window spanning y's rows, no rotation: the natural Ulysses layout) is received in place.
   const int64_t rows = m.bs * m.lloc;
   std::vector<int64_t> soff(G + 1, 0), roff(G + 1, 0);
+  auto in_place = [&](int i) {
+    const auto& ri = m.runs[static_cast<size_t>(i)];
+    return !rope && m.bs == 1 && ri.size() == 1 && ri[0].row0 == 0 && ri[0].n == m.lloc && w.ycol == 0 &&
+           w.pad == 0 && yw == w.n;
+  };
   for (int j = 0; j < G; ++j) soff[j + 1] = soff[j] + rows * m.win[static_cast<size_t>(j)].n;
-  for (int i = 0; i < G; ++i) roff[i + 1] = roff[i] + rows * w.n;
+  for (int i = 0; i < G; ++i) roff[i + 1] = roff[i] + (in_place(i) ? 0 : rows * w.n);
   DevBuf sbuf(static_cast<size_t>(soff[G] * m.elem), s), rbuf(static_cast<size_t>(roff[G] * m.elem), s);
   std::vector<CopyTask> pack;
   for (int j = 0; j < G; ++j) {
@@ -455,13 +462,18 @@ void move_forward(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
   for (int j = 0; j < G; ++j) {
     sends.push_back({j, static_cast<char*>(sbuf.p) + soff[j] * m.elem,
                      static_cast<size_t>((soff[j + 1] - soff[j]) * m.elem)});
-    recvs.push_back({j, static_cast<char*>(rbuf.p) + roff[j] * m.elem,
-                     static_cast<size_t>((roff[j + 1] - roff[j]) * m.elem)});
+    if (in_place(j))
+      recvs.push_back({j, static_cast<char*>(y) + m.runs[static_cast<size_t>(j)][0].pos0 * yw * m.elem,
+                       static_cast<size_t>(rows * w.n * m.elem)});
+    else
+      recvs.push_back({j, static_cast<char*>(rbuf.p) + roff[j] * m.elem,
+                       static_cast<size_t>((roff[j + 1] - roff[j]) * m.elem)});
   }
   ctx.transport->send_recv(g, ctx.rank, sends, recvs, s);
   std::vector<CopyTask> tasks;
   for (int i = 0; i < G; ++i) {
     if (w.n == 0 && w.pad == 0) continue;
+    if (in_place(i)) continue;
     auto t = unpack(i, static_cast<char*>(rbuf.p) + roff[i] * m.elem, w.n, 0, nullptr);
     tasks.insert(tasks.end(), t.begin(), t.end());
   }
@@ -510,8 +522,15 @@ void move_reverse(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
     if (G > 1) ctx.transport->release(g, ctx.rank, s);
     return;
   }
-  // message path: member me packs, for every destination i, its rows of i in i's local order
+  // message path: member me packs, for every destination i, its rows of i in i's local order;
+  // a destination whose rows are one contiguous block of y (bs 1, one run, this member's
+  // window spanning y's rows: the natural Ulysses layout) is sent in place
   const int64_t rows = m.bs * m.lloc;
+  const int64_t ywm = m.yw[static_cast<size_t>(me)];
+  auto in_place = [&](int i) {
+    const auto& ri = m.runs[static_cast<size_t>(i)];
+    return m.bs == 1 && ri.size() == 1 && ri[0].row0 == 0 && ri[0].n == m.lloc && wm.ycol == 0 && ywm == wm.n;
+  };
   DevBuf sbuf(static_cast<size_t>(G * rows * wm.n * m.elem), s);
   std::vector<int64_t> roff(G + 1, 0);
   for (int j = 0; j < G; ++j) roff[j + 1] = roff[j] + rows * m.win[static_cast<size_t>(j)].n;
@@ -519,6 +538,7 @@ void move_reverse(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
   std::vector<CopyTask> pack;
   if (wm.n > 0)
     for (int i = 0; i < G; ++i) {
+      if (in_place(i)) continue;
       char* dst = static_cast<char*>(sbuf.p) + i * rows * wm.n * m.elem;
       for (int64_t b = 0; b < m.bs; ++b)
         for (const auto& r : m.runs[static_cast<size_t>(i)])
@@ -528,8 +548,10 @@ void move_reverse(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
   run_tasks(pack, m.elem, false, s);
   std::vector<Msg> sends, recvs;
   for (int i = 0; i < G; ++i) {
-    sends.push_back({i, static_cast<char*>(sbuf.p) + i * rows * wm.n * m.elem,
-                     static_cast<size_t>(rows * wm.n * m.elem)});
+    char* src = in_place(i) ? static_cast<char*>(const_cast<void*>(y)) +
+                                  m.runs[static_cast<size_t>(i)][0].pos0 * ywm * m.elem
+                            : static_cast<char*>(sbuf.p) + i * rows * wm.n * m.elem;
+    sends.push_back({i, src, static_cast<size_t>(rows * wm.n * m.elem)});
     recvs.push_back({i, static_cast<char*>(rbuf.p) + roff[i] * m.elem,
                      static_cast<size_t>((roff[i + 1] - roff[i]) * m.elem)});
   }
