@@ -34,9 +34,12 @@ def check(res, q, k, v, R, causal=True):
 
 @pytest.mark.parametrize("engine,sp,kw", [("ulysses", 2, {}), ("dummy_head", 4, {}), ("ring", 2, {}),
                                           ("usp", 4, dict(ulysses_degree=2, ring_degree=2)),
-                                          ("xtuner", 4, {}), ("oracle", 1, {})])
+                                          ("xtuner", 4, {}), ("oracle", 1, {}),
+                                          ("ulysses", 2, dict(force_messages=True)),
+                                          ("usp", 4, dict(ulysses_degree=2, ring_degree=2, force_messages=True))])
 def test_batched_engines(P, engine, sp, kw):
-    # tests/test_attention.cpp:317-396 mixes bs=2 into the engine grid
+    # tests/test_attention.cpp:317-396 mixes bs=2 into the engine grid; with force_messages the
+    # bs=2 blocks take the staged (not in-place) message path
     H = 6 if engine in ("dummy_head", "xtuner") else 4
     q, k, v, R = parity_inputs(31 + sp, 256, H, 2, 64, bs=2)
     check(run(P, engine, q, k, v, R, sp, **kw), q, k, v, R)
