@@ -117,6 +117,18 @@ void all_to_all(RankCtx& ctx, const CommGroup& group, const void* local, int64_t
                 int64_t heads, int64_t dim, int elem_bytes, int scatter_dim, int gather_dim,
                 void* out);
 
+// Reference all_gather (comm.cpp:381-447) along one axis of a tensor viewed as
+// [outer, extent, inner_bytes]: out = [outer, G * extent, inner_bytes] with member j's block at
+// [j * extent, (j + 1) * extent) of every outer slice (group order). Every member passes the
+// same outer / extent / inner_bytes (the reference's extent check outside the axis). Counted
+// as one all_gather of local_bytes * (G - 1).
+void all_gather(RankCtx& ctx, const CommGroup& group, const void* local, int64_t outer, int64_t extent,
+                int64_t inner_bytes, void* out);
+
+// Reference ring_shift (comm.cpp:449-460): group index i receives the payload of index i-1
+// (`bytes` on every member). Counted as one p2p of `bytes` (0 for a single member).
+void ring_shift(RankCtx& ctx, const CommGroup& group, const void* payload, int64_t bytes, void* out);
+
 // Event timing of the attention kernels (bench.py): ms[0]/n[0] forward, ms[1]/n[1] backward.
 void profile_enable(bool on);
 void profile_read(double* ms, int64_t* n);

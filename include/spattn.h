@@ -220,6 +220,15 @@ int spattn_fabric_bwd(spattn_fabric* f, spattn_saved* const* saved, const void* 
  * device [bs, len, heads, dim] tensors of elem_bytes each, on the context's stream */
 int spattn_all_to_all(spattn_ctx* ctx, const void* local, void* out, int64_t bs, int64_t len,
                       int64_t heads, int64_t dim, int elem_bytes, int scatter_dim, int gather_dim);
+/* all_gather (comm.hpp:136, comm.cpp:381-447) over a rank context's SP group: the tensor is viewed
+ * as [outer, extent, inner_bytes] around the gather axis; out [outer, G*extent, inner_bytes]
+ * holds member j's block at [j*extent, (j+1)*extent) (group order). Every member passes the same
+ * sizes. Counted as all_gather of local_bytes*(G-1). */
+int spattn_all_gather(spattn_ctx* ctx, const void* local, void* out, int64_t outer, int64_t extent,
+                      int64_t inner_bytes);
+/* ring_shift (comm.hpp:140, comm.cpp:449-460): group index i receives index i-1's payload of
+ * `bytes` into out. Counted as one p2p of `bytes` (0 for a single member). */
+int spattn_ring_shift(spattn_ctx* ctx, const void* payload, void* out, int64_t bytes);
 /* all_to_all (comm.cpp:357-379) on [bs, len, heads, dim] tensors of elem_bytes each */
 int spattn_fabric_all_to_all(spattn_fabric* f, const void* const* local, void* const* out,
                              int64_t bs, int64_t len, int64_t heads, int64_t dim, int elem_bytes,

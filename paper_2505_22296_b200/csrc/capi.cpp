@@ -440,6 +440,15 @@ int spattn_all_to_all(spattn_ctx* ctx, const void* local, void* out, int64_t bs,
   });
 }
 
+int spattn_all_gather(spattn_ctx* ctx, const void* local, void* out, int64_t outer, int64_t extent,
+                      int64_t inner_bytes) {
+  return guard([&] { seqpar::all_gather(*ctx->rc, ctx->rc->sp_group, local, outer, extent, inner_bytes, out); });
+}
+
+int spattn_ring_shift(spattn_ctx* ctx, const void* payload, void* out, int64_t bytes) {
+  return guard([&] { seqpar::ring_shift(*ctx->rc, ctx->rc->sp_group, payload, bytes, out); });
+}
+
 int spattn_block_fwd(void* stream, int64_t bs, int heads, int kv_heads, int dim, const void* q,
                      const int64_t* qpos, int64_t lq, const void* k, const void* v,
                      const int64_t* kpos, int64_t lk, int causal, double scale, float* acc_out,

@@ -1566,4 +1566,63 @@ void all_to_all(RankCtx& ctx, const CommGroup& group, const void* local, int64_t
   }
 }
 
+void all_gather(RankCtx& ctx, const CommGroup& group, const void* local, int64_t outer, int64_t extent,
+                int64_t inner_bytes, void* out) {
+  if (outer < 0 || extent < 0 || inner_bytes < 0) throw ShapeError("all_gather: negative extent");
+  const int G = group.size(), me = group.index_of(ctx.rank);
+  const int64_t blk = extent * inner_bytes, local_bytes = outer * blk;
+  ctx.count(Primitive::all_gather, local_bytes * (G - 1));
+  cudaStream_t s = ctx.stream;
+  if (local_bytes == 0) return;
+  // member j's [outer, blk] block lands at byte column j * blk of out's [outer, G * blk] rows
+  auto place = [&](int j, const void* src, std::vector<CopyTask>& t) {
+    t.push_back({src, out, blk, G * blk, 0, 0, 0, j * blk, outer, blk, 0});
+  };
+  if (G == 1 || ctx.transport->peer_access()) {
+    std::vector<void*> ptrs{const_cast<void*>(local)};
+    if (G > 1) ptrs = ctx.transport->exchange_ptrs(group, ctx.rank, const_cast<void*>(local), s);
+    std::vector<CopyTask> tasks;
+    for (int j = 0; j < G; ++j) place(j, ptrs[static_cast<size_t>(j)], tasks);
+    run_tasks(tasks, 1, false, s);
+    if (G > 1) ctx.transport->release(group, ctx.rank, s);
+    return;
+  }
+  // messages: my block to every member; a member's block is received in place when out's
+  // rows are a single slice (outer == 1), else staged and placed
+  DevBuf rbuf(outer == 1 ? 0 : static_cast<size_t>(G * local_bytes), s);
+  std::vector<Msg> sends, recvs;
+  for (int j = 0; j < G; ++j) {
+    sends.push_back({j, const_cast<void*>(local), static_cast<size_t>(local_bytes)});
+    char* dst = outer == 1 ? static_cast<char*>(out) + j * blk : static_cast<char*>(rbuf.p) + j * local_bytes;
+    recvs.push_back({j, dst, static_cast<size_t>(local_bytes)});
+  }
+  ctx.transport->send_recv(group, ctx.rank, sends, recvs, s);
+  if (outer > 1) {
+    std::vector<CopyTask> tasks;
+    for (int j = 0; j < G; ++j) place(j, static_cast<char*>(rbuf.p) + j * local_bytes, tasks);
+    run_tasks(tasks, 1, false, s);
+  }
+  (void)me;
+}
+
+void ring_shift(RankCtx& ctx, const CommGroup& group, const void* payload, int64_t bytes, void* out) {
+  if (bytes < 0) throw ShapeError("ring_shift: negative size");
+  const int G = group.size(), me = group.index_of(ctx.rank);
+  ctx.count(Primitive::p2p, G == 1 ? 0 : bytes);
+  cudaStream_t s = ctx.stream;
+  if (bytes == 0) return;
+  const int from = (me - 1 + G) % G, to = (me + 1) % G;
+  if (G == 1 || ctx.transport->peer_access()) {
+    std::vector<void*> ptrs{const_cast<void*>(payload)};
+    if (G > 1) ptrs = ctx.transport->exchange_ptrs(group, ctx.rank, const_cast<void*>(payload), s);
+    if (out != ptrs[static_cast<size_t>(from)])
+      SP_CUDA(cudaMemcpyAsync(out, ptrs[static_cast<size_t>(from)], static_cast<size_t>(bytes),
+                              cudaMemcpyDeviceToDevice, s));
+    if (G > 1) ctx.transport->release(group, ctx.rank, s);
+    return;
+  }
+  ctx.transport->send_recv(group, ctx.rank, {{to, const_cast<void*>(payload), static_cast<size_t>(bytes)}},
+                           {{from, out, static_cast<size_t>(bytes)}}, s);
+}
+
 }  // namespace seqpar

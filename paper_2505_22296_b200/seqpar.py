@@ -541,6 +541,98 @@ class RankContext:
         return out
 
 
+def _rank_of(group):
+    """(context handle, group size, index in the group) of a RankContext or a (Fabric, rank)."""
+    if isinstance(group, RankContext):
+        return group._h, group.sp, group.rank % group.sp
+    if isinstance(group, tuple) and len(group) == 2 and isinstance(group[0], Fabric):
+        fab, r = group
+        return fab.ctxs[r], fab.sp, r % fab.sp
+    raise ConfigError("expected a RankContext or a (Fabric, rank) pair")
+
+
+def _around(x: torch.Tensor, dim: int):
+    """x viewed as [outer, extent, inner_bytes] around axis `dim`."""
+    outer = 1
+    for n in x.shape[:dim]:
+        outer *= n
+    inner = x.element_size()
+    for n in x.shape[dim + 1:]:
+        inner *= n
+    return outer, x.shape[dim], inner
+
+
+def _tree_sum(parts):
+    """tree_sum_into (comm.cpp:325-337): balanced pairwise sum in group order."""
+    if len(parts) == 1:
+        return parts[0]
+    mid = len(parts) // 2
+    return _tree_sum(parts[:mid]) + _tree_sum(parts[mid:])
+
+
+class _AllGather(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, h, G, idx, dim):
+        x = x.contiguous()
+        outer, extent, inner = _around(x, dim)
+        shape = list(x.shape)
+        shape[dim] *= G
+        out = torch.empty(shape, dtype=x.dtype, device=x.device)
+        C.check(C.lib().spattn_ctx_set_stream(h, _stream()))
+        C.check(C.lib().spattn_all_gather(h, x.data_ptr(), out.data_ptr(), outer, extent, inner))
+        ctx.meta = (h, G, dim, outer, extent, tuple(x.shape))
+        return out
+
+    @staticmethod
+    def backward(ctx, gy):
+        h, G, dim, outer, extent, xshape = ctx.meta
+        return _reduce_scatter(h, G, gy, outer, extent).reshape(xshape), None, None, None, None
+
+
+def _reduce_scatter(h, G, gy, outer, extent):
+    """The all_gather backward (comm.cpp:418-443): one all_to_all hands every member its block
+    of each member's gathered gradient, tree-summed in group order (counted as all_to_all)."""
+    gy = gy.contiguous()
+    rest = gy.numel() // max(1, outer * G * extent)  # elements after the gather axis
+    buf = torch.empty((1, G * outer, extent, rest), dtype=gy.dtype, device=gy.device)
+    C.check(C.lib().spattn_ctx_set_stream(h, _stream()))
+    C.check(C.lib().spattn_all_to_all(h, gy.data_ptr(), buf.data_ptr(), 1, outer, G * extent, rest,
+                                      gy.element_size(), 2, 1))
+    return _tree_sum(list(buf.view(G, outer, extent, rest).unbind(0)))
+
+
+def all_gather_backward(group, grad_out: torch.Tensor, local_shape, dim: int) -> torch.Tensor:
+    """Gradient of all_gather w.r.t. this member's input (what autograd calls; exposed for
+    callers that drive backward themselves, e.g. one Python thread per loopback rank)."""
+    h, G, idx = _rank_of(group)
+    dim = dim % len(local_shape)
+    outer = 1
+    for n in local_shape[:dim]:
+        outer *= n
+    return _reduce_scatter(h, G, grad_out, outer, local_shape[dim]).reshape(local_shape)
+
+
+def all_gather(group, x: torch.Tensor, dim: int):
+    """all_gather (comm.hpp:136, comm.cpp:381-447) over the group of ``group`` (a RankContext
+    or a (Fabric, rank) pair): members' tensors concatenated along ``dim`` in group order;
+    differentiable (the backward reduce-scatters). Every member must call it."""
+    h, G, idx = _rank_of(group)
+    dim = dim % x.dim()
+    return _AllGather.apply(x, h, G, idx, dim)
+
+
+def ring_shift(group, payload: torch.Tensor) -> torch.Tensor:
+    """ring_shift (comm.hpp:140, comm.cpp:449-460): group index i returns the payload of index
+    i-1 (same shape and dtype on every member). Every member must call it."""
+    h, G, idx = _rank_of(group)
+    payload = payload.contiguous()
+    out = torch.empty_like(payload)
+    C.check(C.lib().spattn_ctx_set_stream(h, _stream()))
+    C.check(C.lib().spattn_ring_shift(h, payload.data_ptr(), out.data_ptr(),
+                                      payload.numel() * payload.element_size()))
+    return out
+
+
 def attention_step_host(engine: str, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                         dout: torch.Tensor, rank_ctx: Optional["RankContext"] = None,
                         seq_len: Optional[int] = None, layout: str = "auto", causal: bool = True,
