@@ -100,3 +100,41 @@ def test_ring_shift_moves_one_hop_and_is_periodic(P, messages):
         assert first == float((r + 3) % 4) and back == float(r)
     assert res[2][0] == 1.0
     assert fab.stats(0)["p2p"] == (4, 4 * 8)
+
+
+def test_asymmetric_failure_aborts_peers_instead_of_hanging(P):
+    """tests/test_comm.cpp:290-300: one rank fails before the exchange (a null q); the others,
+    already waiting in the all-to-all rendezvous, abort and the group call reports the root
+    cause instead of hanging."""
+    import ctypes
+
+    from paper_2505_22296_b200 import _lib as C
+
+    sp, L, H, d = 2, 256, 4, 64
+    fab = P.Fabric(sp)
+    mk = lambda h: torch.randn(1, L // sp, h, d, device="cuda").bfloat16()  # noqa: E731
+    qs, ks, vs = [mk(H) for _ in range(sp)], [mk(2) for _ in range(sp)], [mk(2) for _ in range(sp)]
+    outs = [torch.empty_like(x) for x in qs]
+    lses = [torch.empty(1, L // sp, H, device="cuda") for _ in range(sp)]
+    cfg, lay = C.make_config(H, 2, d, True), C.make_layout("naive", L, sp)
+    saved = (ctypes.c_void_p * sp)()
+    torch.cuda.synchronize()
+    rc, err, msg = [None], [], [""]
+
+    def call():
+        try:
+            rc[0] = C.lib().spattn_fabric_fwd_rope(
+                fab._h, C.engine_id("ulysses"), ctypes.byref(cfg), ctypes.byref(lay), 1,
+                C.ptr_array([qs[0].data_ptr(), 0]), C.ptr_array([x.data_ptr() for x in ks]),
+                C.ptr_array([x.data_ptr() for x in vs]), C.ptr_array([x.data_ptr() for x in outs]),
+                C.ptr_array([x.data_ptr() for x in lses]), None, 0, None, 10000.0, saved)
+            msg[0] = C.lib().spattn_last_error().decode()  # thread-local: read on this thread
+        except Exception as e:  # noqa: BLE001
+            err.append(repr(e))
+
+    t = threading.Thread(target=call)
+    t.start()
+    t.join(timeout=60)
+    assert not t.is_alive(), "the group call hung"
+    assert not err and rc[0] != 0
+    assert msg[0] and "peer rank failed" not in msg[0], msg[0]  # the root cause, not the abort
