@@ -145,6 +145,11 @@ class LoopbackFabric {
 // One process per GPU; NCCL loaded at run time (libnccl.so.2, the copy torch already mapped).
 // `unique_id` is the 128-byte ncclUniqueId rank 0 created (spattn_nccl_unique_id) and the
 // launcher broadcast.
+// broadcast_bytes (comm.hpp:159-161, comm.cpp:526-545): the root RANK's bytes reach every member;
+// counted as bytes * (g - 1) / g per rank. ConfigError when root is not in the group.
+std::vector<uint8_t> broadcast_bytes(RankCtx& ctx, const CommGroup& group, const std::vector<uint8_t>& payload,
+                                     int root);
+
 // replicate_packing_mask (partition.cpp:222-227) over broadcast_bytes (comm.cpp:526-545):
 // group index 0 supplies the neat-packing mask (other ranks pass anything, e.g. empty); every
 // member returns the root's bytes. The mask is replicated, not split. Counted

@@ -81,6 +81,12 @@ int spattn_split_position_map(const spattn_layout* layout, int index, const int6
  * (a -1 padding tail is one more document); ConfigError when an id is not one run. */
 int spattn_documents_from_segments(const int64_t* segment_ids, int64_t len, int64_t* doc_lens,
                                    int max_docs, int* n_docs);
+/* broadcast_bytes (comm.hpp:159-161, comm.cpp:526-545) over a context's SP group: the bytes of
+ * global rank `root` reach every member (members pass any payload); the result (at most `cap`
+ * bytes) lands in out, its length in out_len. Counted as len*(g-1)/g. CONFIG error when root is
+ * not in the group. */
+int spattn_broadcast_bytes(spattn_ctx* ctx, const uint8_t* payload, int64_t len, int root, uint8_t* out,
+                           int64_t cap, int64_t* out_len);
 /* replicate_packing_mask (partition.cpp:222-227): group index 0's bytes to every member over
  * the context's transport; out holds cap bytes, *out_len receives the mask length. */
 int spattn_replicate_packing_mask(spattn_ctx* ctx, const uint8_t* mask, int64_t len, uint8_t* out,

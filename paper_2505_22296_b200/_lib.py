@@ -31,7 +31,7 @@ EXPORTS = [
     "spattn_profile_read", "spattn_selftest_umma", "spattn_plan_heads", "spattn_plan_problems",
     "spattn_debug_bwd_trace", "spattn_debug_fwd_cta_trace", "spattn_debug_transport_selftest", "spattn_fwd_rope", "spattn_fabric_fwd_rope", "spattn_rope_apply",
     "spattn_step_host", "spattn_pick_step_groups", "spattn_pad_batch",
-    "spattn_split_position_map", "spattn_documents_from_segments", "spattn_replicate_packing_mask",
+    "spattn_split_position_map", "spattn_documents_from_segments", "spattn_replicate_packing_mask", "spattn_broadcast_bytes",
     "spattn_fabric_replicate_packing_mask", "spattn_logprob_fwd", "spattn_logprob_bwd",
     "spattn_exact_sum_device", "spattn_exact_sum_host", "spattn_exact_merge", "spattn_exact_round",
     "spattn_exact_sum_all_reduce", "spattn_all_reduce_count", "spattn_all_reduce_values",
@@ -136,6 +136,7 @@ def lib() -> ctypes.CDLL:
         "spattn_split_position_map": [layp, _i32, _i64p, _i64p],
         "spattn_documents_from_segments": [_i64p, _i64, _i64p, _i32, ctypes.POINTER(ctypes.c_int)],
         "spattn_replicate_packing_mask": [_vp, _vp, _i64, _vp, _i64, _i64p],
+        "spattn_broadcast_bytes": [_vp, _vp, _i64, _i32, _vp, _i64, _i64p],
         "spattn_fabric_replicate_packing_mask": [_vp, ctypes.POINTER(_vp), _i64p, ctypes.POINTER(_vp),
                                                  _i64, _i64p],
         "spattn_step_host": [_vp, _i32, cfgp, layp, _i64] + [_vp] * 9 + [_i64p, _i32, _i32],

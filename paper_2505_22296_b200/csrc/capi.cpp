@@ -590,6 +590,14 @@ extern "C" int spattn_replicate_packing_mask(spattn_ctx* ctx, const uint8_t* mas
   });
 }
 
+extern "C" int spattn_broadcast_bytes(spattn_ctx* ctx, const uint8_t* payload, int64_t len, int root,
+                                      uint8_t* out, int64_t cap, int64_t* out_len) {
+  return guard([&] {
+    const std::vector<uint8_t> m = payload ? std::vector<uint8_t>(payload, payload + len) : std::vector<uint8_t>();
+    copy_mask(seqpar::broadcast_bytes(*ctx->rc, ctx->rc->sp_group, m, root), out, cap, out_len);
+  });
+}
+
 extern "C" int spattn_fabric_replicate_packing_mask(spattn_fabric* f, const uint8_t* const* masks,
                                                     const int64_t* lens, uint8_t* const* outs,
                                                     int64_t cap, int64_t* out_lens) {

@@ -369,26 +369,30 @@ void nccl_unique_id(void* out128) {
   std::memcpy(out128, &id, sizeof(id));
 }
 
-std::vector<uint8_t> replicate_packing_mask(RankCtx& ctx, const CommGroup& group,
-                                            const std::vector<uint8_t>& mask) {
+std::vector<uint8_t> broadcast_bytes(RankCtx& ctx, const CommGroup& group, const std::vector<uint8_t>& payload,
+                                     int root) {
   const int g = group.size();
   const int me = group.index_of(ctx.rank);
+  if (!group.contains(root)) throw ConfigError("broadcast root not in group");
+  const int ri = group.index_of(root);
+  const bool is_root = me == ri;
   cudaStream_t s = ctx.stream;
   if (g == 1) {
     ctx.count(Primitive::broadcast, 0);
-    return mask;
+    return payload;
   }
   // the root's size first (members do not know it), then the payload; both staged in device
   // memory so the NCCL transport can carry them
   int64_t* dsize = nullptr;
   SP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dsize), sizeof(int64_t), s));
-  int64_t n = me == 0 ? static_cast<int64_t>(mask.size()) : 0;
-  if (me == 0) SP_CUDA(cudaMemcpyAsync(dsize, &n, sizeof(n), cudaMemcpyHostToDevice, s));
+  int64_t n = is_root ? static_cast<int64_t>(payload.size()) : 0;
+  if (is_root) SP_CUDA(cudaMemcpyAsync(dsize, &n, sizeof(n), cudaMemcpyHostToDevice, s));
   std::vector<Msg> sends, recvs;
-  if (me == 0) {
-    for (int j = 1; j < g; ++j) sends.push_back({j, dsize, sizeof(int64_t)});
+  if (is_root) {
+    for (int j = 0; j < g; ++j)
+      if (j != ri) sends.push_back({j, dsize, sizeof(int64_t)});
   } else {
-    recvs.push_back({0, dsize, sizeof(int64_t)});
+    recvs.push_back({ri, dsize, sizeof(int64_t)});
   }
   ctx.transport->send_recv(group, ctx.rank, sends, recvs, s);
   SP_CUDA(cudaMemcpyAsync(&n, dsize, sizeof(n), cudaMemcpyDeviceToHost, s));
@@ -398,13 +402,14 @@ std::vector<uint8_t> replicate_packing_mask(RankCtx& ctx, const CommGroup& group
   if (n > 0) {
     void* buf = nullptr;
     SP_CUDA(cudaMallocAsync(&buf, static_cast<size_t>(n), s));
-    if (me == 0) SP_CUDA(cudaMemcpyAsync(buf, mask.data(), static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
+    if (is_root) SP_CUDA(cudaMemcpyAsync(buf, payload.data(), static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
     sends.clear();
     recvs.clear();
-    if (me == 0) {
-      for (int j = 1; j < g; ++j) sends.push_back({j, buf, static_cast<size_t>(n)});
+    if (is_root) {
+      for (int j = 0; j < g; ++j)
+        if (j != ri) sends.push_back({j, buf, static_cast<size_t>(n)});
     } else {
-      recvs.push_back({0, buf, static_cast<size_t>(n)});
+      recvs.push_back({ri, buf, static_cast<size_t>(n)});
     }
     ctx.transport->send_recv(group, ctx.rank, sends, recvs, s);
     SP_CUDA(cudaMemcpyAsync(out.data(), buf, static_cast<size_t>(n), cudaMemcpyDeviceToHost, s));
@@ -413,6 +418,11 @@ std::vector<uint8_t> replicate_packing_mask(RankCtx& ctx, const CommGroup& group
   }
   ctx.count(Primitive::broadcast, n * (g - 1) / g);
   return out;
+}
+
+std::vector<uint8_t> replicate_packing_mask(RankCtx& ctx, const CommGroup& group,
+                                            const std::vector<uint8_t>& mask) {
+  return broadcast_bytes(ctx, group, mask, group.ranks.front());
 }
 
 }  // namespace seqpar

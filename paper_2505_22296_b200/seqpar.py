@@ -633,6 +633,19 @@ def ring_shift(group, payload: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def broadcast_bytes(group, payload: Optional[bytes], root: int, max_len: int) -> bytes:
+    """broadcast_bytes (comm.hpp:159-161): the bytes of global rank ``root`` on every member of
+    the group of ``group`` (a RankContext or a (Fabric, rank) pair); ``max_len`` bounds the
+    result. Every member must call it."""
+    h, _, _ = _rank_of(group)
+    m = payload or b""
+    buf = ctypes.create_string_buffer(m, max(1, len(m)))
+    out = ctypes.create_string_buffer(max(1, max_len))
+    n = _i64()
+    C.check(C.lib().spattn_broadcast_bytes(h, buf, len(m), root, out, max_len, n))
+    return out.raw[:n[0]]
+
+
 def attention_step_host(engine: str, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                         dout: torch.Tensor, rank_ctx: Optional["RankContext"] = None,
                         seq_len: Optional[int] = None, layout: str = "auto", causal: bool = True,

@@ -138,3 +138,31 @@ def test_asymmetric_failure_aborts_peers_instead_of_hanging(P):
     assert not t.is_alive(), "the group call hung"
     assert not err and rc[0] != 0
     assert msg[0] and "peer rank failed" not in msg[0], msg[0]  # the root cause, not the abort
+
+
+@pytest.mark.parametrize("messages", [False, True])
+def test_broadcast_replicates_the_root_payload(P, messages):
+    # tests/test_comm.cpp:325-338 (root 0) and a non-zero root
+    for root in (0, 2):
+        fab = P.Fabric(4, force_messages=messages)
+        got = on_ranks(fab, lambda r: P.broadcast_bytes((fab, r), bytes([1, 1, 0, 1]) if r == root else None,
+                                                        root, 16))
+        for r in range(4):
+            assert got[r] == bytes([1, 1, 0, 1])
+            assert fab.stats(r)["broadcast"] == (1, 4 * 3 // 4)
+
+
+def test_group_of_one_is_identity_with_zero_bytes(P):
+    # tests/test_comm.cpp:340-360
+    fab = P.Fabric(1)
+    x = torch.tensor([[1.0, 2.0], [3.0, 4.0]], dtype=torch.float64, device="cuda")
+    assert torch.equal(P.all_gather((fab, 0), x, 0), x)
+    assert torch.equal(P.ring_shift((fab, 0), x), x)
+    assert P.broadcast_bytes((fab, 0), b"\x05\x06", 0, 8) == b"\x05\x06"
+    assert all(b == 0 for _, b in fab.stats(0).values())
+
+
+def test_broadcast_root_outside_group_raises(P):
+    fab = P.Fabric(2, sp=1)  # two SP groups of one rank each
+    with pytest.raises(ValueError):
+        P.broadcast_bytes((fab, 0), b"x", 1, 8)
