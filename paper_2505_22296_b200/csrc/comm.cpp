@@ -295,8 +295,11 @@ class NcclTransport : public Transport {
     nccl_check(nccl().CommInitRank(&world_comm_, world, id, rank), "CommInitRank");
   }
   ~NcclTransport() override {
-    for (auto& kv : sub_) nccl().CommDestroy(kv.second);
-    if (world_comm_) nccl().CommDestroy(world_comm_);
+    // after a failed NCCL call the communicators may hold operations that never complete:
+    // abort them (the reference aborts the group on a peer failure, comm.cpp:206-230)
+    auto end = failed_ ? nccl().CommAbort : nccl().CommDestroy;
+    for (auto& kv : sub_) end(kv.second);
+    if (world_comm_) end(world_comm_);
   }
   bool peer_access() const override { return false; }
   std::vector<void*> exchange_ptrs(const CommGroup&, int, void*, cudaStream_t) override {
@@ -322,13 +325,18 @@ class NcclTransport : public Transport {
 
   void send_recv(const CommGroup& g, int, const std::vector<Msg>& sends,
                  const std::vector<Msg>& recvs, cudaStream_t s) override {
-    ncclComm_t c = comm_for(g);
-    nccl_check(nccl().GroupStart(), "GroupStart");
-    for (const Msg& m : sends)
-      if (m.bytes) nccl_check(nccl().Send(m.ptr, m.bytes, ncclUint8, m.peer, c, s), "Send");
-    for (const Msg& m : recvs)
-      if (m.bytes) nccl_check(nccl().Recv(m.ptr, m.bytes, ncclUint8, m.peer, c, s), "Recv");
-    nccl_check(nccl().GroupEnd(), "GroupEnd");
+    try {
+      ncclComm_t c = comm_for(g);
+      nccl_check(nccl().GroupStart(), "GroupStart");
+      for (const Msg& m : sends)
+        if (m.bytes) nccl_check(nccl().Send(m.ptr, m.bytes, ncclUint8, m.peer, c, s), "Send");
+      for (const Msg& m : recvs)
+        if (m.bytes) nccl_check(nccl().Recv(m.ptr, m.bytes, ncclUint8, m.peer, c, s), "Recv");
+      nccl_check(nccl().GroupEnd(), "GroupEnd");
+    } catch (...) {
+      failed_ = true;
+      throw;
+    }
   }
 
  private:
@@ -353,6 +361,7 @@ class NcclTransport : public Transport {
   }
 
   int rank_, world_;
+  bool failed_ = false;
   ncclComm_t world_comm_ = nullptr;
   std::map<std::string, ncclComm_t> sub_;
 };
