@@ -525,11 +525,48 @@ void launch_attn_fwd_mma(const FwdArgs& a, const ProblemSet& in, cudaStream_t s)
   }
 }
 
+// delta with 16-byte loads: TPH = d/8 lanes per (row, head), 32/TPH (row, head) pairs per warp
+// (the one-warp-per-pair kernel above keeps 4-byte loads and reaches ~half the HBM rate)
+template <int TPH>
+__global__ void __launch_bounds__(256) attn_bwd_pre_v16(BwdArgs a, int rows) {
+  const int64_t pair = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / TPH;
+  const int sub = threadIdx.x % TPH;
+  const int hq = a.hm.hq;
+  const bool live = pair < (int64_t)rows * hq;
+  float acc = 0.f;
+  int64_t row = 0;
+  int h = 0;
+  if (live) {
+    row = pair / hq, h = (int)(pair % hq);
+    const int64_t off = row * a.o_row_stride + (int64_t)h * a.d + sub * 8;
+    const uint4 x = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.o) + off);
+    const uint4 y = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.dout) + off);
+    const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&x);
+    const __nv_bfloat162* yp = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 u = __bfloat1622float2(xp[i]), w = __bfloat1622float2(yp[i]);
+      acc += u.x * w.x + u.y * w.y;
+    }
+  }
+#pragma unroll
+  for (int sft = TPH / 2; sft > 0; sft >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sft);
+  if (live && sub == 0) a.delta[row * a.lse_row_stride + h] = acc;
+}
+
 void launch_attn_bwd_pre(const BwdArgs& a, int rows, cudaStream_t s) {
-  const int warps = rows * a.hm.hq;
-  if (warps == 0) return;
-  attn_bwd_pre<<<(warps + 7) / 8, 256, 0, s>>>(a, rows);
-    note_launch();
+  const int64_t pairs = (int64_t)rows * a.hm.hq;
+  if (pairs == 0) return;
+  const bool v16 = (a.d == 64 || a.d == 128) && (a.o_row_stride % 8) == 0 &&
+                   reinterpret_cast<uintptr_t>(a.o) % 16 == 0 && reinterpret_cast<uintptr_t>(a.dout) % 16 == 0;
+  if (v16 && a.d == 128) {
+    attn_bwd_pre_v16<16><<<(unsigned)((pairs * 16 + 255) / 256), 256, 0, s>>>(a, rows);
+  } else if (v16) {
+    attn_bwd_pre_v16<8><<<(unsigned)((pairs * 8 + 255) / 256), 256, 0, s>>>(a, rows);
+  } else {
+    attn_bwd_pre<<<(unsigned)((pairs + 7) / 8), 256, 0, s>>>(a, rows);
+  }
+  note_launch();
 }
 
 void launch_attn_bwd_mma(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
