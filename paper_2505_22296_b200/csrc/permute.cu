@@ -122,6 +122,28 @@ __global__ void f32_to_bf16_kernel(__nv_bfloat162* dst, const float2* src, float
   }
 }
 
+// 8 values per thread: two 16-byte loads, one 16-byte store, unrolled twice so four loads are
+// in flight per thread (the 8-byte grid-stride loop above reaches ~77 % of the HBM rate)
+__global__ void __launch_bounds__(256) f32_to_bf16_v8_kernel(uint4* dst, const float4* src, float scale, int64_t n8) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto cvt = [&](const float4& a, const float4& b) {
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(a.x * scale, a.y * scale);
+    __nv_bfloat162 p1 = __floats2bfloat162_rn(a.z * scale, a.w * scale);
+    __nv_bfloat162 p2 = __floats2bfloat162_rn(b.x * scale, b.y * scale);
+    __nv_bfloat162 p3 = __floats2bfloat162_rn(b.z * scale, b.w * scale);
+    return make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
+                      *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
+  };
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + stride < n8; i += 2 * stride) {
+    const float4 a0 = __ldcs(src + 2 * i), b0 = __ldcs(src + 2 * i + 1);
+    const float4 a1 = __ldcs(src + 2 * (i + stride)), b1 = __ldcs(src + 2 * (i + stride) + 1);
+    dst[i] = cvt(a0, b0);
+    dst[i + stride] = cvt(a1, b1);
+  }
+  if (i < n8) dst[i] = cvt(__ldcs(src + 2 * i), __ldcs(src + 2 * i + 1));
+}
+
 __global__ void bf16_to_f32_kernel(float* dst, const __nv_bfloat16* src, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -220,7 +242,11 @@ void launch_fill_f32(float* p, float v, int64_t n, cudaStream_t s) {
 
 void launch_f32_to_bf16(void* dst, const float* src, float scale, int64_t n, cudaStream_t s) {
   if (n == 0) return;
-  if (n % 2 == 0) {
+  if (n % 8 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) {
+    f32_to_bf16_v8_kernel<<<grid_for(n / 8, 512), 256, 0, s>>>(reinterpret_cast<uint4*>(dst),
+                                                               reinterpret_cast<const float4*>(src), scale, n / 8);
+    note_launch();
+  } else if (n % 2 == 0) {
     f32_to_bf16_kernel<<<grid_for(n / 2, 1024), 256, 0, s>>>(
         reinterpret_cast<__nv_bfloat162*>(dst), reinterpret_cast<const float2*>(src), scale, n / 2);
   note_launch();
