@@ -50,7 +50,22 @@ __global__ void __launch_bounds__(256) copy_rows_kernel(CopyLaunch L, int elem_b
     const int64_t nv = T.cols * elem_bytes / VW;
     const V* s = reinterpret_cast<const V*>(src);
     V* d = reinterpret_cast<V*>(dst);
-    for (int64_t i = lane; i < nv; i += 32) d[i] = s[i];
+    // loads batched ahead of their stores (src and dst may alias as far as the compiler knows,
+    // so a plain loop keeps one load in flight per lane)
+    int64_t i = lane;
+    for (; i + 96 < nv; i += 128) {
+      const V a = s[i], b = s[i + 32], c = s[i + 64], e = s[i + 96];
+      d[i] = a;
+      d[i + 32] = b;
+      d[i + 64] = c;
+      d[i + 96] = e;
+    }
+    for (; i + 32 < nv; i += 64) {
+      const V a = s[i], b = s[i + 32];
+      d[i] = a;
+      d[i + 32] = b;
+    }
+    for (; i < nv; i += 32) d[i] = s[i];
     const int64_t nz = T.zero_cols * elem_bytes / VW;
     V z;
     memset(&z, 0, sizeof(V));
