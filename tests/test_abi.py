@@ -74,3 +74,41 @@ def test_binding_arity_matches_header():
         n = 0 if params in ("", "void") else params.count(",") + 1
         at = getattr(L, name).argtypes
         assert at is None or len(at) == n, (name, n, len(at))
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """The boundary is a C ABI: a plain C program (gcc, no C++) includes spattn.h, links
+    libspattn.so and calls the host-side entry points (what a cgo / JNI / FFI stub does)."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "abi.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include "spattn.h"
+int main(void) {
+  int64_t n = 0, pairs = 0;
+  if (spattn_abi_version() != 1) return 1;
+  if (spattn_pad_length(1000, 4, 2048, 0, &n) != 0) return 2;
+  spattn_layout lay = {0};
+  lay.mode = 1; lay.sp = 2; lay.global_len = 8;  /* zigzag(8, 2) */
+  int64_t pos[4];
+  if (spattn_layout_positions(&lay, 0, pos) != 0) return 3;
+  if (spattn_causal_pairs(&lay, 0, &pairs) != 0) return 4;
+  if (spattn_pad_length(10, 4, 3, 0, &n) == 0) return 5;  /* cutoff below len*: an error code */
+  printf("%lld %lld %lld %lld %lld %s\n", (long long)pos[0], (long long)pos[1], (long long)pos[2],
+         (long long)pos[3], (long long)pairs, spattn_last_error());
+  return 0;
+}
+''')
+    exe = tmp_path / "abi"
+    libdir = os.path.dirname(C.LIB_PATH)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src),
+                    "-L", libdir, "-l:" + os.path.basename(C.LIB_PATH), "-Wl,-rpath," + libdir, "-o", str(exe)],
+                   check=True, capture_output=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, (out.returncode, out.stderr)
+    vals = out.stdout.split()
+    assert [int(x) for x in vals[:5]] == [0, 1, 6, 7, 18]  # tests/test_partition.cpp:19-33
