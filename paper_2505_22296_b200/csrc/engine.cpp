@@ -400,9 +400,114 @@ void set_rope(CopyTask& t, const float2* table, int64_t row0, int64_t mod, int d
   t.rope_sign = sign;
 }
 
+// One forward move (sequence -> head shard) of a tensor for the message path.
+struct FwdMove {
+  const MoveSpec* m;
+  const void* x;
+  void* y;
+  const RopeMove* rope;
+};
+
+// Message path of one or more forward moves over the same group: pack per destination (RoPE
+// rotates while packing) -> ONE grouped send/recv carrying every move's messages (per peer in
+// move order, the order NCCL matches them in) -> unpack per source. A source whose rows land as
+// one contiguous block of y (bs 1, one run of all its rows, this member's window spanning y's
+// rows: the natural Ulysses layout) is received in place.
+void move_forward_messages(RankCtx& ctx, const CommGroup& g, const std::vector<FwdMove>& moves,
+                           cudaStream_t s) {
+  const int G = g.size(), me = g.index_of(ctx.rank);
+  struct Plan {
+    std::vector<int64_t> soff, roff;
+    std::vector<char> in_place;
+    DevBuf sbuf, rbuf;
+  };
+  std::vector<Plan> plans(moves.size());
+  std::vector<CopyTask> pack_plain, unpack;
+  int elem = 0;
+  bool same_elem = true;
+  for (size_t k = 0; k < moves.size(); ++k) {
+    const MoveSpec& m = *moves[k].m;
+    same_elem &= (elem == 0 || elem == m.elem);
+    elem = m.elem;
+  }
+  for (size_t k = 0; k < moves.size(); ++k) {
+    const MoveSpec& m = *moves[k].m;
+    const RopeMove* rope = moves[k].rope;
+    Plan& pl = plans[k];
+    const Window& w = m.win[static_cast<size_t>(me)];
+    const int64_t yw = m.yw[static_cast<size_t>(me)], rows = m.bs * m.lloc;
+    int64_t sent = 0;
+    for (int j = 0; j < G; ++j)
+      if (j != me) sent += m.bs * m.lloc * m.win[static_cast<size_t>(j)].n * m.elem;
+    ctx.count(Primitive::all_to_all, sent);
+    pl.soff.assign(G + 1, 0);
+    pl.roff.assign(G + 1, 0);
+    pl.in_place.assign(G, 0);
+    for (int i = 0; i < G; ++i) {
+      const auto& ri = m.runs[static_cast<size_t>(i)];
+      pl.in_place[i] = m.bs == 1 && ri.size() == 1 && ri[0].row0 == 0 && ri[0].n == m.lloc && w.ycol == 0 &&
+                       w.pad == 0 && yw == w.n;
+    }
+    for (int j = 0; j < G; ++j) pl.soff[j + 1] = pl.soff[j] + rows * m.win[static_cast<size_t>(j)].n;
+    for (int i = 0; i < G; ++i) pl.roff[i + 1] = pl.roff[i] + (pl.in_place[i] ? 0 : rows * w.n);
+    pl.sbuf = DevBuf(static_cast<size_t>(pl.soff[G] * m.elem), s);
+    pl.rbuf = DevBuf(static_cast<size_t>(pl.roff[G] * m.elem), s);
+    std::vector<CopyTask> pack;
+    for (int j = 0; j < G; ++j) {
+      const Window& wj = m.win[static_cast<size_t>(j)];
+      if (wj.n == 0) continue;
+      pack.push_back({moves[k].x, static_cast<char*>(pl.sbuf.p) + pl.soff[j] * m.elem, m.xw, wj.n, 0, 0, wj.xcol,
+                      0, rows, wj.n, 0});
+      if (rope) set_rope(pack.back(), rope->table, 0, m.lloc, rope->dim, rope->sign);
+    }
+    if (rope || !same_elem)
+      run_tasks(pack, m.elem, false, s);  // rotating packs run the RoPE copier
+    else
+      pack_plain.insert(pack_plain.end(), pack.begin(), pack.end());
+    for (int i = 0; i < G; ++i) {
+      if ((w.n == 0 && w.pad == 0) || pl.in_place[i]) continue;
+      for (int64_t b = 0; b < m.bs; ++b)
+        for (const auto& r : m.runs[static_cast<size_t>(i)])
+          unpack.push_back({static_cast<char*>(pl.rbuf.p) + pl.roff[i] * m.elem, moves[k].y, w.n, yw,
+                            b * m.lloc + r.row0, b * m.lg + r.pos0, 0, w.ycol, r.n, w.n, w.pad});
+    }
+  }
+  run_tasks(pack_plain, elem, false, s);
+  std::vector<Msg> sends, recvs;
+  for (int j = 0; j < G; ++j)
+    for (size_t k = 0; k < moves.size(); ++k) {
+      const MoveSpec& m = *moves[k].m;
+      const Plan& pl = plans[k];
+      const Window& w = m.win[static_cast<size_t>(me)];
+      const int64_t yw = m.yw[static_cast<size_t>(me)], rows = m.bs * m.lloc;
+      sends.push_back({j, static_cast<char*>(pl.sbuf.p) + pl.soff[j] * m.elem,
+                       static_cast<size_t>((pl.soff[j + 1] - pl.soff[j]) * m.elem)});
+      if (pl.in_place[j])
+        recvs.push_back({j, static_cast<char*>(moves[k].y) + m.runs[static_cast<size_t>(j)][0].pos0 * yw * m.elem,
+                         static_cast<size_t>(rows * w.n * m.elem)});
+      else
+        recvs.push_back({j, static_cast<char*>(pl.rbuf.p) + pl.roff[j] * m.elem,
+                         static_cast<size_t>((pl.roff[j + 1] - pl.roff[j]) * m.elem)});
+    }
+  ctx.transport->send_recv(g, ctx.rank, sends, recvs, s);
+  if (same_elem) {
+    run_tasks(unpack, elem, false, s);
+  } else {
+    for (size_t k = 0, t0 = 0; k < moves.size(); ++k) {  // unpack tasks are in move order
+      std::vector<CopyTask> mine;
+      while (t0 < unpack.size() && unpack[t0].dst == moves[k].y) mine.push_back(unpack[t0++]);
+      run_tasks(mine, moves[k].m->elem, false, s);
+    }
+  }
+}
+
 void move_forward(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const void* x, void* y,
                   cudaStream_t s, const RopeMove* rope = nullptr) {
   const int G = g.size(), me = g.index_of(ctx.rank);
+  if (G > 1 && !ctx.transport->peer_access()) {
+    move_forward_messages(ctx, g, {{&m, x, y, rope}}, s);  // counts the move itself
+    return;
+  }
   int64_t sent = 0;
   for (int j = 0; j < G; ++j)
     if (j != me) sent += m.bs * m.lloc * m.win[static_cast<size_t>(j)].n * m.elem;
@@ -436,48 +541,16 @@ void move_forward(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
     if (G > 1) ctx.transport->release(g, ctx.rank, s);
     return;
   }
-  // message path: pack per destination -> grouped send/recv -> unpack per source. A source
-  // whose rows land as one contiguous block of y (bs 1, one run of all its rows, this member's
-  // window spanning y's rows, no rotation: the natural Ulysses layout) is received in place.
-  const int64_t rows = m.bs * m.lloc;
-  std::vector<int64_t> soff(G + 1, 0), roff(G + 1, 0);
-  auto in_place = [&](int i) {
-    const auto& ri = m.runs[static_cast<size_t>(i)];
-    return !rope && m.bs == 1 && ri.size() == 1 && ri[0].row0 == 0 && ri[0].n == m.lloc && w.ycol == 0 &&
-           w.pad == 0 && yw == w.n;
-  };
-  for (int j = 0; j < G; ++j) soff[j + 1] = soff[j] + rows * m.win[static_cast<size_t>(j)].n;
-  for (int i = 0; i < G; ++i) roff[i + 1] = roff[i] + (in_place(i) ? 0 : rows * w.n);
-  DevBuf sbuf(static_cast<size_t>(soff[G] * m.elem), s), rbuf(static_cast<size_t>(roff[G] * m.elem), s);
-  std::vector<CopyTask> pack;
-  for (int j = 0; j < G; ++j) {
-    const Window& wj = m.win[static_cast<size_t>(j)];
-    if (wj.n == 0) continue;
-    pack.push_back({x, static_cast<char*>(sbuf.p) + soff[j] * m.elem, m.xw, wj.n, 0, 0, wj.xcol, 0,
-                    rows, wj.n, 0});
-    if (rope) set_rope(pack.back(), rope->table, 0, m.lloc, rope->dim, rope->sign);
+}
+
+// Several forward moves over one group: one grouped exchange on the message path, one move at
+// a time on the peer-read path (each already a single copy pass).
+void move_forward_many(RankCtx& ctx, const CommGroup& g, const std::vector<FwdMove>& moves, cudaStream_t s) {
+  if (g.size() > 1 && !ctx.transport->peer_access() && !getenv("SPATTN_NO_GROUPED_MOVES")) {
+    move_forward_messages(ctx, g, moves, s);
+    return;
   }
-  run_tasks(pack, m.elem, false, s);
-  std::vector<Msg> sends, recvs;
-  for (int j = 0; j < G; ++j) {
-    sends.push_back({j, static_cast<char*>(sbuf.p) + soff[j] * m.elem,
-                     static_cast<size_t>((soff[j + 1] - soff[j]) * m.elem)});
-    if (in_place(j))
-      recvs.push_back({j, static_cast<char*>(y) + m.runs[static_cast<size_t>(j)][0].pos0 * yw * m.elem,
-                       static_cast<size_t>(rows * w.n * m.elem)});
-    else
-      recvs.push_back({j, static_cast<char*>(rbuf.p) + roff[j] * m.elem,
-                       static_cast<size_t>((roff[j + 1] - roff[j]) * m.elem)});
-  }
-  ctx.transport->send_recv(g, ctx.rank, sends, recvs, s);
-  std::vector<CopyTask> tasks;
-  for (int i = 0; i < G; ++i) {
-    if (w.n == 0 && w.pad == 0) continue;
-    if (in_place(i)) continue;
-    auto t = unpack(i, static_cast<char*>(rbuf.p) + roff[i] * m.elem, w.n, 0, nullptr);
-    tasks.insert(tasks.end(), t.begin(), t.end());
-  }
-  run_tasks(tasks, m.elem, false, s);
+  for (const FwdMove& mv : moves) move_forward(ctx, g, *mv.m, mv.x, mv.y, s, mv.rope);
 }
 
 void move_reverse(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const void* y, void* x,
@@ -567,6 +640,94 @@ void move_reverse(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const voi
     }
   }
   run_tasks(tasks, m.elem, add, s);
+}
+
+// One reverse move (head -> sequence shard, overwrite) of a tensor for the message path.
+struct RevMove {
+  const MoveSpec* m;
+  const void* y;
+  void* x;
+  const RopeMove* rope;
+};
+
+// Message path of several non-accumulating reverse moves over one group: each member packs,
+// per destination, its rows of that destination (contiguous blocks of the natural Ulysses
+// layout are sent in place), ONE grouped send/recv carries every move's messages (per peer in
+// move order), then each move unpacks (inverse RoPE rotates while unpacking).
+void move_reverse_messages(RankCtx& ctx, const CommGroup& g, const std::vector<RevMove>& moves, cudaStream_t s) {
+  const int G = g.size(), me = g.index_of(ctx.rank);
+  struct Plan {
+    std::vector<int64_t> roff;
+    std::vector<char> in_place;
+    DevBuf sbuf, rbuf;
+  };
+  std::vector<Plan> plans(moves.size());
+  std::vector<Msg> sends, recvs;
+  for (size_t k = 0; k < moves.size(); ++k) {
+    const MoveSpec& m = *moves[k].m;
+    Plan& pl = plans[k];
+    const Window& wm = m.win[static_cast<size_t>(me)];
+    ctx.count(Primitive::all_to_all, (G - 1) * m.bs * m.lloc * wm.n * m.elem);
+    const int64_t rows = m.bs * m.lloc, ywm = m.yw[static_cast<size_t>(me)];
+    pl.in_place.assign(G, 0);
+    for (int i = 0; i < G; ++i) {
+      const auto& ri = m.runs[static_cast<size_t>(i)];
+      pl.in_place[i] = m.bs == 1 && ri.size() == 1 && ri[0].row0 == 0 && ri[0].n == m.lloc && wm.ycol == 0 &&
+                       ywm == wm.n;
+    }
+    pl.sbuf = DevBuf(static_cast<size_t>(G * rows * wm.n * m.elem), s);
+    pl.roff.assign(G + 1, 0);
+    for (int j = 0; j < G; ++j) pl.roff[j + 1] = pl.roff[j] + rows * m.win[static_cast<size_t>(j)].n;
+    pl.rbuf = DevBuf(static_cast<size_t>(pl.roff[G] * m.elem), s);
+    std::vector<CopyTask> pack;
+    if (wm.n > 0)
+      for (int i = 0; i < G; ++i) {
+        if (pl.in_place[i]) continue;
+        char* dst = static_cast<char*>(pl.sbuf.p) + i * rows * wm.n * m.elem;
+        for (int64_t b = 0; b < m.bs; ++b)
+          for (const auto& r : m.runs[static_cast<size_t>(i)])
+            pack.push_back({moves[k].y, dst, ywm, wm.n, b * m.lg + r.pos0, b * m.lloc + r.row0, wm.ycol, 0, r.n,
+                            wm.n, 0});
+      }
+    run_tasks(pack, m.elem, false, s);
+  }
+  for (int i = 0; i < G; ++i)
+    for (size_t k = 0; k < moves.size(); ++k) {
+      const MoveSpec& m = *moves[k].m;
+      const Plan& pl = plans[k];
+      const Window& wm = m.win[static_cast<size_t>(me)];
+      const int64_t rows = m.bs * m.lloc, ywm = m.yw[static_cast<size_t>(me)];
+      char* src = pl.in_place[i] ? static_cast<char*>(const_cast<void*>(moves[k].y)) +
+                                      m.runs[static_cast<size_t>(i)][0].pos0 * ywm * m.elem
+                                : static_cast<char*>(pl.sbuf.p) + i * rows * wm.n * m.elem;
+      sends.push_back({i, src, static_cast<size_t>(rows * wm.n * m.elem)});
+      recvs.push_back({i, static_cast<char*>(pl.rbuf.p) + pl.roff[i] * m.elem,
+                       static_cast<size_t>((pl.roff[i + 1] - pl.roff[i]) * m.elem)});
+    }
+  ctx.transport->send_recv(g, ctx.rank, sends, recvs, s);
+  for (size_t k = 0; k < moves.size(); ++k) {
+    const MoveSpec& m = *moves[k].m;
+    const RopeMove* rope = moves[k].rope;
+    const Plan& pl = plans[k];
+    std::vector<CopyTask> tasks;
+    for (int j = 0; j < G; ++j) {
+      const Window& wj = m.win[static_cast<size_t>(j)];
+      if (wj.n == 0) continue;
+      tasks.push_back({static_cast<char*>(pl.rbuf.p) + pl.roff[j] * m.elem, moves[k].x, wj.n, m.xw, 0, 0, 0, wj.xcol,
+                       m.bs * m.lloc, wj.n, 0});
+      if (rope) set_rope(tasks.back(), rope->table, 0, m.lloc, rope->dim, rope->sign);
+    }
+    run_tasks(tasks, m.elem, false, s);
+  }
+}
+
+// Several non-accumulating reverse moves over one group (see move_forward_many).
+void move_reverse_many(RankCtx& ctx, const CommGroup& g, const std::vector<RevMove>& moves, cudaStream_t s) {
+  if (g.size() > 1 && !ctx.transport->peer_access() && !getenv("SPATTN_NO_GROUPED_MOVES")) {
+    move_reverse_messages(ctx, g, moves, s);
+    return;
+  }
+  for (const RevMove& mv : moves) move_reverse(ctx, g, *mv.m, mv.y, mv.x, false, s, mv.rope);
 }
 
 bool windows_overlap(const std::vector<Window>& w) {
@@ -1269,9 +1430,7 @@ SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig
   void* vg = keep(static_cast<size_t>(bs * lg * nkv * d * 2));
   void* og = keep(static_cast<size_t>(bs * lg * nq * d * 2));
   float* glse = static_cast<float*>(keep(static_cast<size_t>(bs * lg * nq * 4)));
-  move_forward(ctx, inner, mq, qd, qg, s, rfwd);
-  move_forward(ctx, inner, mkv, kd, kg, s, rfwd);
-  move_forward(ctx, inner, mkv, v.data, vg, s);
+  move_forward_many(ctx, inner, {{&mq, qd, qg, rfwd}, {&mkv, kd, kg, rfwd}, {&mkv, v.data, vg, nullptr}}, s);
   Local Lc{qg, kg, vg, bs * lg, nq * d, nkv * d,
            {nq, nkv, hp.qlo[static_cast<size_t>(iota)], hp.kvlo[static_cast<size_t>(iota)], rep}};
   if (engine == Engine::usp && r > 1) {
@@ -1456,16 +1615,16 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& S, const DeviceTens
   // the inverse rotation of dq/dk rides the head->sequence copy back (rope.cu)
   const RopeMove rinv{S.rope_table, d, -1};
   const RopeMove* rbwd = S.rope_table ? &rinv : nullptr;
-  move_reverse(ctx, inner, mq, dqg.p, dq.data, false, s, rbwd);
   const int64_t rows = bs * lloc;
   if (!kv_overlap) {
     if (!direct) {
       spattn::launch_f32_to_bf16(dkg.p, dka.as<float>(), 1.f, bs * lg * nkv * d, s);
       spattn::launch_f32_to_bf16(dvg.p, dva.as<float>(), 1.f, bs * lg * nkv * d, s);
     }
-    move_reverse(ctx, inner, mkv, dkg.p, dk.data, false, s, rbwd);
-    move_reverse(ctx, inner, mkv, dvg.p, dv.data, false, s);
+    move_reverse_many(ctx, inner, {{&mq, dqg.p, dq.data, rbwd}, {&mkv, dkg.p, dk.data, rbwd},
+                                   {&mkv, dvg.p, dv.data, nullptr}}, s);
   } else {
+    move_reverse(ctx, inner, mq, dqg.p, dq.data, false, s, rbwd);
     // kv heads shared by members (Hkv % u != 0): sum fp32 partials (repeat_heads backward)
     MoveSpec mk4 = head_move(hp, true, bs, lloc, Hkv, d, S.inner_runs, 4);
     DevBuf dkf(static_cast<size_t>(rows * Hkv * d * 4), s), dvf(static_cast<size_t>(rows * Hkv * d * 4), s);
