@@ -422,7 +422,7 @@ void move_forward_messages(RankCtx& ctx, const CommGroup& g, const std::vector<F
     DevBuf sbuf, rbuf;
   };
   std::vector<Plan> plans(moves.size());
-  std::vector<CopyTask> pack_plain, unpack;
+  std::vector<CopyTask> pack_plain, pack_rope, unpack;
   int elem = 0;
   bool same_elem = true;
   for (size_t k = 0; k < moves.size(); ++k) {
@@ -460,8 +460,10 @@ void move_forward_messages(RankCtx& ctx, const CommGroup& g, const std::vector<F
                       0, rows, wj.n, 0});
       if (rope) set_rope(pack.back(), rope->table, 0, m.lloc, rope->dim, rope->sign);
     }
-    if (rope || !same_elem)
-      run_tasks(pack, m.elem, false, s);  // rotating packs run the RoPE copier
+    if (!same_elem)
+      run_tasks(pack, m.elem, false, s);
+    else if (rope)  // rotating packs share one launch of the RoPE copier
+      pack_rope.insert(pack_rope.end(), pack.begin(), pack.end());
     else
       pack_plain.insert(pack_plain.end(), pack.begin(), pack.end());
     for (int i = 0; i < G; ++i) {
@@ -472,6 +474,7 @@ void move_forward_messages(RankCtx& ctx, const CommGroup& g, const std::vector<F
                             b * m.lloc + r.row0, b * m.lg + r.pos0, 0, w.ycol, r.n, w.n, w.pad});
     }
   }
+  run_tasks(pack_rope, elem, false, s);
   run_tasks(pack_plain, elem, false, s);
   std::vector<Msg> sends, recvs;
   for (int j = 0; j < G; ++j)
