@@ -708,6 +708,9 @@ void move_reverse_messages(RankCtx& ctx, const CommGroup& g, const std::vector<R
                        static_cast<size_t>((pl.roff[i + 1] - pl.roff[i]) * m.elem)});
     }
   ctx.transport->send_recv(g, ctx.rank, sends, recvs, s);
+  // unpacks: rotating ones share one launch, plain ones another (per element size)
+  std::vector<CopyTask> un_rope, un_plain;
+  int elem = moves.empty() ? 2 : moves[0].m->elem;
   for (size_t k = 0; k < moves.size(); ++k) {
     const MoveSpec& m = *moves[k].m;
     const RopeMove* rope = moves[k].rope;
@@ -720,8 +723,15 @@ void move_reverse_messages(RankCtx& ctx, const CommGroup& g, const std::vector<R
                        m.bs * m.lloc, wj.n, 0});
       if (rope) set_rope(tasks.back(), rope->table, 0, m.lloc, rope->dim, rope->sign);
     }
-    run_tasks(tasks, m.elem, false, s);
+    if (m.elem != elem) {
+      run_tasks(tasks, m.elem, false, s);
+      continue;
+    }
+    auto& dst = rope ? un_rope : un_plain;
+    dst.insert(dst.end(), tasks.begin(), tasks.end());
   }
+  run_tasks(un_rope, elem, false, s);
+  run_tasks(un_plain, elem, false, s);
 }
 
 // Several non-accumulating reverse moves over one group (see move_forward_many).
