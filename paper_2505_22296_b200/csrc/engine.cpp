@@ -1461,9 +1461,8 @@ SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig
     ctx.add_flops(4 * d * pairs * nq);
     plain_forward(ctx, Lc, d, S->plain_probs, og, glse);
   }
-  move_reverse(ctx, inner, mq, og, out.data, false, s);
   MoveSpec ml = head_move(hp, false, bs, lloc, H, d, runs, 4, 1);
-  move_reverse(ctx, inner, ml, glse, lse_local, false, s);
+  move_reverse_many(ctx, inner, {{&mq, og, out.data, nullptr}, {&ml, glse, lse_local, nullptr}}, s);
   S->rq = qg, S->rk = kg, S->rv = vg, S->ro = og;
   S->lse = glse;
   S->rrows = bs * lg;
