@@ -67,7 +67,7 @@ class Clocks:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                 "--format=csv,noheader,nounits", "-lms", "25"], stdout=self.f,
                 stderr=subprocess.DEVNULL)
             time.sleep(0.3)
         return self
@@ -92,7 +92,8 @@ class Clocks:
         mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
-        loaded = sorted(sm)[len(sm) // 4:] if len(sm) > 4 else sm
+        # samples every 25 ms over the barrier + timed steps; the first one precedes the load
+        loaded = sm[1:] if len(sm) > 2 else sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(rows)}
