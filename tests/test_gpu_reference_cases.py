@@ -128,10 +128,12 @@ def test_rank_all_to_all_matches_fabric_driver(P):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("engine,sp", [("ulysses", 2), ("ring", 2), ("dummy_head", 4)])
-def test_batched_varlen_with_rope(P, engine, sp):
+@pytest.mark.parametrize("engine,sp,messages", [("ulysses", 2, False), ("ring", 2, False), ("dummy_head", 4, False),
+                                                ("ulysses", 2, True), ("dummy_head", 4, True)])
+def test_batched_varlen_with_rope(P, engine, sp, messages):
     """bs=2 neat-packed batches (the same document cut for every batch entry) with RoPE at
-    per-document reset ids, against the composed per-document oracle."""
+    per-document reset ids, against the composed per-document oracle; with ``messages`` the
+    grouped q|k|v / dq|dk|dv exchanges carry rotated, staged (bs=2) blocks."""
     import seqpar_oracle as O
 
     docs = [100, 60, 96]
@@ -139,7 +141,8 @@ def test_batched_varlen_with_rope(P, engine, sp):
     H = 6 if engine == "dummy_head" else 4
     q, k, v, R = parity_inputs(81 + sp, L, H, 2, 64, bs=2)
     ids = P.document_position_ids(docs)
-    res = run(P, engine, q, k, v, R, sp, docs=docs, position_ids=ids)
+    res = run(P, engine, q, k, v, R, sp, docs=docs, position_ids=ids,
+              **(dict(force_messages=True) if messages else {}))
     qr, kr = O.rope_apply(q, ids), O.rope_apply(k, ids)
     orc = O.varlen_attention_fwd_bwd(qr, kr, v, R, docs)
     orc["dq"] = O.rope_apply(orc["dq"], ids, inverse=True)
