@@ -1,10 +1,12 @@
 #!/usr/bin/env python
 """SP attention fwd+bwd throughput (BASELINE.json metric) on B200.
 
-Workload (BASELINE.json configs[1]): Llama-3-8B attention shape — 32 Q / 8 KV heads, head_dim
-128, causal, seq 32768, bs 1 — as Ulysses SP=N over N GPUs (one process per GPU, NCCL). At
-N=1 the layer degenerates to the single-GPU attention kernel pair (Ulysses at sp=1).
-A step = one forward + one backward of the layer over the whole sequence (all ranks).
+Headline workload (BASELINE.json configs[3], the largest config that fits one GPU and the one
+north_star quotes its 128K scaling target on): Llama-3-8B attention shape — 32 Q / 8 KV heads,
+head_dim 128, causal, seq 131072, bs 1 — as zigzag Ring SP=N over N GPUs (one process per GPU,
+NCCL). At N=1 the layer degenerates to the single-GPU attention kernel pair. A step = one
+forward + one backward of the layer over the whole sequence (all ranks). The line also carries
+`secondary` measurements: Ulysses at the same 128K shape and c2 (32K, Ulysses).
 
   python bench.py [--gpus N --steps K --warmup W]           # our arm
   python bench.py --impl reference [...]                    # reference CPU arm (oracle/_ref)
@@ -100,7 +102,7 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------- CPU baseline
-def cpu_reference_sample(heads, kv, d, L, threads=None):
+def cpu_reference_sample(heads, kv, d, L, threads=None, engine="ulysses"):
     """Time the UNMODIFIED reference (oracle/_ref/ref_driver, built from /root/reference by
     oracle/Makefile) on a bounded sample of the workload: same head_dim and GQA ratio, 8 query
     heads, seq 4096, Ulysses over `threads` rank threads (comm.cpp:197-222); extrapolated to the
@@ -114,7 +116,7 @@ def cpu_reference_sample(heads, kv, d, L, threads=None):
     s_heads, s_kv, s_L = 8, max(1, 8 * kv // heads), 4096
     drv = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
     if os.path.exists(drv):
-        out = subprocess.run([drv, "bench", "ulysses", str(sp), str(s_L), str(s_heads), str(s_kv),
+        out = subprocess.run([drv, "bench", engine, str(sp), str(s_L), str(s_heads), str(s_kv),
                               str(d), "1"], capture_output=True, text=True, check=True)
         rec = json.loads(out.stdout.strip().splitlines()[-1])
         secs, kind = rec["s_per_step"], "reference"
@@ -131,9 +133,10 @@ def cpu_reference_sample(heads, kv, d, L, threads=None):
     work_full = causal_pairs(L) * heads
     t_full = secs * work_full / work_sample
     return {"value": L / t_full, "unit": "tokens/s", "cores": sp, "kind": kind,
-            "sample": f"ulysses fwd+bwd, {s_heads}q/{s_kv}kv heads, d={d}, L={s_L}, {sp} rank "
-                      f"threads: {secs:.2f} s; extrapolated x{work_full / work_sample:.1f} by "
-                      f"causal pairs x heads to L={L}, {heads} heads",
+            "extrapolated": True,
+            "sample": f"EXTRAPOLATED: {engine if kind == 'reference' else 'oracle'} fwd+bwd, {s_heads}q/{s_kv}kv heads, d={d}, L={s_L}, "
+                      f"{sp} rank threads: {secs:.2f} s measured; scaled x{work_full / work_sample:.1f} "
+                      f"by causal pairs x heads to L={L}, {heads} heads",
             "sample_seconds": secs}
 
 
@@ -144,14 +147,19 @@ def run_reference(args, cfg):
         return
     vals, samples = [], []
     if args.warmup > 0:  # one untimed sample warms the page cache and the CPU frequency
-        cpu_reference_sample(heads, kv, d, L)
+        cpu_reference_sample(heads, kv, d, L, engine=engine)
     for _ in range(args.steps):
-        r = cpu_reference_sample(heads, kv, d, L)
+        r = cpu_reference_sample(heads, kv, d, L, engine=engine)
         vals.append(r["value"])
         samples.append(r)
     v = statistics.median(vals)
+    # ms_per_step is the wall time of one timed sample (what this run actually spent per step);
+    # value is that sample's throughput extrapolated to the full workload (exact causal pairs x
+    # heads), since a full-size CPU step would take hours
+    sample_ms = 1000.0 * statistics.median(r["sample_seconds"] for r in samples)
     line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * L / v,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sample_ms,
+            "extrapolated": {"from": samples[-1]["sample"], "full_step_ms": 1000.0 * L / v},
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference Rng uniform(-2,2))", "impl": "reference",
             "config": {"workload": f"{cfg}: {heads}q/{kv}kv heads d={d} seq {L} causal, bs 1",
@@ -170,7 +178,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--engine", default=None)
     ap.add_argument("--seq-len", type=int, default=None)
     ap.add_argument("--family", default="tcgen05", choices=["tcgen05", "mma", "tcgen05_pp", "tcgen05_pair"])
@@ -302,6 +311,55 @@ def main():
                 "d2h_bytes_per_step": d2h, "ms_per_step": ems,
                 "api": "spattn_step_host (C ABI, pinned host buffers)", "head_groups": groups}
 
+    def secondary(name, sh, sk, sd, sL, seng):
+        """The same device-timed fwd+bwd step for another workload on this context (fewer
+        steps): tokens/s and the attention kernels' TFLOP/s."""
+        smode = "zigzag" if seng == "ring" else "naive"
+        slay = C.make_layout(smode, sL, sp)
+        scfg = C.make_config(sh, sk, sd, True)
+        sl = sL // sp
+        mk2 = lambda h: torch.randn(1, sl, h, sd, device="cuda", dtype=torch.bfloat16, generator=g)  # noqa
+        t = [mk2(sh), mk2(sk), mk2(sk), mk2(sh)]
+        o2, q2g, k2g, v2g = (torch.empty_like(x) for x in (t[0], t[0], t[1], t[2]))
+        l2 = torch.empty(1, sl, sh, device="cuda", dtype=torch.float32)
+        sid = C.engine_id(seng)
+
+        def st():
+            saved = ctypes.c_void_p()
+            C.check(C.lib().spattn_fwd(ctx, sid, ctypes.byref(scfg), ctypes.byref(slay), 1, t[0].data_ptr(),
+                                       t[1].data_ptr(), t[2].data_ptr(), o2.data_ptr(), l2.data_ptr(), None,
+                                       0, ctypes.byref(saved)))
+            C.check(C.lib().spattn_bwd(ctx, saved, t[3].data_ptr(), q2g.data_ptr(), k2g.data_ptr(),
+                                       v2g.data_ptr()))
+            C.lib().spattn_saved_free(saved)
+
+        n = max(3, min(args.steps, 5))
+        for _ in range(max(3, min(args.warmup, 3))):
+            st()
+        barrier()
+        ev0.record(stream)
+        for _ in range(n):
+            st()
+        ev1.record(stream)
+        barrier()
+        sms = max_over_ranks(ev0.elapsed_time(ev1)) / n
+        del t, o2, q2g, k2g, v2g, l2
+        torch.cuda.empty_cache()
+        return {"workload": f"{name}: {sh}q/{sk}kv heads d={sd} seq {sL} causal bs 1", "engine": seng,
+                "parallelism": f"sp{sp}", "value": sL / (sms / 1e3), "unit": "tokens/s", "ms_per_step": sms,
+                "steps": n, "layer_tflops": 14 * sd * causal_pairs(sL) * sh / (sms / 1e3) / 1e12}
+
+    sec = []
+    if not args.no_secondary and args.seq_len is None:
+        try:
+            if args.config == "c4" and engine == "ring":
+                sec.append(secondary("c4/ulysses", heads, kv, d, L, "ulysses"))
+            if args.config != "c2":
+                h2, k2, d2, L2, e2 = CONFIGS["c2"]
+                sec.append(secondary("c2", h2, k2, d2, L2, e2))
+        except Exception as ex:  # noqa: BLE001
+            sec.append({"error": str(ex)[:200]})
+
     # the metric's second half at N>1: all-to-all NVLink GB/s of this library's collective
     # (one q-shaped sequence->head exchange, send-side bytes per rank / device time, max over ranks)
     comm = None
@@ -385,14 +443,17 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
+    if sec:
+        line["secondary"] = sec
     if e2e:
         line["e2e"] = e2e
     if comm:
         line["comm"] = comm
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_reference_sample(heads, kv, d, L)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cb = cpu_reference_sample(heads, kv, d, L, engine=engine)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                       "extrapolated")}
         except Exception as ex:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "error": str(ex)}
     print(json.dumps(line), flush=True)

@@ -124,6 +124,11 @@ void all_to_all(RankCtx& ctx, const CommGroup& group, const void* local, int64_t
 // as one all_gather of local_bytes * (G - 1).
 void all_gather(RankCtx& ctx, const CommGroup& group, const void* local, int64_t outer, int64_t extent,
                 int64_t inner_bytes, void* out);
+// Backward exchange of all_gather (comm.cpp:415-443): parts [G, outer, extent, inner_bytes],
+// part j = member j's gathered gradient at this member's block (the caller tree-sums them in
+// group order). Counted as a second all_gather of local_bytes * (G - 1) (comm.cpp:418-420).
+void all_gather_backward(RankCtx& ctx, const CommGroup& group, const void* grad_gathered, int64_t outer,
+                         int64_t extent, int64_t inner_bytes, void* parts);
 
 // Reference ring_shift (comm.cpp:449-460): group index i receives the payload of index i-1
 // (`bytes` on every member). Counted as one p2p of `bytes` (0 for a single member).

@@ -232,6 +232,12 @@ int spattn_all_to_all(spattn_ctx* ctx, const void* local, void* out, int64_t bs,
  * sizes. Counted as all_gather of local_bytes*(G-1). */
 int spattn_all_gather(spattn_ctx* ctx, const void* local, void* out, int64_t outer, int64_t extent,
                       int64_t inner_bytes);
+/* all_gather backward exchange (comm.cpp:415-443): gathered [outer, G*extent, inner_bytes]
+ * gradient in; parts [G, outer, extent, inner_bytes] out, part j = member j's gradient at this
+ * member's block (the caller tree-sums the parts in group order). Counted, as the reference
+ * counts it (comm.cpp:418-420), as a second all_gather of local_bytes*(G-1). */
+int spattn_all_gather_backward(spattn_ctx* ctx, const void* grad_gathered, void* parts, int64_t outer,
+                               int64_t extent, int64_t inner_bytes);
 /* ring_shift (comm.hpp:140, comm.cpp:449-460): group index i receives index i-1's payload of
  * `bytes` into out. Counted as one p2p of `bytes` (0 for a single member). */
 int spattn_ring_shift(spattn_ctx* ctx, const void* payload, void* out, int64_t bytes);

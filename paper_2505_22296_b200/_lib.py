@@ -35,7 +35,7 @@ EXPORTS = [
     "spattn_fabric_replicate_packing_mask", "spattn_logprob_fwd", "spattn_logprob_bwd",
     "spattn_exact_sum_device", "spattn_exact_sum_host", "spattn_exact_merge", "spattn_exact_round",
     "spattn_exact_sum_all_reduce", "spattn_all_reduce_count", "spattn_all_reduce_values",
-    "spattn_all_to_all", "spattn_all_gather", "spattn_ring_shift",
+    "spattn_all_to_all", "spattn_all_gather", "spattn_all_gather_backward", "spattn_ring_shift",
 ]
 
 
@@ -145,6 +145,7 @@ def lib() -> ctypes.CDLL:
                               ctypes.POINTER(_vp), ctypes.POINTER(_vp)],
         "spattn_all_to_all": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _i32],
         "spattn_all_gather": [_vp, _vp, _vp, _i64, _i64, _i64],
+        "spattn_all_gather_backward": [_vp, _vp, _vp, _i64, _i64, _i64],
         "spattn_ring_shift": [_vp, _vp, _vp, _i64],
         "spattn_fabric_all_to_all": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, _i64,
                                      _i64, _i64, _i32, _i32, _i32],

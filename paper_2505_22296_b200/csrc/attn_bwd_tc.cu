@@ -129,11 +129,18 @@ __device__ __forceinline__ void grad_chunk(const uint32_t (&rs)[32], const uint3
   }
 }
 
-// SV: variant bits (A/B builds, SPATTN_BWD_SV; default 64): 64 dS^T also stored to TMEM so dK
-// is a TS MMA (2300 -> 2245 cycles per iteration); 1 prefetch chunk 1's TMEM loads, 2 packed
-// fp32x2 math, 4 separate full / masked code paths, 8 FMA-pipe exp2 for 1 pair in 4 (each
-// measured no faster than the scalar loop)
-template <int SV>
+// SV: variant bits of the softmax-gradient code (fixed at 64: dS^T also stored to TMEM so dK is
+// a TS MMA, 2300 -> 2245 cycles per iteration). Measured no faster and removed from the build:
+// 1 prefetch chunk 1's TMEM loads, 2 packed fp32x2 math, 4 separate full / masked code paths,
+// 8 FMA-pipe exp2 for 1 pair in 4.
+constexpr int SV = 64;
+// Profiling switches (wrong results by design) exist only in -DSPATTN_PROFILING builds.
+#ifdef SPATTN_PROFILING
+#define BWD_DBG(bit) ((a.debug & (bit)) != 0)
+#else
+#define BWD_DBG(bit) false
+#endif
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_bwd_tc_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int warp = threadIdx.x / 32;
   long long* trace = (a.trace && blockIdx.x == 0) ? a.trace : nullptr;
   // debug bit 4: record only the iteration-start event (minimal perturbation)
-  const bool tr_all = !(a.debug & 4);
+  const bool tr_all = !BWD_DBG(4);
 #define TR(slot, it) \
   if (trace && (tr_all || (slot) == 0)) trace[(it) * 16 + (slot)] = clock64()
   // 1-D grid, kv head fastest: the heaviest causal key tiles of every head run first (LPT)
@@ -162,11 +169,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // resident CTAs then reduce into one kv head's dQ rows (64 MB at c2) instead of all of them
   // (512 MB), which keeps the fp32 dQ partial sums L2-resident (measured 22.3 -> 21.4 ms at c2).
   // debug bit 8 restores the tile-major order for A/B runs.
-  const bool head_major = !(a.debug & 8);
+  const bool head_major = !BWD_DBG(8);
   const int tile = head_major ? blockIdx.x % ntiles : blockIdx.x / hm.hkv;
   const int kvh = head_major ? blockIdx.x / ntiles : blockIdx.x % hm.hkv;
-  int pi = 0;
-  while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= tile) ++pi;
+  const int pi = find_problem(ps, tile);
   const AttnProblem P = ps.p[pi];
   const int n0 = (tile - ps.tile_prefix[pi]) * 128;
   const int g_lo = (kvh + hm.kv_head_base) * hm.rep;
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         tc::commit(bar(E_SF + b));
         TR(2, it);
-        if (it >= 2 && !(a.debug & 64)) {  // dQ^T of it-2 (same columns) must be drained (debug 64: skip, wrong dq)
+        if (it >= 2 && !BWD_DBG(64)) {  // dQ^T of it-2 (same columns) must be drained (debug 64: skip, wrong dq)
           tc::mbar_wait(bar(E_DQF + b), ((it - 2) >> 1) & 1);
           tc::fence_after();
         }
@@ -377,7 +383,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if constexpr ((SV & 64) != 0) tc::tmem_st16(tmem + lane_base + 64 * b + 32, wds);
         }
         uint32_t wp[16], wd[16];
-        if (a.debug & 16) {  // profiling: no softmax-gradient math (wrong results)
+        if (BWD_DBG(16)) {  // profiling: no softmax-gradient math (wrong results)
 #pragma unroll
           for (int i = 0; i < 16; ++i) wp[i] = rs[cc][i] ^ rp[cc][i], wd[i] = rs[cc][i + 16] ^ rp[cc][i + 16];
         } else if ((SV & 4) && full) {
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // (per-lane red.global.add.f32 from registers measured 1.8x slower than this staging, and
       // a quad-transpose via shuffles + red.global.add.v4.f32 1.6x slower: 3620 vs 2229 cycles
       // per iteration — the L2 atomics, not the smem traffic, would bound it)
-      if (a.debug & 32) continue;  // profiling: no dQ staging / reduce (wrong dq)
+      if (BWD_DBG(32)) continue;  // profiling: no dQ staging / reduce (wrong dq)
       const uint32_t stg = stg0 + (it % NSTG) * 8192;
       if (lane == 0) tc::bulk_wait_read<NSTG - 1>();  // the slot's previous reduce has read it
       __syncwarp();
@@ -472,7 +478,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       tc::fence_proxy_async();
       __syncwarp();
-      if (lane == 0 && !(a.debug & 1)) {
+      if (lane == 0 && !BWD_DBG(1)) {
         tc::tma_reduce_add_2d(&tmDQ, stg, h * D + w * 32, P.q_row0 + m0);
         tc::bulk_commit();
       }
@@ -534,9 +540,12 @@ bool tc_bwd_q64_supported(const BwdArgs& a) {
 
 void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
   ProblemSet ps = in;
-  static const int dbg = getenv("SPATTN_DEBUG") ? atoi(getenv("SPATTN_DEBUG")) : 0;
   BwdArgs args = a;
-  args.debug = dbg;
+#ifdef SPATTN_PROFILING
+  args.debug = getenv("SPATTN_DEBUG") ? atoi(getenv("SPATTN_DEBUG")) : 0;
+#else
+  args.debug = 0;
+#endif
   args.trace = g_bwd_trace;
   ps.tile_prefix[0] = 0;
   for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nk + 127) / 128;
@@ -547,26 +556,10 @@ void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t
   const uint64_t qrows = max(1, max_rows(ps, true)), krows = max(1, max_rows(ps, false));
   if (!make_tma_2d(&tq, a.q, qw, qrows, qw, BQ) || !make_tma_2d(&tk, a.k, kw, krows, kw, 128) ||
       !make_tma_2d(&tv, a.v, kw, krows, kw, 128) || !make_tma_2d(&tdo, a.dout, qw, qrows, qw, BQ) ||
-      !make_tma_2d_f32(&tdq, a.dq_acc, (uint64_t)a.hm.hq * D, qrows, (uint64_t)a.dq_row_stride, BQ)) {
-    cudaGetLastError();
-    return;
-  }
-  static const int sv = getenv("SPATTN_BWD_SV") ? atoi(getenv("SPATTN_BWD_SV")) : 64;
-  auto launch = [&](auto kern) {
-    static std::once_flag once;
-    std::call_once(once, [&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM); });
-    kern<<<dim3(tiles * a.hm.hkv), NTHREADS, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
-  };
-  switch (sv) {
-    case 0: launch(attn_bwd_tc_q64_kernel<0>); break;
-    case 1: launch(attn_bwd_tc_q64_kernel<1>); break;
-    case 3: launch(attn_bwd_tc_q64_kernel<3>); break;
-    case 7: launch(attn_bwd_tc_q64_kernel<7>); break;
-    case 15: launch(attn_bwd_tc_q64_kernel<15>); break;
-    case 11: launch(attn_bwd_tc_q64_kernel<11>); break;
-    case 64: launch(attn_bwd_tc_q64_kernel<64>); break;
-    default: launch(attn_bwd_tc_q64_kernel<64>); break;
-  }
+      !make_tma_2d_f32(&tdq, a.dq_acc, (uint64_t)a.hm.hq * D, qrows, (uint64_t)a.dq_row_stride, BQ))
+    launch_error("attn_bwd_tc_q64", "TMA descriptor encode failed (q/k/v/dout/dq base, strides or extents)");
+  ensure_smem_for(attn_bwd_tc_q64_kernel, SMEM);
+  attn_bwd_tc_q64_kernel<<<dim3(tiles * a.hm.hkv), NTHREADS, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
   note_launch();
 }
 

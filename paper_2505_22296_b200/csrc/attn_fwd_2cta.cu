@@ -66,8 +66,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(352, 1)
   const int warp = threadIdx.x / 32;
   // ---- pair decode (heavy causal pairs first; one head's pairs run together)
   const int pair = blockIdx.x >> 1;
-  int pi = 0;
-  while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= pair) ++pi;
+  const int pi = find_problem(ps, pair);
   const AttnProblem P = ps.p[pi];
   int mt = pair - ps.tile_prefix[pi];
   if (P.causal) mt = (ps.tile_prefix[pi + 1] - ps.tile_prefix[pi]) - 1 - mt;
@@ -359,7 +358,7 @@ int max_rows2(const ProblemSet& ps, bool q) {
 bool tc_fwd_pair_supported(const FwdArgs& a) {
   auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
   return a.d == D && al(a.q) && al(a.k) && al(a.v) && (a.q_row_stride * 2) % 16 == 0 &&
-         (a.kv_row_stride * 2) % 16 == 0 && !getenv("SPATTN_FWD_1CTA");
+         (a.kv_row_stride * 2) % 16 == 0;
 }
 
 void launch_attn_fwd_pair(const FwdArgs& a, const ProblemSet& in, cudaStream_t s) {
@@ -372,12 +371,9 @@ void launch_attn_fwd_pair(const FwdArgs& a, const ProblemSet& in, cudaStream_t s
   const uint64_t qw = (uint64_t)a.q_row_stride, kw = (uint64_t)a.kv_row_stride;
   const uint64_t krows = max(1, max_rows2(ps, false));
   if (!make_tma_2d(&tq, a.q, qw, max_rows2(ps, true), qw, 128) || !make_tma_2d(&tk, a.k, kw, krows, kw, 64) ||
-      !make_tma_2d(&tv, a.v, kw, krows, kw, 128)) {
-    cudaGetLastError();
-    return;
-  }
-  static std::once_flag once;
-  std::call_once(once, [] { cudaFuncSetAttribute(attn_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM); });
+      !make_tma_2d(&tv, a.v, kw, krows, kw, 128))
+    launch_error("attn_fwd_pair", "TMA descriptor encode failed");
+  ensure_smem_for(attn_fwd_pair_kernel, SMEM);
   attn_fwd_pair_kernel<<<dim3(2 * pairs, a.hm.hq), 352, SMEM, s>>>(tq, tk, tv, a, ps);
   note_launch();
 }

@@ -81,8 +81,7 @@ __global__ void __launch_bounds__(352, 1)
   const int warp = threadIdx.x / 32;
 
   // ---- tile decode: heavy causal tiles first, one head's tiles together (K/V reuse in L2)
-  int pi = 0;
-  while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= (int)blockIdx.x) ++pi;
+  const int pi = find_problem(ps, (int)blockIdx.x);
   const AttnProblem P = ps.p[pi];
   int mt = blockIdx.x - ps.tile_prefix[pi];
   if (P.causal) mt = (ps.tile_prefix[pi + 1] - ps.tile_prefix[pi]) - 1 - mt;
@@ -407,15 +406,9 @@ void launch_pp_d(const FwdArgs& a, const ProblemSet& in, cudaStream_t s) {
   const uint64_t qw = (uint64_t)a.q_row_stride, kw = (uint64_t)a.kv_row_stride;
   if (!make_tma_2d(&tq, a.q, qw, max_rows_pp(ps, true), qw, 128) ||
       !make_tma_2d(&tk, a.k, kw, max(1, max_rows_pp(ps, false)), kw, 128) ||
-      !make_tma_2d(&tv, a.v, kw, max(1, max_rows_pp(ps, false)), kw, 128)) {
-    cudaGetLastError();
-    return;
-  }
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(attn_fwd_pp_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         PPLayout<D>::SMEM);
-  });
+      !make_tma_2d(&tv, a.v, kw, max(1, max_rows_pp(ps, false)), kw, 128))
+    launch_error("attn_fwd_pp", "TMA descriptor encode failed");
+  ensure_smem_for(attn_fwd_pp_kernel<D>, PPLayout<D>::SMEM);
   attn_fwd_pp_kernel<D><<<dim3(tiles, a.hm.hq), 352, PPLayout<D>::SMEM, s>>>(tq, tk, tv, a, ps);
   note_launch();
 }

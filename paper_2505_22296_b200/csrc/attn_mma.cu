@@ -20,12 +20,6 @@ constexpr int kBM = 64;   // query rows per CTA tile (4 warps x 16)
 constexpr int kBN = 64;   // key rows per tile
 constexpr int kThreads = 128;
 
-__device__ __forceinline__ int find_problem(const ProblemSet& ps, int tile) {
-  int pi = 0;
-  while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= tile) ++pi;
-  return pi;
-}
-
 template <int D>
 __device__ __forceinline__ void load_tile(uint32_t sbase, const __nv_bfloat16* g, int64_t stride,
                                           int rows_valid, int tid) {
@@ -514,12 +508,7 @@ void launch_attn_fwd_mma(const FwdArgs& a, const ProblemSet& in, cudaStream_t s)
     note_launch();
   } else {
     const int sm = 5 * kBN * 128 * 2;
-    static bool once = [] {
-      cudaFuncSetAttribute(attn_fwd_mma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           5 * kBN * 128 * 2);
-      return true;
-    }();
-    (void)once;
+    ensure_smem_for(attn_fwd_mma<128>, sm);
     attn_fwd_mma<128><<<grid, kThreads, sm, s>>>(a, ps);
     note_launch();
   }
@@ -582,11 +571,7 @@ void launch_attn_bwd_mma(const BwdArgs& a, const ProblemSet& in, cudaStream_t s)
     note_launch();
   } else {
     const int sm = 4 * kBN * 128 * 2 + kBN * kBM * 2 + 2 * kBM * 4;
-    static bool once = [sm] {
-      cudaFuncSetAttribute(attn_bwd_mma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      return true;
-    }();
-    (void)once;
+    ensure_smem_for(attn_bwd_mma<128>, sm);
     attn_bwd_mma<128><<<grid, kThreads, sm, s>>>(a, ps);
     note_launch();
   }

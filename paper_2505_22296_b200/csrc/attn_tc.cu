@@ -5,6 +5,9 @@
 #include <cstdlib>
 #include <mutex>
 
+#include <set>
+#include <stdexcept>
+#include <string>
 #include "tc.cuh"
 
 namespace spattn {
@@ -27,6 +30,23 @@ EncodeFn encode_fn() {
   return fn;
 }
 }  // namespace
+
+void launch_error(const char* kernel, const char* what) {
+  cudaGetLastError();
+  throw std::runtime_error(std::string(kernel) + ": " + what);
+}
+
+void ensure_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) launch_error("ensure_smem", "cudaGetDevice failed");
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({kernel, dev})) return;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    launch_error("ensure_smem", "cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed");
+  done.insert({kernel, dev});
+}
 
 bool make_tma_2d(CUtensorMap* m, const void* base, uint64_t width, uint64_t rows,
                  uint64_t row_stride_elems, uint32_t box_rows) {
@@ -253,8 +273,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   const int warp = threadIdx.x / 32;
   // ---- tile decode (heavy causal tiles first; one head's tiles run together, sharing K/V in L2)
-  int pi = 0;
-  while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= (int)blockIdx.x) ++pi;
+  const int pi = find_problem(ps, (int)blockIdx.x);
   const AttnProblem P = ps.p[pi];
   int mt = blockIdx.x - ps.tile_prefix[pi];
   if (P.causal) mt = (ps.tile_prefix[pi + 1] - ps.tile_prefix[pi]) - 1 - mt;
@@ -648,15 +667,9 @@ void launch_fwd_tc_d(const FwdArgs& a, const ProblemSet& in, cudaStream_t s) {
   const uint64_t qw = (uint64_t)a.q_row_stride, kw = (uint64_t)a.kv_row_stride;
   if (!make_tma_2d(&tq, a.q, qw, max_rows(ps, true), qw, 128) ||
       !make_tma_2d(&tk, a.k, kw, max(1, max_rows(ps, false)), kw, 128) ||
-      !make_tma_2d(&tv, a.v, kw, max(1, max_rows(ps, false)), kw, 128)) {
-    cudaGetLastError();
-    return;
-  }
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         FwdLayout<D>::SMEM);
-  });
+      !make_tma_2d(&tv, a.v, kw, max(1, max_rows(ps, false)), kw, 128))
+    launch_error("attn_fwd_tc", "TMA descriptor encode failed (q/k/v base, strides or extents)");
+  ensure_smem_for(attn_fwd_tc_kernel<D>, FwdLayout<D>::SMEM);
   attn_fwd_tc_kernel<D><<<dim3(tiles, a.hm.hq), kFwdThreads, FwdLayout<D>::SMEM, s>>>(tq, tk, tv, a, ps);
   note_launch();
 }
@@ -729,8 +742,7 @@ __global__ void __launch_bounds__(384, 1)
   auto bar = [&](int i) { return bars + 8u * i; };
 
   const int warp = threadIdx.x / 32;
-  int pi = 0;
-  while (pi + 1 < ps.n && ps.tile_prefix[pi + 1] <= (int)blockIdx.x) ++pi;
+  const int pi = find_problem(ps, (int)blockIdx.x);
   const AttnProblem P = ps.p[pi];
   const int n0 = (blockIdx.x - ps.tile_prefix[pi]) * 128;
   const int kvh = blockIdx.y;
@@ -955,7 +967,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         tc::fence_proxy_async();
         asm volatile("bar.sync 2, 128;\n" ::: "memory");
-        if (t == 0 && !(a.debug & 1)) {
+        if (t == 0) {
           tc::tma_reduce_add_2d(&tmDQ, stg, h * D + cc * 32, P.q_row0 + m0);
           tc::bulk_commit();
         }
@@ -992,8 +1004,6 @@ __global__ void __launch_bounds__(384, 1)
 template <int D>
 void launch_bwd_tc_d(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
   ProblemSet ps = in;
-  static const int dbg = getenv("SPATTN_DEBUG") ? atoi(getenv("SPATTN_DEBUG")) : 0;
-  const_cast<BwdArgs&>(a).debug = dbg;
   ps.tile_prefix[0] = 0;
   for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nk + 127) / 128;
   const int tiles = ps.tile_prefix[ps.n];
@@ -1003,15 +1013,9 @@ void launch_bwd_tc_d(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
   const uint64_t qrows = max(1, max_rows(ps, true)), krows = max(1, max_rows(ps, false));
   if (!make_tma_2d(&tq, a.q, qw, qrows, qw, 128) || !make_tma_2d(&tk, a.k, kw, krows, kw, 128) ||
       !make_tma_2d(&tv, a.v, kw, krows, kw, 128) || !make_tma_2d(&tdo, a.dout, ow, qrows, ow, 128) ||
-      !make_tma_2d_f32(&tdq, a.dq_acc, (uint64_t)a.hm.hq * a.d, qrows, (uint64_t)a.dq_row_stride, 128)) {
-    cudaGetLastError();
-    return;
-  }
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         BwdLayout<D>::SMEM);
-  });
+      !make_tma_2d_f32(&tdq, a.dq_acc, (uint64_t)a.hm.hq * a.d, qrows, (uint64_t)a.dq_row_stride, 128))
+    launch_error("attn_bwd_tc", "TMA descriptor encode failed (q/k/v/dout/dq base, strides or extents)");
+  ensure_smem_for(attn_bwd_tc_kernel<D>, BwdLayout<D>::SMEM);
   attn_bwd_tc_kernel<D><<<dim3(tiles, a.hm.hkv), 384, BwdLayout<D>::SMEM, s>>>(tq, tk, tv, tdo, tdq, a, ps);
   note_launch();
 }

@@ -445,6 +445,13 @@ int spattn_all_gather(spattn_ctx* ctx, const void* local, void* out, int64_t out
   return guard([&] { seqpar::all_gather(*ctx->rc, ctx->rc->sp_group, local, outer, extent, inner_bytes, out); });
 }
 
+int spattn_all_gather_backward(spattn_ctx* ctx, const void* grad_gathered, void* parts, int64_t outer,
+                               int64_t extent, int64_t inner_bytes) {
+  return guard([&] {
+    seqpar::all_gather_backward(*ctx->rc, ctx->rc->sp_group, grad_gathered, outer, extent, inner_bytes, parts);
+  });
+}
+
 int spattn_ring_shift(spattn_ctx* ctx, const void* payload, void* out, int64_t bytes) {
   return guard([&] { seqpar::ring_shift(*ctx->rc, ctx->rc->sp_group, payload, bytes, out); });
 }

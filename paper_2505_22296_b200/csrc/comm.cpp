@@ -1,6 +1,7 @@
 // Transports for the SP collectives: a single-device loopback fabric (ranks = host threads,
 // mirroring CommFabric, /root/reference/proj/src/comm.cpp:127-231) and NCCL (one process per
 // GPU over NVLink/NVSwitch), NCCL resolved at run time with dlopen.
+#include <algorithm>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -351,9 +352,9 @@ class NcclTransport : public Transport {
     const std::string k = g.key();
     auto it = sub_.find(k);
     if (it != sub_.end()) return it->second;
-    int color = 0;
-    for (int r : g.ranks) color = color * 31 + r + 1;
-    color &= 0x3fffffff;
+    // every split call partitions the ranks into disjoint groups (the USP inner / outer
+    // groups), so the group's lowest rank is a collision-free colour
+    const int color = *std::min_element(g.ranks.begin(), g.ranks.end());
     ncclComm_t c;
     nccl_check(nccl().CommSplit(world_comm_, color, g.index_of(rank_), &c, nullptr), "CommSplit");
     sub_[k] = c;

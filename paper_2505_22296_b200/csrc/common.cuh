@@ -8,6 +8,20 @@
 
 namespace spattn {
 
+// The problem a launch's tile (or tile pair) index belongs to: the first pi in [0, n) with
+// tile_prefix[pi + 1] > tile (binary search over up to kMaxProblems prefix sums).
+__device__ __forceinline__ int find_problem(const ProblemSet& ps, int tile) {
+  int lo = 0, hi = ps.n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (ps.tile_prefix[mid + 1] > tile)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

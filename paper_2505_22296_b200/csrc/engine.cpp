@@ -268,8 +268,11 @@ void launch_attn_fwd(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
     launch_attn_fwd_pair(a, ps, s);
   else if (seqpar::kernel_family() != seqpar::KernelFamily::mma && tc_fwd_supported(a))
     launch_attn_fwd_tc(a, ps, s);
+  else if (seqpar::kernel_family() == seqpar::KernelFamily::mma)
+    launch_attn_fwd_mma(a, ps, s);  // selected explicitly (A/B anchor), never a fallback
   else
-    launch_attn_fwd_mma(a, ps, s);
+    throw seqpar::ShapeError("attention forward: the tcgen05 kernels need 16-byte aligned q/k/v base "
+                             "pointers and row strides (head_dim 64 or 128)");
 }
 bool tc_bwd_q64_supported(const BwdArgs& a);
 void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
@@ -277,8 +280,7 @@ void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& ps, cudaStream_t
 // The backward launch picks the q64 tcgen05 kernel for these arguments (the only one that can
 // write dK / dV directly as bf16).
 bool bwd_uses_q64(const BwdArgs& a) {
-  static const bool use_q64 = !getenv("SPATTN_BWD_Q128");
-  return seqpar::kernel_family() != seqpar::KernelFamily::mma && use_q64 && tc_bwd_q64_supported(a);
+  return seqpar::kernel_family() != seqpar::KernelFamily::mma && tc_bwd_q64_supported(a);
 }
 
 void launch_attn_bwd(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
@@ -287,8 +289,11 @@ void launch_attn_bwd(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
     launch_attn_bwd_tc_q64(a, ps, s);
   else if (tc && tc_bwd_supported(a))
     launch_attn_bwd_tc(a, ps, s);
+  else if (!tc)
+    launch_attn_bwd_mma(a, ps, s);  // selected explicitly (A/B anchor), never a fallback
   else
-    launch_attn_bwd_mma(a, ps, s);
+    throw seqpar::ShapeError("attention backward: the tcgen05 kernels need 16-byte aligned q/k/v/dout "
+                             "base pointers and row strides (head_dim 64 or 128)");
 }
 }  // namespace spattn
 namespace seqpar {
@@ -328,14 +333,33 @@ void require_dim(int d) {
   if (d != 64 && d != 128) throw ConfigError("attention kernels support head_dim 64 or 128, got " + std::to_string(d));
 }
 
-// Plain (single wave) or merging (any number of waves) forward over a problem list.
+bool q_rows_disjoint(const std::vector<AttnProblem>& probs) {
+  std::vector<std::pair<int64_t, int64_t>> iv;
+  for (const auto& p : probs) iv.emplace_back(p.q_row0, static_cast<int64_t>(p.q_row0) + p.nq);
+  std::sort(iv.begin(), iv.end());
+  for (size_t i = 1; i < iv.size(); ++i)
+    if (iv[i].first < iv[i - 1].second) return false;
+  return true;
+}
+
+// Plain or merging forward over a problem list. Plain mode writes every query row once, so its
+// problems must cover disjoint query rows (one document / one run each); any number of them is
+// launched kMaxProblems at a time. Merge mode (ring steps, fused runs) groups problems into
+// q-disjoint waves that merge into the running output one after another.
 void attention_forward(cudaStream_t s, const spattn::FwdArgs& base,
                        const std::vector<AttnProblem>& probs, bool merge) {
   require_dim(base.d);
-  auto waves = q_disjoint_waves(probs);
-  if (!merge && waves.size() > 1) throw StateError("attention_forward: overlapping problems need merge mode");
   ProfScope prof(s, 0);
-  for (const auto& w : waves) {
+  if (!merge) {
+    if (!q_rows_disjoint(probs)) throw StateError("attention_forward: overlapping problems need merge mode");
+    for (size_t i = 0; i < probs.size(); i += spattn::kMaxProblems) {
+      const size_t n = std::min<size_t>(spattn::kMaxProblems, probs.size() - i);
+      spattn::launch_attn_fwd(base, to_set(probs, i, n), s);
+      check_launch();
+    }
+    return;
+  }
+  for (const auto& w : q_disjoint_waves(probs)) {
     spattn::launch_attn_fwd(base, to_set(w, 0, w.size()), s);
     check_launch();
   }
@@ -1774,6 +1798,20 @@ void all_gather(RankCtx& ctx, const CommGroup& group, const void* local, int64_t
     run_tasks(tasks, 1, false, s);
   }
   (void)me;
+}
+
+// all_gather's backward exchange (comm.cpp:415-443): member i receives block i of every member's
+// gathered gradient (one all-to-all of [outer, G*extent] rows viewed as heads), counted as the
+// reference counts it: a second all_gather at gather volume (comm.cpp:418-420).
+void all_gather_backward(RankCtx& ctx, const CommGroup& group, const void* grad_gathered, int64_t outer,
+                         int64_t extent, int64_t inner_bytes, void* parts) {
+  if (outer < 0 || extent < 0 || inner_bytes < 0) throw ShapeError("all_gather: negative extent");
+  const int G = group.size();
+  const auto before = ctx.stats[static_cast<int>(Primitive::all_to_all)];
+  all_to_all(ctx, group, grad_gathered, 1, outer, G * extent, inner_bytes, 1, 2, 1, parts);
+  // the exchange above counted itself as an all_to_all; book it under all_gather instead
+  ctx.stats[static_cast<int>(Primitive::all_to_all)] = before;
+  ctx.count(Primitive::all_gather, outer * extent * inner_bytes * (G - 1));
 }
 
 void ring_shift(RankCtx& ctx, const CommGroup& group, const void* payload, int64_t bytes, void* out) {

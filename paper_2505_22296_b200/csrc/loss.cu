@@ -81,12 +81,23 @@ __host__ __device__ inline void exact_merge(uint64_t* x, const uint64_t* y) {
 
 // One block: thread t accumulates values t, t + blockDim, ... into its own accumulator in
 // shared memory; accumulators merge pairwise (exact, so the tree order does not matter).
+// out[kLimbs] = 1 when any value is Inf / NaN (exponent field 0x7ff): the host then throws like
+// ExactSum::add (exact_sum.cpp) instead of returning a sum of garbage fixed-point chunks.
 __global__ void exact_sum_kernel(const double* v, int64_t n, uint64_t* out) {
   extern __shared__ uint64_t acc[];  // [blockDim][kLimbs]
   uint64_t* mine = acc + threadIdx.x * ExactSum::kLimbs;
   for (int i = 0; i < ExactSum::kLimbs; ++i) mine[i] = 0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) exact_add(mine, v[i]);
-  __syncthreads();
+  int bad = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double x = v[i];
+    if (((__double_as_longlong(x) >> 52) & 0x7ff) == 0x7ff) {
+      bad = 1;
+      continue;
+    }
+    exact_add(mine, x);
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) out[ExactSum::kLimbs] = bad;
   for (int s = blockDim.x / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) exact_merge(mine, acc + (threadIdx.x + s) * ExactSum::kLimbs);
     __syncthreads();
@@ -228,16 +239,19 @@ ExactSum exact_sum_device(const double* values, int64_t n, cudaStream_t s) {
   ExactSum r;
   if (n <= 0) return r;
   uint64_t* d = nullptr;
-  LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), ExactSum::kLimbs * 8, s));
+  LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), (ExactSum::kLimbs + 1) * 8, s));
   constexpr int kThreads = 128;
   exact_sum_kernel<<<1, kThreads, kThreads * ExactSum::kLimbs * 8, s>>>(values, n, d);
   spattn::note_launch();
   LS_CUDA(cudaGetLastError());
-  std::array<uint64_t, ExactSum::kLimbs> h{};
+  std::array<uint64_t, ExactSum::kLimbs + 1> h{};
   LS_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(h), cudaMemcpyDeviceToHost, s));
   LS_CUDA(cudaFreeAsync(d, s));
   LS_CUDA(cudaStreamSynchronize(s));
-  return ExactSum::from_limbs(h);
+  if (h[ExactSum::kLimbs]) throw ConfigError("ExactSum requires finite values");
+  std::array<uint64_t, ExactSum::kLimbs> limbs{};
+  for (int i = 0; i < ExactSum::kLimbs; ++i) limbs[static_cast<size_t>(i)] = h[static_cast<size_t>(i)];
+  return ExactSum::from_limbs(limbs);
 }
 
 void logprob_forward(cudaStream_t s, const void* logits, int dtype, int64_t T, int64_t V,

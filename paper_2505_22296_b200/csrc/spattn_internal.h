@@ -17,13 +17,18 @@ struct AttnProblem {
   int causal;
 };
 
-constexpr int kMaxProblems = 48;
+// Problems per launch. ProblemSet travels by value in the kernel parameters (CUDA 12.1+ allows
+// 32764 bytes); 1000 problems keep every kernel's parameters (ProblemSet + args + up to five
+// 128-byte tensor maps) under that limit, enough for a neat-packed batch of hundreds of
+// documents per launch (larger problem lists are split into several launches).
+constexpr int kMaxProblems = 1000;
 
 struct ProblemSet {
   AttnProblem p[kMaxProblems];
   int tile_prefix[kMaxProblems + 1];  // cumulative q tiles (of the launching kernel's BLOCK_M)
   int n;
 };
+static_assert(sizeof(ProblemSet) + 5 * 128 + 512 <= 32764, "kernel parameter space");
 
 // Head mapping of a rank's local tensors: local q head h is global head q_head_base + h; it
 // reads kv head (q_head_base + h) / rep - kv_head_base of the local kv tensor. This indexes
@@ -76,6 +81,18 @@ struct BwdArgs {
   int debug;  // profiling switches (SPATTN_DEBUG env): 1 skip dQ atomics, 2 skip dK/dV atomics
   long long* trace;  // profiling: per-iteration clock64 events of CTA (0,0), or null
 };
+
+// Launch-side failures throw std::runtime_error (SPATTN_ERR_STATE at the C ABI): a TMA
+// descriptor that does not encode or a failed shared-memory opt-in never leaves the outputs
+// silently unwritten.
+[[noreturn]] void launch_error(const char* kernel, const char* what);
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `kernel` on the CURRENT device, once per
+// (kernel, device) pair (a process may drive several GPUs).
+void ensure_smem(const void* kernel, int bytes);
+template <class K>
+void ensure_smem_for(K* kernel, int bytes) {
+  ensure_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
 
 // Launch accounting (bench.py's gpu_launches): every launcher in this library calls this.
 void note_launch(int n = 1);

@@ -419,6 +419,9 @@ class _FabricEngine(torch.autograd.Function):
     def backward(ctx, dout, _dlse):
         fab, mode, u, r = ctx.fab, ctx.mode, ctx.u, ctx.r
         sp = fab.sp
+        if not ctx.fin.alive:
+            raise StateError("engine_attention: backward ran twice over one forward; its saved "
+                             "state was released by the first (retain_graph is not supported)")
         qs, ks, vs = ctx.keep.tensors[:3]
         dos = [shard_rows(dout.contiguous(), mode, sp, i, u, r) for i in range(sp)]
         dqs = [torch.empty_like(x) for x in qs]
@@ -520,7 +523,22 @@ class RankContext:
                                                raw, ctypes.byref(h)))
         self._h = h
         self.rank, self.world = rank, world
+        self._pending = []  # _RankSaved of forwards whose backward has not run yet
         self._fin = weakref.finalize(self, C.lib().spattn_ctx_destroy, h)
+
+    def finish_backward(self):
+        """Zero participation (reference attention.cpp:311-320, comm.cpp:366-370): every forward
+        of this rank whose output received no gradient — autograd never reaches its node when
+        the output is unused — runs its backward with a zero upstream gradient, in forward
+        order, so the peers' collectives complete; the gradients the peers send back still flow
+        into q / k / v. Call it on every rank after ``loss.backward()`` (a no-op when every
+        output was used)."""
+        for e in list(self._pending):
+            q, k, v = e.tensors[:3]
+            grads = e.backward(torch.zeros_like(e.tensors[3]))
+            pairs = [(t, g) for t, g in zip((q, k, v), grads) if t.requires_grad]
+            if pairs:
+                torch.autograd.backward([t for t, _ in pairs], [g for _, g in pairs])
 
     def replicate_packing_mask(self, mask: Optional[bytes], max_len: int) -> bytes:
         """replicate_packing_mask (partition.cpp:222-227) over NCCL: group index 0 supplies
@@ -590,15 +608,17 @@ class _AllGather(torch.autograd.Function):
 
 
 def _reduce_scatter(h, G, gy, outer, extent):
-    """The all_gather backward (comm.cpp:418-443): one all_to_all hands every member its block
-    of each member's gathered gradient, tree-summed in group order (counted as all_to_all)."""
+    """The all_gather backward (comm.cpp:415-443): one exchange hands every member its block of
+    each member's gathered gradient, tree-summed in group order; counted as a second
+    all_gather at gather volume (comm.cpp:418-420)."""
     gy = gy.contiguous()
-    rest = gy.numel() // max(1, outer * G * extent)  # elements after the gather axis
-    buf = torch.empty((1, G * outer, extent, rest), dtype=gy.dtype, device=gy.device)
+    inner = gy.numel() * gy.element_size() // max(1, outer * G * extent)  # bytes after the axis
+    buf = torch.empty((G, outer, extent, inner // gy.element_size()), dtype=gy.dtype,
+                      device=gy.device)
     C.check(C.lib().spattn_ctx_set_stream(h, _stream()))
-    C.check(C.lib().spattn_all_to_all(h, gy.data_ptr(), buf.data_ptr(), 1, outer, G * extent, rest,
-                                      gy.element_size(), 2, 1))
-    return _tree_sum(list(buf.view(G, outer, extent, rest).unbind(0)))
+    C.check(C.lib().spattn_all_gather_backward(h, gy.data_ptr(), buf.data_ptr(), outer, extent,
+                                               inner))
+    return _tree_sum(list(buf.unbind(0)))
 
 
 def all_gather_backward(group, grad_out: torch.Tensor, local_shape, dim: int) -> torch.Tensor:
@@ -688,9 +708,38 @@ def attention_step_host(engine: str, q: torch.Tensor, k: torch.Tensor, v: torch.
     return (dq, dk, dv, out, lse) if want_out else (dq, dk, dv)
 
 
+class _RankSaved:
+    """One _RankEngine forward's library state (spattn_saved) and the tensors it points into.
+    The handle is freed by the backward that consumes it, or when this holder is collected —
+    never by the lifetime of the returned ``out`` object, which autograd may drop before it runs
+    the backward."""
+
+    def __init__(self, rc, h, q, k, v, out, lse):
+        self.rc, self.h = rc, h
+        self.tensors = (q, k, v, out, lse)
+        self.done = False
+        self._fin = weakref.finalize(self, C.lib().spattn_saved_free, h)
+
+    def backward(self, dout):
+        if self.done:
+            raise StateError("SequenceParallelAttention: backward ran twice over one forward; its "
+                             "saved state was released by the first (retain_graph is not "
+                             "supported)")
+        q, k, v = self.tensors[:3]
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        C.check(C.lib().spattn_ctx_set_stream(self.rc._h, _stream()))
+        C.check(C.lib().spattn_bwd(self.rc._h, self.h, dout.contiguous().data_ptr(), dq.data_ptr(),
+                                   dk.data_ptr(), dv.data_ptr()))
+        self.done = True
+        self.rc._pending = [e for e in self.rc._pending if e is not self]
+        self.tensors = None
+        self._fin()  # the state's buffers are not needed any more
+        return dq, dk, dv
+
+
 class _RankEngine(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, rc, engine, cfg, lay, docs, pos=None):
+    def forward(ctx, q, k, v, rc, engine, cfg, lay, docs, pos=None, track=False):
         out = torch.empty_like(q)
         lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
         C.check(C.lib().spattn_ctx_set_stream(rc._h, _stream()))
@@ -702,20 +751,17 @@ class _RankEngine(torch.autograd.Function):
                                         ctypes.byref(lay), q.shape[0], q.data_ptr(), k.data_ptr(),
                                         v.data_ptr(), out.data_ptr(), lse.data_ptr(), darr, nd,
                                         parr, ROPE_BASE, ctypes.byref(saved)))
-        ctx.rc, ctx.h = rc, saved
-        ctx.lse = lse  # the saved state reads this LSE in backward
-        ctx.save_for_backward(q, k, v, out)
-        ctx.fin = weakref.finalize(out, C.lib().spattn_saved_free, saved)
+        # the autograd ctx owns the holder (and so the handle); the rank context lists it until
+        # a backward consumes it, so finish_backward() can make an unused output take part
+        ctx.entry = _RankSaved(rc, saved, q, k, v, out, lse)
+        if track:
+            rc._pending.append(ctx.entry)
         return out
 
     @staticmethod
     def backward(ctx, dout):
-        q, k, v, out = ctx.saved_tensors
-        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-        C.check(C.lib().spattn_ctx_set_stream(ctx.rc._h, _stream()))
-        C.check(C.lib().spattn_bwd(ctx.rc._h, ctx.h, dout.contiguous().data_ptr(), dq.data_ptr(),
-                                   dk.data_ptr(), dv.data_ptr()))
-        return dq, dk, dv, None, None, None, None, None, None
+        dq, dk, dv = ctx.entry.backward(dout)
+        return dq, dk, dv, None, None, None, None, None, None, None
 
 
 class SequenceParallelAttention(torch.nn.Module):
@@ -737,7 +783,12 @@ class SequenceParallelAttention(torch.nn.Module):
         """``position_ids``: the GLOBAL ids of this rank's rows; when given q and k are rotated
         (rope_apply) before attention — a local 0-based range would corrupt the rotary phases
         (reference model.cpp:313-318)."""
-        return _RankEngine.apply(q.contiguous(), k.contiguous(), v.contiguous(), self.rc,
-                                 self.engine, self.cfg, self.lay,
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        track = torch.is_grad_enabled() and any(t.requires_grad for t in (q, k, v))
+        return _RankEngine.apply(q, k, v, self.rc, self.engine, self.cfg, self.lay,
                                  None if docs is None else list(docs),
-                                 None if position_ids is None else list(position_ids))
+                                 None if position_ids is None else list(position_ids), track)
+
+    def finish_backward(self):
+        """See RankContext.finish_backward."""
+        self.rc.finish_backward()

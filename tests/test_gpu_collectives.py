@@ -72,6 +72,10 @@ def test_all_gather_backward_reduce_scatters(P, messages):
 
     grads = on_ranks(fab, rank)
     assert grads[0] == [3.0, 6.0] and grads[1] == [9.0, 12.0]
+    # test_comm.cpp:154-155: the backward counts as a second all_gather at gather volume
+    for r in range(2):
+        assert fab.stats(r)["all_gather"] == (2, 2 * 16)
+        assert fab.stats(r)["all_to_all"] == (0, 0)
 
 
 def test_all_gather_autograd_single_member(P):

@@ -180,6 +180,18 @@ def test_gpu_exact_sum_matches_host():
     assert P.exact_sum(x.cuda()) == P.exact_sum(x) == math.fsum(x.tolist())
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("bad", [math.inf, -math.inf, math.nan])
+def test_gpu_exact_sum_rejects_non_finite_like_host(bad):
+    # ExactSum::add throws 'ExactSum requires finite values' (exact_sum.cpp); the device kernel
+    # must not fold an exponent-0x7ff value in as a finite fixed-point chunk
+    x = torch.tensor([1.0, 2.0, bad, 3.0], dtype=torch.float64)
+    with pytest.raises(ValueError, match="finite"):
+        P.exact_sum(x)
+    with pytest.raises(ValueError, match="finite"):
+        P.exact_sum(x.cuda())
+
+
 def _run_ranks(sp, fn):
     fab = P.Fabric(sp)
     res, errs = [None] * sp, []
