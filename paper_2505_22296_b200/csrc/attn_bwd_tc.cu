@@ -1,30 +1,22 @@
 // tcgen05 attention backward for head_dim 128 with 64-row query tiles (sm_100a).
-// attn_block_backward (attention.cpp:167-216): delta = rowsum(dO * O); P = exp(S*scale - lse);
-// dV += P^T dO; dS = P (dP - delta) * scale; dQ += dS K; dK += dS^T Q.
 //
 // One CTA = one 128-row key/value tile x one kv head; it loops over every (query head of the
-// GQA group, 64-row query tile) that sees the tile. The bound of this kernel is the SM's
-// shared-memory port (128 B/clk), so the design minimises shared-memory operand traffic:
-// K and V are copied ONCE into tensor memory and are the A operands of S^T = K Q^T and
-// dP^T = V dO^T (TS MMAs read only the 64-query B operand from shared memory: 2 KB instead of
-// 6 KB per 16-wide K step). TMEM map (512 columns, lane = key row unless noted):
-//   [0, 64)     S^T of the tile: half a (queries 0-31) cols [0,32), half b [32,64);
-//               P^T_h (bf16) overwrites cols [32h, 32h+16), dS^T_h (bf16) [32h+16, 32h+32)
-//   [64, 128)   dP^T (half a [64,96), half b [96,128)); dQ^T (lane = head-dim index) reuses it
-//   [128, 192)  K (bf16 pairs), [192, 256) V
-//   [256, 384)  dV accumulator, [384, 512) dK accumulator
-// The query tile is processed as two 32-query halves by two softmax-gradient warpgroups, so
-// one half's softmax overlaps the other half's MMAs; with one S/dP buffer (the K/V copies take
-// the second buffer's columns) the tensor pipe then idles only for the part of a half's
-// softmax that outlasts the 128-cycle dP MMA of the other half. Per-iteration MMA order:
-//   [wait PR_a] dV_a dK_a [wait PR_b] dQ^T dV_b dK_b | S_a' S_b' [wait dQ^T drained] dP_a' dP_b'
-// Shared-memory traffic per 128x64 iteration: 16+16 KB (S, dP B operands) + 16+16 (dV, dK B)
-// + 48 (dQ^T = K^T dS^T, SS) + 32 (Q/dO TMA) + 16 (dS^T stores) + 64 (dQ staging + TMA
-// reduce) = 224 KB, against 288 KB for the SS design it replaces.
+// GQA group, 64-row query tile) that sees the tile. TMEM (512 columns, lane = key row unless
+// noted) is double-buffered per query tile so the softmax-gradient math of tile i overlaps the
+// dV/dK/dQ MMAs of tile i-1:
+//   S^T_b  = K Q^T          cols [64b, 64b+64)        P^T_b (bf16) written back over it
+//   dP^T_b = V dO^T         cols [128+64b, +64)        dQ^T_b (lane = head-dim index) reuses it
+//   dV    += P^T_b dO       cols [256, 384)            (A operand from TMEM)
+//   dK    += dS^T_b Q       cols [384, 512)            (dS^T from swizzled smem)
+//   dQ^T_b = K^T dS^T_b     M = head dim 128, N = 64 queries, K = 128 keys
+// MMA issue order: S(i), dP(i), [dV dK dQ](i-1), S(i+1), ... The dQ warpgroup drains dQ^T
+// (warp w owns head-dim columns 32w..32w+31) through an 8 KB smem slot per warp into the fp32
+// accumulator with TMA reduce-add. attn_block_backward (attention.cpp:167-216).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <mutex>
 
 #include "tc.cuh"
 
@@ -33,14 +25,26 @@ namespace {
 
 constexpr int D = 128;
 constexpr int BQ = 64;
-constexpr int NST = 3;                      // Q/dO pipeline stages
-constexpr int NSMW = 8;                     // softmax-gradient warps: (lane quadrant, half)
-constexpr int DRAIN0 = NSMW;                // 4 dQ drain warps (also load K/V into TMEM)
+#ifndef BWD_NST
+#define BWD_NST 3
+#endif
+#ifndef BWD_NSTG
+#define BWD_NSTG 1
+#endif
+#ifndef BWD_SMW
+#define BWD_SMW 4
+#endif
+constexpr int NST = BWD_NST;                // Q/dO pipeline stages
+// Softmax-gradient warps: 4 (one per TMEM lane quadrant, 64 queries per thread) or 8 (two per
+// quadrant, 32 queries each: two warps per SMSP hide each other's latency chains).
+constexpr int NSMW = BWD_SMW;
+constexpr int DRAIN0 = NSMW;               // first of the 4 dQ drain warps
 constexpr int PRODW = DRAIN0 + 4, TALLOCW = PRODW + 1, MMAW = PRODW + 3;
-constexpr int NTHREADS = (PRODW + 4) * 32;  // 512
-constexpr int REG_SM = 160, REG_DQ = 96, REG_CTL = 96;
+constexpr int NTHREADS = (PRODW + 4) * 32;
+// registers per thread: softmax / drain / control, sum over warps <= 2048
+constexpr int REG_SM = NSMW == 4 ? 232 : 160, REG_DQ = NSMW == 4 ? 120 : 96, REG_CTL = NSMW == 4 ? 152 : 96;
 static_assert(NSMW * REG_SM + 4 * REG_DQ + 4 * REG_CTL <= 2048, "register budget");
-constexpr int NSTG = 1;                     // dQ staging slots per drain warp
+constexpr int NSTG = BWD_NSTG;              // dQ staging slots per drain warp
 constexpr int KV_TILE = 128 * D * 2;        // 32 KB (two 16 KB column blocks)
 constexpr int Q_TILE = BQ * D * 2;          // 16 KB (two 8 KB column blocks)
 constexpr int K_OFF = 0, V_OFF = KV_TILE;
@@ -50,17 +54,16 @@ constexpr int DS_OFF = DO_OFF + NST * Q_TILE;    // 2 x [128 keys x 64 queries] 
 constexpr int STG_OFF = DS_OFF + 2 * 16384;      // 4 warps x NSTG x [64 queries x 32 fp32] (8 KB)
 constexpr int LD_OFF = STG_OFF + 4 * NSTG * 8192;  // lse*log2e, delta: [NST][64] each
 constexpr int BAR_OFF = LD_OFF + 2 * NST * 64 * 4;
-constexpr uint32_t T_S = 0, T_DP = 64, T_K = 128, T_V = 192, T_DV = 256, T_DK = 384;
 
 enum {
-  E_KV = 0,                 // K/V tiles landed (TMA)
-  E_KVT = 1,                // K/V copied into TMEM (128 arrivals)
-  E_QF = 2,                 // [NST] Q/dO stage full (TMA bytes + 32 producer lanes)
-  E_QE = E_QF + NST,        // [NST] stage consumed (MMA commit)
-  E_HF = E_QE + NST,        // [2] S^T_h and dP^T_h done
-  E_PR = E_HF + 2,          // [2] half h's P^T / dS^T written (128 arrivals)
-  E_MD = E_PR + 2,          // [2] dQ^T of iteration i (buffer i&1) done
-  E_DQF = E_MD + 2,         // [2] dQ^T drained to registers (128 arrivals)
+  E_KV = 0,
+  E_QF = 1,                 // [NST]
+  E_QE = E_QF + NST,        // [NST]
+  E_SF = E_QE + NST,        // [2]
+  E_DPF = E_SF + 2,         // [2]
+  E_PR = E_DPF + 2,         // [2] 128 arrivals
+  E_MD = E_PR + 2,          // [2]
+  E_DQF = E_MD + 2,         // [2] 128 arrivals
   E_FIN = E_DQF + 2,
   E_N = E_FIN + 1
 };
@@ -82,28 +85,61 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                : "memory");
 }
 
-// Softmax gradient of one 32-query half for one key (thread): P = 2^(s*scale*log2e - lse*log2e)
-// and dS = P (dP - delta) * scale, both packed to bf16 pairs (attention.cpp:199-209). MASK (only
+// Softmax gradient of one 32-query chunk for one key (thread): P = 2^(s*scale*log2e - lse*log2e)
+// and dS = P (dP - delta), both packed to bf16 pairs (attention.cpp:199-209). Packed fp32x2
+// math; one pair in four takes the FMA-pipe exp2 so MUFU and FMA finish together. MASK (only
 // for tiles crossing the causal diagonal or the row end) zeroes queries outside [ilo, ihi).
-// dl2 holds -delta*scale, so dS comes out pre-scaled and dQ / dK need no rescaling.
-template <bool MASK>
-__device__ __forceinline__ void grad_half(const uint32_t (&rs)[32], const uint32_t (&rp)[32], const float2* nl2,
-                                          const float2* dl2, float sl2, float sc, int ilo, int ihi,
-                                          uint32_t (&wp)[16], uint32_t (&wd)[16]) {
+// dS is produced already multiplied by the softmax scale (dl2 holds -delta*scale): the dQ and
+// dK accumulators then need no rescaling (dS scale = scale * P (dP - delta)).
+template <bool MASK, bool PACKED, bool POLY>
+__device__ __forceinline__ void grad_chunk(const uint32_t (&rs)[32], const uint32_t (&rp)[32], const float2* nl2,
+                                           const float2* dl2, uint64_t sl2x2, uint64_t sc2, int ilo, int ihi,
+                                           uint32_t (&wp)[16], uint32_t (&wd)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const float2 nl = nl2[i], dl = dl2[i];
-    float2 pp = make_float2(fast_exp2(fmaf(__uint_as_float(rs[2 * i]), sl2, nl.x)),
-                            fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), sl2, nl.y)));
+    float2 pp;
+    if (PACKED) {
+      const float2 x = f2_unpack(f2_fma(f2_pack(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1])), sl2x2,
+                                        f2_pack(nl.x, nl.y)));
+      if (POLY && (i & 3) == 3)
+        pp = poly_exp2x2(x.x, x.y);
+      else
+        pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+    } else {
+      const float sl2 = f2_unpack(sl2x2).x;
+      pp = make_float2(fast_exp2(fmaf(__uint_as_float(rs[2 * i]), sl2, nl.x)),
+                       fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), sl2, nl.y)));
+    }
     if (MASK) {
       pp.x = (2 * i >= ilo && 2 * i < ihi) ? pp.x : 0.f;
       pp.y = (2 * i + 1 >= ilo && 2 * i + 1 < ihi) ? pp.y : 0.f;
     }
     wp[i] = pack_bf16(pp.x, pp.y);
-    wd[i] = pack_bf16(pp.x * fmaf(__uint_as_float(rp[2 * i]), sc, dl.x),
-                      pp.y * fmaf(__uint_as_float(rp[2 * i + 1]), sc, dl.y));
+    if (PACKED) {
+      const float2 dsv = f2_unpack(f2_mul(
+          f2_pack(pp.x, pp.y),
+          f2_fma(f2_pack(__uint_as_float(rp[2 * i]), __uint_as_float(rp[2 * i + 1])), sc2, f2_pack(dl.x, dl.y))));
+      wd[i] = pack_bf16(dsv.x, dsv.y);
+    } else {
+      const float sc = f2_unpack(sc2).x;
+      wd[i] = pack_bf16(pp.x * fmaf(__uint_as_float(rp[2 * i]), sc, dl.x),
+                        pp.y * fmaf(__uint_as_float(rp[2 * i + 1]), sc, dl.y));
+    }
   }
 }
+
+// SV: variant bits of the softmax-gradient code (fixed at 64: dS^T also stored to TMEM so dK is
+// a TS MMA, 2300 -> 2245 cycles per iteration). Measured no faster and removed from the build:
+// 1 prefetch chunk 1's TMEM loads, 2 packed fp32x2 math, 4 separate full / masked code paths,
+// 8 FMA-pipe exp2 for 1 pair in 4.
+constexpr int SV = 64;
+// Profiling switches (wrong results by design) exist only in -DSPATTN_PROFILING builds.
+#ifdef SPATTN_PROFILING
+#define BWD_DBG(bit) ((a.debug & (bit)) != 0)
+#else
+#define BWD_DBG(bit) false
+#endif
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_bwd_tc_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -115,22 +151,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t sK = sbase + K_OFF, sV = sbase + V_OFF, sQ = sbase + Q_OFF, sdO = sbase + DO_OFF,
                  sdS = sbase + DS_OFF, sStg = sbase + STG_OFF;
   float* sL = reinterpret_cast<float*>(smem + LD_OFF);  // [NST][64] -lse * log2e (-inf: empty row)
-  float* sDl = sL + NST * 64;                           // [NST][64] -delta * scale
+  float* sDl = sL + NST * 64;                           // [NST][64] delta
   const uint32_t bars = sbase + BAR_OFF;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + BAR_OFF + E_N * 8);
   auto bar = [&](int i) { return bars + 8u * i; };
 
   const int warp = threadIdx.x / 32;
   long long* trace = (a.trace && blockIdx.x == 0) ? a.trace : nullptr;
+  // debug bit 4: record only the iteration-start event (minimal perturbation)
+  const bool tr_all = !BWD_DBG(4);
 #define TR(slot, it) \
-  if (trace) trace[(it) * 16 + (slot)] = clock64()
-  // head-major order (kv head slowest, heaviest causal key tiles first within a head): the
-  // resident CTAs reduce into one kv head's dQ rows, which keeps the fp32 dQ partial sums
-  // L2-resident
+  if (trace && (tr_all || (slot) == 0)) trace[(it) * 16 + (slot)] = clock64()
+  // 1-D grid, kv head fastest: the heaviest causal key tiles of every head run first (LPT)
   const HeadMap hm = a.hm;
   const int ntiles = ps.tile_prefix[ps.n];
-  const int tile = blockIdx.x % ntiles;
-  const int kvh = blockIdx.x / ntiles;
+  // head-major order (kv head slowest, heaviest causal key tiles first within a head): the
+  // resident CTAs then reduce into one kv head's dQ rows (64 MB at c2) instead of all of them
+  // (512 MB), which keeps the fp32 dQ partial sums L2-resident (measured 22.3 -> 21.4 ms at c2).
+  // debug bit 8 restores the tile-major order for A/B runs.
+  const bool head_major = !BWD_DBG(8);
+  const int tile = head_major ? blockIdx.x % ntiles : blockIdx.x / hm.hkv;
+  const int kvh = head_major ? blockIdx.x / ntiles : blockIdx.x % hm.hkv;
   const int pi = find_problem(ps, tile);
   const AttnProblem P = ps.p[pi];
   const int n0 = (tile - ps.tile_prefix[pi]) * 128;
@@ -145,10 +186,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < E_N; ++i) {
-      int cnt = 1;
-      if (i == E_KVT || (i >= E_PR && i < E_PR + 2) || (i >= E_DQF && i < E_DQF + 2)) cnt = 128;
-      if (i >= E_QF && i < E_QF + NST) cnt = 33;  // TMA bytes + the producer's 32 lse/delta lanes
-      tc::mbar_init(bar(i), cnt);
+      const bool many = (i >= E_PR && i < E_PR + 2) || (i >= E_DQF && i < E_DQF + 2);
+      // a stage is full after the TMA bytes and the producer warp's 32 lse/delta stores
+      const bool stage = i >= E_QF && i < E_QF + NST;
+      const bool pr = i >= E_PR && i < E_PR + 2;
+      tc::mbar_init(bar(i), pr ? 32 * NSMW : many ? 128 : stage ? 33 : 1);
     }
     tc::fence_barrier_init();
   }
@@ -157,15 +199,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t tDV = tmem + 256, tDK = tmem + 384;
   if (warp >= PRODW) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_CTL));
 
-  // Roles (the scheduler favours the highest warp id, so the single-thread MMA issuer is the
-  // last warp): warps 0-7 softmax-gradient (quadrant w&3, query half w>>2), 8-11 dQ drain,
-  // 12 TMA producer, 13 TMEM allocator, 15 MMA issuer.
+  // Roles. The scheduler favours the highest warp id, so the single-thread MMA issuer is the
+  // last warp and the producer sits above the math warps: warps 0-3 softmax-gradient, 4-7 dQ
+  // drain, 8 TMA producer, 9 TMEM allocator, 11 MMA issuer.
   if (warp == PRODW) {
     // ------------------------------------------------------------------ TMA producer
-    // lane 0 issues the TMA loads; all 32 lanes stage the tile's lse/delta (2 query rows each)
-    // into the stage's smem slot and arrive on the stage barrier
+    // lane 0 issues the TMA loads; all 32 lanes stage this tile's lse/delta (2 query rows each)
+    // into the stage's smem slot and arrive on the stage barrier, so the softmax warpgroup
+    // never waits on global-memory latency
     const int lane = threadIdx.x % 32;
     if (T > 0) {
       if (lane == 0) {
@@ -175,13 +219,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tc::tma_load_2d(sV + b * 16384, &tmV, kvh * D + b * 64, P.k_row0 + n0, bar(E_KV));
         }
       }
+      // lse/delta of iteration it are fetched into registers one iteration ahead, so their
+      // global latency overlaps the wait for the stage instead of following it
       float pl[2], pd[2];
       auto fetch = [&](int it) {
         const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * BQ;
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           const int row = m0 + lane + 32 * k;
-          pl[k] = -INFINITY, pd[k] = 0.f;
+          pl[k] = -INFINITY, pd[k] = 0.f;  // stored negated: p = 2^(s*scale*log2e + l2)
           if (row < P.nq) {
             const int64_t g = (int64_t)(P.q_row0 + row) * a.lse_row_stride + h;
             pl[k] = __ldg(a.lse + g);
@@ -193,8 +239,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int it = 0; it < T; ++it) {
         const int st = it % NST;
         const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * BQ;
+        if (lane == 0) TR(14, it);
         if (it >= NST) tc::mbar_wait(bar(E_QE + st), ((it - NST) / NST) & 1);
         if (lane == 0) {
+          TR(15, it);
           tc::mbar_expect_tx(bar(E_QF + st), 2 * Q_TILE);
           for (int b = 0; b < 2; ++b) {
             tc::tma_load_2d(sQ + st * Q_TILE + b * 8192, &tmQ, h * D + b * 64, P.q_row0 + m0, bar(E_QF + st));
@@ -213,143 +261,173 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp == MMAW) {
     // ---------------------------------------------------------------------- MMA issuer
     if (tc::elect_one() && T > 0) {
-      constexpr uint32_t id_h = tc::idesc_bf16(128, 32, false, false);  // S^T_h, dP^T_h (A in TMEM)
-      constexpr uint32_t id_kv = tc::idesc_bf16(128, D, false, true);   // dV, dK (A in TMEM)
+      constexpr uint32_t id_s = tc::idesc_bf16(128, BQ, false, false);  // S^T, dP^T
+      constexpr uint32_t id_kv = tc::idesc_bf16(128, D, false, true);   // dV, dK
       constexpr uint32_t id_q = tc::idesc_bf16(128, BQ, true, true);    // dQ^T
-      // S^T_h = K Q_h^T and dP^T_h = V dO_h^T of iteration `it` (query half h = rows 32h..)
-      auto s_half = [&](int it, int h) {
-        const uint32_t q = sQ + (it % NST) * Q_TILE + h * 4096;
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-          tc::mma_ts(tmem + T_S + 32 * h, tmem + T_K + ks * 8,
-                     tc::sdesc(q + (ks >> 2) * 8192 + (ks & 3) * 32, 16, 1024), id_h, ks > 0);
-      };
-      auto dp_half = [&](int it, int h) {
-        const uint32_t dO = sdO + (it % NST) * Q_TILE + h * 4096;
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-          tc::mma_ts(tmem + T_DP + 32 * h, tmem + T_V + ks * 8,
-                     tc::sdesc(dO + (ks >> 2) * 8192 + (ks & 3) * 32, 16, 1024), id_h, ks > 0);
-      };
-      // dV += P^T_h dO_h, dK += dS^T_h Q_h (both A operands in TMEM, 2 K-steps of 16 queries)
-      auto kv_half = [&](int it, int h) {
-        const int st = it % NST;
-        const uint32_t q = sQ + st * Q_TILE, dO = sdO + st * Q_TILE;
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk)
-          tc::mma_ts(tmem + T_DV, tmem + T_S + 32 * h + kk * 8, tc::sdesc(dO + (2 * h + kk) * 2048, 8192, 1024),
-                     id_kv, (it > 0 || h > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk)
-          tc::mma_ts(tmem + T_DK, tmem + T_S + 32 * h + 16 + kk * 8,
-                     tc::sdesc(q + (2 * h + kk) * 2048, 8192, 1024), id_kv, (it > 0 || h > 0 || kk > 0) ? 1u : 0u);
-      };
-      tc::mbar_wait(bar(E_KVT), 0);
-      tc::fence_after();
-      tc::mbar_wait(bar(E_QF), 0);
-      tc::fence_after();
-      s_half(0, 0);
-      s_half(0, 1);
-      dp_half(0, 0);
-      tc::commit(bar(E_HF + 0));
-      dp_half(0, 1);
-      tc::commit(bar(E_HF + 1));
-      for (int it = 0; it < T; ++it) {
-        const int b = it & 1, st = it % NST;
-        TR(0, it);
-        tc::mbar_wait(bar(E_PR + 0), it & 1);
+      auto tail = [&](int i) {  // dV, dK, dQ^T of iteration i
+        const int b = i & 1, st = i % NST;
+        const uint32_t q = sQ + st * Q_TILE, dO = sdO + st * Q_TILE, ds = sdS + b * 16384;
+        TR(5, i);
+        tc::mbar_wait(bar(E_PR + b), (i >> 1) & 1);
+        TR(6, i);
         tc::fence_after();
-        TR(1, it);
-        kv_half(it, 0);
-        tc::mbar_wait(bar(E_PR + 1), it & 1);
-        tc::fence_after();
-        TR(2, it);
-        // dQ^T = K^T dS^T (M = head dim, N = 64 queries, K = 128 keys) into the dP^T columns
-        // (both halves' dP^T were consumed before PR); dS^T from smem buffer b
-        const uint32_t ds = sdS + b * 16384;
+#pragma unroll
+        for (int kk = 0; kk < BQ / 16; ++kk)
+          tc::mma_ts(tDV, tmem + 64 * b + kk * 8, tc::sdesc(dO + kk * 2048, 8192, 1024), id_kv,
+                     (i > 0 || kk > 0) ? 1u : 0u);
+        if constexpr ((SV & 64) != 0) {
+          // dS^T also sits in TMEM (the dead upper half of the S^T buffer): dK is a TS MMA and
+          // reads no A operand from shared memory
+#pragma unroll
+          for (int kk = 0; kk < BQ / 16; ++kk)
+            tc::mma_ts(tDK, tmem + 64 * b + 32 + kk * 8, tc::sdesc(q + kk * 2048, 8192, 1024), id_kv,
+                       (i > 0 || kk > 0) ? 1u : 0u);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < BQ / 16; ++kk)
+            tc::mma_ss(tDK, tc::sdesc(ds + kk * 32, 16, 1024), tc::sdesc(q + kk * 2048, 8192, 1024), id_kv,
+                       (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::commit(bar(E_QE + st));
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          tc::mma_ss(tmem + T_DP, tc::sdesc(sK + kk * 2048, 16384, 1024), tc::sdesc(ds + kk * 2048, 8192, 1024),
-                     id_q, kk > 0 ? 1u : 0u);
+          tc::mma_ss(tmem + 128 + 64 * b, tc::sdesc(sK + kk * 2048, 16384, 1024),
+                     tc::sdesc(ds + kk * 2048, 8192, 1024), id_q, kk > 0 ? 1u : 0u);
         tc::commit(bar(E_MD + b));
-        kv_half(it, 1);
-        tc::commit(bar(E_QE + st));  // last readers of this Q/dO stage issued
-        if (it + 1 < T) {
-          tc::mbar_wait(bar(E_QF + (it + 1) % NST), ((it + 1) / NST) & 1);
-          tc::fence_after();
-          s_half(it + 1, 0);  // the S^T columns' last readers (dV/dK of `it`) are issued
-          s_half(it + 1, 1);
-          TR(3, it);
-          tc::mbar_wait(bar(E_DQF + b), (it >> 1) & 1);  // dQ^T(it) left the dP^T columns
-          tc::fence_after();
-          TR(4, it);
-          dp_half(it + 1, 0);
-          tc::commit(bar(E_HF + 0));
-          dp_half(it + 1, 1);
-          tc::commit(bar(E_HF + 1));
+        TR(7, i);
+      };
+      tc::mbar_wait(bar(E_KV), 0);
+      for (int it = 0; it < T; ++it) {
+        const int b = it & 1, st = it % NST;
+        const uint32_t q = sQ + st * Q_TILE, dO = sdO + st * Q_TILE;
+        TR(0, it);
+        tc::mbar_wait(bar(E_QF + st), (it / NST) & 1);
+        TR(1, it);
+        tc::fence_after();
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t ko = (ks >> 2) * 16384 + (ks & 3) * 32, qo = (ks >> 2) * 8192 + (ks & 3) * 32;
+          tc::mma_ss(tmem + 64 * b, tc::sdesc(sK + ko, 16, 1024), tc::sdesc(q + qo, 16, 1024), id_s, ks > 0);
         }
+        tc::commit(bar(E_SF + b));
+        TR(2, it);
+        if (it >= 2 && !BWD_DBG(64)) {  // dQ^T of it-2 (same columns) must be drained (debug 64: skip, wrong dq)
+          tc::mbar_wait(bar(E_DQF + b), ((it - 2) >> 1) & 1);
+          tc::fence_after();
+        }
+        TR(3, it);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t ko = (ks >> 2) * 16384 + (ks & 3) * 32, qo = (ks >> 2) * 8192 + (ks & 3) * 32;
+          tc::mma_ss(tmem + 128 + 64 * b, tc::sdesc(sV + ko, 16, 1024), tc::sdesc(dO + qo, 16, 1024), id_s,
+                     ks > 0);
+        }
+        tc::commit(bar(E_DPF + b));
+        TR(4, it);
+        if (it >= 1) tail(it - 1);
       }
+      tail(T - 1);
       tc::commit(bar(E_FIN));
     }
   } else if (warp < NSMW) {
-    // ----------------------------------- softmax-gradient warpgroups (lane = key, half = w>>2)
+    // ----------------------------------------------- softmax-gradient warpgroup (lane = key)
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_SM));
-    const int qd = warp & 3, half = warp >> 2;
-    const int t = qd * 32 + (threadIdx.x & 31);  // key row within the tile == TMEM lane
-    const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
+    const int t = (warp & 3) * 32 + (threadIdx.x & 31);  // key row within the tile == TMEM lane
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    // query chunks of 32 this warp owns: both (4 warps) or chunk warp/4 (8 warps)
+    const int cc_lo = NSMW == 8 ? warp >> 2 : 0, cc_hi = NSMW == 8 ? cc_lo + 1 : 2;
     const float sl2 = a.scale * kLog2e;
     const int c = n0 + t;
     for (int it = 0; it < T; ++it) {
       const int b = it & 1;
-      const int m0 = m_begin + (it % nqt) * BQ + 32 * half;
-      const int lb = (it % NST) * 64 + 32 * half;  // this half's lse/delta slot
-      int ilo = 0, ihi = min(32, P.nq - m0);
+      const int m0 = m_begin + (it % nqt) * BQ;
+      const int lb = (it % NST) * 64;  // this tile's lse/delta slot (complete once S^T is)
+      if (warp == 0 && t == 0) TR(8, it);
+      int ilo = 0, ihi = min(BQ, P.nq - m0);
       if (c >= P.nk) ihi = 0;
       if (P.causal) ilo = max(0, c - P.off - m0);
-      const bool full = ilo <= 0 && ihi >= 32;
-      tc::mbar_wait(bar(E_HF + half), it & 1);
-      if (it >= 2) tc::mbar_wait(bar(E_MD + b), ((it - 2) >> 1) & 1);  // dS^T buffer b free
+      const bool full = ilo <= 0 && ihi >= BQ;
+      tc::mbar_wait(bar(E_SF + b), (it >> 1) & 1);
+      tc::mbar_wait(bar(E_DPF + b), (it >> 1) & 1);
+      if (it >= 2) tc::mbar_wait(bar(E_MD + b), ((it - 2) >> 1) & 1);  // dS^T_b read by dK/dQ
       tc::fence_after();
-      uint32_t rs[32], rp[32];
-      tc::tmem_ld32(tmem + lane_base + T_S + 32 * half, rs);
-      tc::tmem_ld32(tmem + lane_base + T_DP + 32 * half, rp);
+      if (warp == 0 && t == 0) TR(9, it);
+      const uint32_t ds = sdS + b * 16384;
+      // both 32-query chunks of S^T / dP^T are loaded up front; chunk 1's loads fly while
+      // chunk 0 is computed (one TMEM round trip per tile instead of two)
+      uint32_t rs[2][32], rp[2][32];
+      tc::tmem_ld32(tmem + lane_base + 64 * b + cc_lo * 32, rs[cc_lo]);
+      tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + cc_lo * 32, rp[cc_lo]);
       tc::tmem_wait_ld();
-      tc::reg_fence(rs);
-      tc::reg_fence(rp);
-      const float2* nl2 = reinterpret_cast<const float2*>(sL + lb);
-      const float2* dl2 = reinterpret_cast<const float2*>(sDl + lb);
-      uint32_t wp[16], wd[16];
-      if (full)
-        grad_half<false>(rs, rp, nl2, dl2, sl2, a.scale, 0, 32, wp, wd);
-      else
-        grad_half<true>(rs, rp, nl2, dl2, sl2, a.scale, ilo, ihi, wp, wd);
-      tc::tmem_st16(tmem + lane_base + T_S + 32 * half, wp);       // P^T_h: A operand of dV
-      tc::tmem_st16(tmem + lane_base + T_S + 32 * half + 16, wd);  // dS^T_h: A operand of dK
-      const uint32_t ds = sdS + b * 16384;                          // dS^T_h: B operand of dQ^T
+      tc::reg_fence(rs[cc_lo]);
+      tc::reg_fence(rp[cc_lo]);
+      if ((SV & 1) && NSMW == 4) {
+        tc::tmem_ld32(tmem + lane_base + 64 * b + 32, rs[1]);
+        tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, rp[1]);
+      }
+      const float2* lse2 = reinterpret_cast<const float2*>(sL + lb);   // -lse*log2e per query
+      const float2* dl2 = reinterpret_cast<const float2*>(sDl + lb);   // delta per query
+      const uint64_t sl2x2 = f2_pack(sl2, sl2), sc2 = f2_pack(a.scale, a.scale);
+      constexpr bool PK = SV & 2, PO = SV & 8;
+      uint32_t wds[16];  // (SV & 64) chunk 0's dS^T, parked until chunk 1's S^T is out of TMEM
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t addr = tc::sw128(ds, t, half * 4 + k);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(wd[4 * k]), "r"(wd[4 * k + 1]),
-                     "r"(wd[4 * k + 2]), "r"(wd[4 * k + 3]));
+      for (int cc = cc_lo; cc < cc_hi; ++cc) {
+        if (NSMW == 4 && cc == 1) {
+          if (!(SV & 1)) {
+            tc::tmem_ld32(tmem + lane_base + 64 * b + 32, rs[1]);
+            tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, rp[1]);
+          }
+          tc::tmem_wait_ld();
+          tc::reg_fence(rs[1]);
+          tc::reg_fence(rp[1]);
+          if constexpr ((SV & 64) != 0) tc::tmem_st16(tmem + lane_base + 64 * b + 32, wds);
+        }
+        uint32_t wp[16], wd[16];
+        if (BWD_DBG(16)) {  // profiling: no softmax-gradient math (wrong results)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) wp[i] = rs[cc][i] ^ rp[cc][i], wd[i] = rs[cc][i + 16] ^ rp[cc][i + 16];
+        } else if ((SV & 4) && full) {
+          grad_chunk<false, PK, PO>(rs[cc], rp[cc], lse2 + cc * 16, dl2 + cc * 16, sl2x2, sc2, 0, 0, wp, wd);
+        } else {
+          grad_chunk<true, PK, PO>(rs[cc], rp[cc], lse2 + cc * 16, dl2 + cc * 16, sl2x2, sc2, ilo - cc * 32,
+                                   ihi - cc * 32, wp, wd);
+        }
+        tc::tmem_st16(tmem + lane_base + 64 * b + cc * 16, wp);
+        if constexpr ((SV & 64) != 0) {
+          if (cc == 0) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) wds[i] = wd[i];
+          } else {
+            tc::tmem_st16(tmem + lane_base + 64 * b + 48, wd);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t addr = tc::sw128(ds, t, cc * 4 + k);
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(wd[4 * k]),
+                       "r"(wd[4 * k + 1]), "r"(wd[4 * k + 2]), "r"(wd[4 * k + 3]));
+        }
       }
       tc::tmem_wait_st();
       tc::fence_proxy_async();
       tc::fence_before();
-      tc::mbar_arrive(bar(E_PR + half));
+      tc::mbar_arrive(bar(E_PR + b));
+      if (warp == 0 && t == 0) TR(10, it);
     }
-    // dV epilogue: each half's warps own 64 of the 128 columns
+    constexpr int NC = D / 32 / (NSMW / 4);  // 32-column chunks of dV per warp
+    const int cc0 = NSMW == 8 ? (warp >> 2) * NC : 0;
     __nv_bfloat16* dvb = a.dv_bf16 ? reinterpret_cast<__nv_bfloat16*>(a.dv_bf16) +
                                          (int64_t)(P.k_row0 + c) * a.dkv_bf16_row_stride + kvh * D
                                    : nullptr;
-    if (T > 0) {
+    if (T > 0) {  // dV epilogue
       tc::mbar_wait(bar(E_FIN), 0);
       tc::fence_after();
       float* dv = a.dv_acc + (int64_t)(P.k_row0 + c) * a.dkv_row_stride + kvh * D;
 #pragma unroll
-      for (int ci = 0; ci < 2; ++ci) {
-        const int cc = half * 2 + ci;
+      for (int ci = 0; ci < NC; ++ci) {
+        const int cc = cc0 + ci;
         uint32_t r[32];
-        tc::tmem_ld32(tmem + lane_base + T_DV + cc * 32, r);
+        tc::tmem_ld32(tDV + lane_base + cc * 32, r);
         tc::tmem_wait_ld();
         if (c < P.nk) {
           if (dvb) {
@@ -365,48 +443,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else if (dvb && c < P.nk) {  // no query sees this key tile: dV = 0
       uint32_t z[32] = {};
 #pragma unroll
-      for (int ci = 0; ci < 2; ++ci) store_bf16x32(dvb + (half * 2 + ci) * 32, z);
+      for (int ci = 0; ci < NC; ++ci) store_bf16x32(dvb + (cc0 + ci) * 32, z);
     }
   } else if (warp >= DRAIN0 && warp < DRAIN0 + 4) {
     // ------------------------------------------- dQ warpgroup (lane = head-dim index)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_DQ));
     const int w = warp - DRAIN0, lane = threadIdx.x % 32;
     const uint32_t lane_base = (uint32_t)(w * 32) << 16;
-    if (T > 0) {
-      // K and V rows (this thread's key row = TMEM lane) from the swizzled smem tiles into TMEM:
-      // column 32b + 4j + i holds the bf16 pair (64b + 8j + 2i, +1), the TS A-operand layout
-      tc::mbar_wait(bar(E_KV), 0);
-      const int t = w * 32 + lane;
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const uint32_t src = m == 0 ? sK : sV;
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          uint32_t r[32];
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
-                         : "=r"(r[4 * j]), "=r"(r[4 * j + 1]), "=r"(r[4 * j + 2]), "=r"(r[4 * j + 3])
-                         : "r"(tc::sw128(src + b * 16384, t, j)));
-          tc::tmem_st32(tmem + lane_base + (m == 0 ? T_K : T_V) + 32 * b, r);
-        }
-      }
-      tc::tmem_wait_st();
-      tc::fence_before();
-      tc::mbar_arrive(bar(E_KVT));
-    }
     const uint32_t stg0 = sStg + w * NSTG * 8192;  // NSTG x [64 queries x 32 fp32], 128B-swizzled rows
     for (int it = 0; it < T; ++it) {
       const int b = it & 1;
       const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * BQ;
       tc::mbar_wait(bar(E_MD + b), (it >> 1) & 1);
       tc::fence_after();
+      if (w == 0 && lane == 0) TR(11, it);
       uint32_t r[2][32];
-      tc::tmem_ld32(tmem + lane_base + T_DP, r[0]);
-      tc::tmem_ld32(tmem + lane_base + T_DP + 32, r[1]);
+      tc::tmem_ld32(tmem + lane_base + 128 + 64 * b, r[0]);
+      tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, r[1]);
       tc::tmem_wait_ld();
       tc::fence_before();
       tc::mbar_arrive(bar(E_DQF + b));
+      if (w == 0 && lane == 0) TR(12, it);
+      // (per-lane red.global.add.f32 from registers measured 1.8x slower than this staging, and
+      // a quad-transpose via shuffles + red.global.add.v4.f32 1.6x slower: 3620 vs 2229 cycles
+      // per iteration — the L2 atomics, not the smem traffic, would bound it)
+      if (BWD_DBG(32)) continue;  // profiling: no dQ staging / reduce (wrong dq)
       const uint32_t stg = stg0 + (it % NSTG) * 8192;
       if (lane == 0) tc::bulk_wait_read<NSTG - 1>();  // the slot's previous reduce has read it
       __syncwarp();
@@ -417,10 +478,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       tc::fence_proxy_async();
       __syncwarp();
-      if (lane == 0) {
+      if (lane == 0 && !BWD_DBG(1)) {
         tc::tma_reduce_add_2d(&tmDQ, stg, h * D + w * 32, P.q_row0 + m0);
         tc::bulk_commit();
       }
+      if (w == 0 && lane == 0) TR(13, it);
     }
     if (lane == 0) tc::bulk_wait_read<0>();
     const int ck = n0 + w * 32 + lane;
@@ -434,7 +496,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t r[32];
-        tc::tmem_ld32(tmem + lane_base + T_DK + cc * 32, r);
+        tc::tmem_ld32(tDK + lane_base + cc * 32, r);
         tc::tmem_wait_ld();
         if (ck < P.nk) {
           if (dkb) {
@@ -456,7 +518,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc::fence_before();
   __syncthreads();
   if (warp == TALLOCW) tc::tmem_dealloc<512>(tmem);
-#undef TR
 }
 
 int max_rows(const ProblemSet& ps, bool q) {
@@ -467,7 +528,7 @@ int max_rows(const ProblemSet& ps, bool q) {
 
 }  // namespace
 
-long long* g_bwd_trace = nullptr;  // profiling (spattn_debug_bwd_trace): clock64 events of CTA 0
+long long* g_bwd_trace = nullptr;  // profiling (spattn_debug_bwd_trace)
 void set_bwd_trace(void* p) { g_bwd_trace = static_cast<long long*>(p); }
 
 bool tc_bwd_q64_supported(const BwdArgs& a) {
@@ -480,7 +541,11 @@ bool tc_bwd_q64_supported(const BwdArgs& a) {
 void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
   ProblemSet ps = in;
   BwdArgs args = a;
+#ifdef SPATTN_PROFILING
+  args.debug = getenv("SPATTN_DEBUG") ? atoi(getenv("SPATTN_DEBUG")) : 0;
+#else
   args.debug = 0;
+#endif
   args.trace = g_bwd_trace;
   ps.tile_prefix[0] = 0;
   for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nk + 127) / 128;
