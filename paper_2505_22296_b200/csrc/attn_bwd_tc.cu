@@ -1,4 +1,4 @@
-// tcgen05 attention backward for head_dim 128 with 64-row query tiles (sm_100a).
+// tcgen05 attention backward with 64-row query tiles, head_dim 64 or 128 (sm_100a).
 //
 // One CTA = one 128-row key/value tile x one kv head; it loops over every (query head of the
 // GQA group, 64-row query tile) that sees the tile. TMEM (512 columns, lane = key row unless
@@ -6,9 +6,10 @@
 // dV/dK/dQ MMAs of tile i-1:
 //   S^T_b  = K Q^T          cols [64b, 64b+64)        P^T_b (bf16) written back over it
 //   dP^T_b = V dO^T         cols [128+64b, +64)        dQ^T_b (lane = head-dim index) reuses it
-//   dV    += P^T_b dO       cols [256, 384)            (A operand from TMEM)
-//   dK    += dS^T_b Q       cols [384, 512)            (dS^T from swizzled smem)
-//   dQ^T_b = K^T dS^T_b     M = head dim 128, N = 64 queries, K = 128 keys
+//   dV    += P^T_b dO       cols [256, 256+D)          (A operand from TMEM)
+//   dK    += dS^T_b Q       cols [256+D, 256+2D)       (A operand from TMEM: dS^T_b)
+//   dQ^T_b = K^T dS^T_b     M = 128 (head dim; for D = 64 rows 64-127 are padding that reads
+//                           the V tile and is never drained), N = 64 queries, K = 128 keys
 // MMA issue order: S(i), dP(i), [dV dK dQ](i-1), S(i+1), ... The dQ warpgroup drains dQ^T
 // (warp w owns head-dim columns 32w..32w+31) through an 8 KB smem slot per warp into the fp32
 // accumulator with TMA reduce-add. attn_block_backward (attention.cpp:167-216).
@@ -23,51 +24,55 @@
 namespace spattn {
 namespace {
 
-constexpr int D = 128;
 constexpr int BQ = 64;
-#ifndef BWD_NST
-#define BWD_NST 3
-#endif
-#ifndef BWD_NSTG
-#define BWD_NSTG 1
-#endif
-#ifndef BWD_SMW
-#define BWD_SMW 4
-#endif
-constexpr int NST = BWD_NST;                // Q/dO pipeline stages
-// Softmax-gradient warps: 4 (one per TMEM lane quadrant, 64 queries per thread) or 8 (two per
-// quadrant, 32 queries each: two warps per SMSP hide each other's latency chains).
-constexpr int NSMW = BWD_SMW;
-constexpr int DRAIN0 = NSMW;               // first of the 4 dQ drain warps
-constexpr int PRODW = DRAIN0 + 4, TALLOCW = PRODW + 1, MMAW = PRODW + 3;
-constexpr int NTHREADS = (PRODW + 4) * 32;
-// registers per thread: softmax / drain / control, sum over warps <= 2048
-constexpr int REG_SM = NSMW == 4 ? 232 : 160, REG_DQ = NSMW == 4 ? 120 : 96, REG_CTL = NSMW == 4 ? 152 : 96;
-static_assert(NSMW * REG_SM + 4 * REG_DQ + 4 * REG_CTL <= 2048, "register budget");
-constexpr int NSTG = BWD_NSTG;              // dQ staging slots per drain warp
-constexpr int KV_TILE = 128 * D * 2;        // 32 KB (two 16 KB column blocks)
-constexpr int Q_TILE = BQ * D * 2;          // 16 KB (two 8 KB column blocks)
-constexpr int K_OFF = 0, V_OFF = KV_TILE;
-constexpr int Q_OFF = 2 * KV_TILE;          // NST x Q tile
-constexpr int DO_OFF = Q_OFF + NST * Q_TILE;
-constexpr int DS_OFF = DO_OFF + NST * Q_TILE;    // 2 x [128 keys x 64 queries] bf16 (16 KB each)
-constexpr int STG_OFF = DS_OFF + 2 * 16384;      // 4 warps x NSTG x [64 queries x 32 fp32] (8 KB)
-constexpr int LD_OFF = STG_OFF + 4 * NSTG * 8192;  // lse*log2e, delta: [NST][64] each
-constexpr int BAR_OFF = LD_OFF + 2 * NST * 64 * 4;
+// Warp roles: NSMW softmax-gradient warps (4: one per TMEM lane quadrant, 64 queries per thread;
+// 8 — two per quadrant, one 32-query chunk each — measured no faster for either head dim:
+// 711 vs 746 TFLOP/s at d=64, L=32K), 4 dQ drain warps, the TMA producer, the TMEM allocator and
+// (last) the MMA issuer.
+template <int D>
+struct Roles {
+  static constexpr int NSMW = 4;
+  static constexpr int DRAIN0 = NSMW;
+  static constexpr int PRODW = DRAIN0 + 4, TALLOCW = PRODW + 1, MMAW = PRODW + 3;
+  static constexpr int NTHREADS = (PRODW + 4) * 32;
+  // registers per thread: softmax / drain / control, sum over warps <= 2048
+  static constexpr int REG_SM = NSMW == 4 ? 232 : 160, REG_DQ = NSMW == 4 ? 120 : 96,
+                       REG_CTL = NSMW == 4 ? 152 : 96;
+  static_assert(NSMW * REG_SM + 4 * REG_DQ + 4 * REG_CTL <= 2048, "register budget");
+};
+constexpr int NSTG = 1;                     // dQ staging slots per drain warp
 
 enum {
   E_KV = 0,
-  E_QF = 1,                 // [NST]
-  E_QE = E_QF + NST,        // [NST]
-  E_SF = E_QE + NST,        // [2]
+  E_QF = 1,                 // [NST_MAX]
+  E_QE = E_QF + 4,          // [NST_MAX]
+  E_SF = E_QE + 4,          // [2]
   E_DPF = E_SF + 2,         // [2]
-  E_PR = E_DPF + 2,         // [2] 128 arrivals
+  E_PR = E_DPF + 2,         // [2] 32 * NSMW arrivals
   E_MD = E_PR + 2,          // [2]
   E_DQF = E_MD + 2,         // [2] 128 arrivals
   E_FIN = E_DQF + 2,
   E_N = E_FIN + 1
 };
-constexpr int SMEM = BAR_OFF + E_N * 8 + 16;
+
+// Shared-memory layout per head dim (128-byte-swizzled 64-column blocks: 16 KB per 128 K/V rows,
+// 8 KB per 64 Q/dO rows). head_dim 64 has room for a deeper Q/dO pipeline.
+template <int D>
+struct Q64 {
+  static constexpr int NB = D / 64;                 // 64-column blocks per row
+  static constexpr int NST = D == 64 ? 4 : 3;       // Q/dO pipeline stages
+  static constexpr int KV_TILE = 128 * D * 2;
+  static constexpr int Q_TILE = BQ * D * 2;
+  static constexpr int K_OFF = 0, V_OFF = KV_TILE;
+  static constexpr int Q_OFF = 2 * KV_TILE;
+  static constexpr int DO_OFF = Q_OFF + NST * Q_TILE;
+  static constexpr int DS_OFF = DO_OFF + NST * Q_TILE;    // 2 x [128 keys x 64 queries] bf16
+  static constexpr int STG_OFF = DS_OFF + 2 * 16384;      // 4 warps x NSTG x [64 queries x 32 fp32]
+  static constexpr int LD_OFF = STG_OFF + 4 * NSTG * 8192;  // lse*log2e, delta: [NST][64] each
+  static constexpr int BAR_OFF = LD_OFF + 2 * NST * 64 * 4;
+  static constexpr int SMEM = BAR_OFF + E_N * 8 + 16;
+  static_assert(NST <= 4, "barrier slots");
+};
 
 // 32 consecutive fp32 columns of one row -> 32 bf16 (4 x 16-byte stores)
 __device__ __forceinline__ void store_bf16x32(void* dst, const uint32_t (&r)[32]) {
@@ -129,11 +134,6 @@ __device__ __forceinline__ void grad_chunk(const uint32_t (&rs)[32], const uint3
   }
 }
 
-// SV: variant bits of the softmax-gradient code (fixed at 64: dS^T also stored to TMEM so dK is
-// a TS MMA, 2300 -> 2245 cycles per iteration). Measured no faster and removed from the build:
-// 1 prefetch chunk 1's TMEM loads, 2 packed fp32x2 math, 4 separate full / masked code paths,
-// 8 FMA-pipe exp2 for 1 pair in 4.
-constexpr int SV = 64;
 // Profiling switches (wrong results by design) exist only in -DSPATTN_PROFILING builds.
 #ifdef SPATTN_PROFILING
 #define BWD_DBG(bit) ((a.debug & (bit)) != 0)
@@ -141,10 +141,18 @@ constexpr int SV = 64;
 #define BWD_DBG(bit) false
 #endif
 
-__global__ void __launch_bounds__(NTHREADS, 1)
+template <int D>
+__global__ void __launch_bounds__(Roles<D>::NTHREADS, 1)
     attn_bwd_tc_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                            const __grid_constant__ CUtensorMap tmDQ, BwdArgs a, ProblemSet ps) {
+  using L = Q64<D>;
+  using R = Roles<D>;
+  constexpr int NSMW = R::NSMW, DRAIN0 = R::DRAIN0, PRODW = R::PRODW, TALLOCW = R::TALLOCW, MMAW = R::MMAW,
+                REG_SM = R::REG_SM, REG_DQ = R::REG_DQ, REG_CTL = R::REG_CTL;
+  constexpr int NST = L::NST, KV_TILE = L::KV_TILE, Q_TILE = L::Q_TILE, K_OFF = L::K_OFF, V_OFF = L::V_OFF,
+                Q_OFF = L::Q_OFF, DO_OFF = L::DO_OFF, DS_OFF = L::DS_OFF, STG_OFF = L::STG_OFF,
+                LD_OFF = L::LD_OFF, BAR_OFF = L::BAR_OFF, NB = L::NB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   if (sbase & 1023) __trap();
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tDV = tmem + 256, tDK = tmem + 384;
+  const uint32_t tDV = tmem + 256, tDK = tmem + 256 + D;
   if (warp >= PRODW) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_CTL));
 
   // Roles. The scheduler favours the highest warp id, so the single-thread MMA issuer is the
@@ -214,7 +222,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (T > 0) {
       if (lane == 0) {
         tc::mbar_expect_tx(bar(E_KV), 2 * KV_TILE);
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NB; ++b) {
           tc::tma_load_2d(sK + b * 16384, &tmK, kvh * D + b * 64, P.k_row0 + n0, bar(E_KV));
           tc::tma_load_2d(sV + b * 16384, &tmV, kvh * D + b * 64, P.k_row0 + n0, bar(E_KV));
         }
@@ -244,7 +252,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0) {
           TR(15, it);
           tc::mbar_expect_tx(bar(E_QF + st), 2 * Q_TILE);
-          for (int b = 0; b < 2; ++b) {
+          for (int b = 0; b < NB; ++b) {
             tc::tma_load_2d(sQ + st * Q_TILE + b * 8192, &tmQ, h * D + b * 64, P.q_row0 + m0, bar(E_QF + st));
             tc::tma_load_2d(sdO + st * Q_TILE + b * 8192, &tmDO, h * D + b * 64, P.q_row0 + m0, bar(E_QF + st));
           }
@@ -271,23 +279,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::mbar_wait(bar(E_PR + b), (i >> 1) & 1);
         TR(6, i);
         tc::fence_after();
+        // P^T / dS^T of query chunk c (32 queries) sit in that chunk's own S^T columns:
+        // P^T at [64b + 32c, +16), dS^T at [64b + 32c + 16, +16) (16 queries = 8 columns per K step)
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk)
-          tc::mma_ts(tDV, tmem + 64 * b + kk * 8, tc::sdesc(dO + kk * 2048, 8192, 1024), id_kv,
-                     (i > 0 || kk > 0) ? 1u : 0u);
-        if constexpr ((SV & 64) != 0) {
-          // dS^T also sits in TMEM (the dead upper half of the S^T buffer): dK is a TS MMA and
-          // reads no A operand from shared memory
+          tc::mma_ts(tDV, tmem + 64 * b + (kk >> 1) * 32 + (kk & 1) * 8, tc::sdesc(dO + kk * 2048, 8192, 1024),
+                     id_kv, (i > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk)
-            tc::mma_ts(tDK, tmem + 64 * b + 32 + kk * 8, tc::sdesc(q + kk * 2048, 8192, 1024), id_kv,
-                       (i > 0 || kk > 0) ? 1u : 0u);
-        } else {
-#pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk)
-            tc::mma_ss(tDK, tc::sdesc(ds + kk * 32, 16, 1024), tc::sdesc(q + kk * 2048, 8192, 1024), id_kv,
-                       (i > 0 || kk > 0) ? 1u : 0u);
-        }
+        for (int kk = 0; kk < BQ / 16; ++kk)
+          tc::mma_ts(tDK, tmem + 64 * b + (kk >> 1) * 32 + 16 + (kk & 1) * 8, tc::sdesc(q + kk * 2048, 8192, 1024),
+                     id_kv, (i > 0 || kk > 0) ? 1u : 0u);
         tc::commit(bar(E_QE + st));
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
@@ -346,63 +347,38 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       int ilo = 0, ihi = min(BQ, P.nq - m0);
       if (c >= P.nk) ihi = 0;
       if (P.causal) ilo = max(0, c - P.off - m0);
-      const bool full = ilo <= 0 && ihi >= BQ;
       tc::mbar_wait(bar(E_SF + b), (it >> 1) & 1);
       tc::mbar_wait(bar(E_DPF + b), (it >> 1) & 1);
       if (it >= 2) tc::mbar_wait(bar(E_MD + b), ((it - 2) >> 1) & 1);  // dS^T_b read by dK/dQ
       tc::fence_after();
       if (warp == 0 && t == 0) TR(9, it);
       const uint32_t ds = sdS + b * 16384;
-      // both 32-query chunks of S^T / dP^T are loaded up front; chunk 1's loads fly while
-      // chunk 0 is computed (one TMEM round trip per tile instead of two)
-      uint32_t rs[2][32], rp[2][32];
-      tc::tmem_ld32(tmem + lane_base + 64 * b + cc_lo * 32, rs[cc_lo]);
-      tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + cc_lo * 32, rp[cc_lo]);
-      tc::tmem_wait_ld();
-      tc::reg_fence(rs[cc_lo]);
-      tc::reg_fence(rp[cc_lo]);
-      if ((SV & 1) && NSMW == 4) {
-        tc::tmem_ld32(tmem + lane_base + 64 * b + 32, rs[1]);
-        tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, rp[1]);
-      }
+      // chunk c (32 queries) of S^T / dP^T: the first chunk is loaded up front, the second (4
+      // warps) after the first is computed; each chunk's P^T / dS^T go back into its own S^T
+      // columns, which its loads have already emptied
       const float2* lse2 = reinterpret_cast<const float2*>(sL + lb);   // -lse*log2e per query
-      const float2* dl2 = reinterpret_cast<const float2*>(sDl + lb);   // delta per query
+      const float2* dl2 = reinterpret_cast<const float2*>(sDl + lb);   // -delta*scale per query
       const uint64_t sl2x2 = f2_pack(sl2, sl2), sc2 = f2_pack(a.scale, a.scale);
-      constexpr bool PK = SV & 2, PO = SV & 8;
-      uint32_t wds[16];  // (SV & 64) chunk 0's dS^T, parked until chunk 1's S^T is out of TMEM
 #pragma unroll
       for (int cc = cc_lo; cc < cc_hi; ++cc) {
-        if (NSMW == 4 && cc == 1) {
-          if (!(SV & 1)) {
-            tc::tmem_ld32(tmem + lane_base + 64 * b + 32, rs[1]);
-            tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + 32, rp[1]);
-          }
-          tc::tmem_wait_ld();
-          tc::reg_fence(rs[1]);
-          tc::reg_fence(rp[1]);
-          if constexpr ((SV & 64) != 0) tc::tmem_st16(tmem + lane_base + 64 * b + 32, wds);
-        }
+        uint32_t rs[32], rp[32];
+        tc::tmem_ld32(tmem + lane_base + 64 * b + cc * 32, rs);
+        tc::tmem_ld32(tmem + lane_base + 128 + 64 * b + cc * 32, rp);
+        tc::tmem_wait_ld();
+        tc::reg_fence(rs);
+        tc::reg_fence(rp);
         uint32_t wp[16], wd[16];
         if (BWD_DBG(16)) {  // profiling: no softmax-gradient math (wrong results)
 #pragma unroll
-          for (int i = 0; i < 16; ++i) wp[i] = rs[cc][i] ^ rp[cc][i], wd[i] = rs[cc][i + 16] ^ rp[cc][i + 16];
-        } else if ((SV & 4) && full) {
-          grad_chunk<false, PK, PO>(rs[cc], rp[cc], lse2 + cc * 16, dl2 + cc * 16, sl2x2, sc2, 0, 0, wp, wd);
+          for (int i = 0; i < 16; ++i) wp[i] = rs[i] ^ rp[i], wd[i] = rs[i + 16] ^ rp[i + 16];
         } else {
-          grad_chunk<true, PK, PO>(rs[cc], rp[cc], lse2 + cc * 16, dl2 + cc * 16, sl2x2, sc2, ilo - cc * 32,
-                                   ihi - cc * 32, wp, wd);
+          grad_chunk<true, false, false>(rs, rp, lse2 + cc * 16, dl2 + cc * 16, sl2x2, sc2, ilo - cc * 32,
+                                         ihi - cc * 32, wp, wd);
         }
-        tc::tmem_st16(tmem + lane_base + 64 * b + cc * 16, wp);
-        if constexpr ((SV & 64) != 0) {
-          if (cc == 0) {
+        tc::tmem_st16(tmem + lane_base + 64 * b + cc * 32, wp);       // P^T: A operand of dV
+        tc::tmem_st16(tmem + lane_base + 64 * b + cc * 32 + 16, wd);  // dS^T: A operand of dK
 #pragma unroll
-            for (int i = 0; i < 16; ++i) wds[i] = wd[i];
-          } else {
-            tc::tmem_st16(tmem + lane_base + 64 * b + 48, wd);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < 4; ++k) {  // dS^T: B operand of dQ^T
           const uint32_t addr = tc::sw128(ds, t, cc * 4 + k);
           asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(wd[4 * k]),
                        "r"(wd[4 * k + 1]), "r"(wd[4 * k + 2]), "r"(wd[4 * k + 3]));
@@ -468,6 +444,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // a quad-transpose via shuffles + red.global.add.v4.f32 1.6x slower: 3620 vs 2229 cycles
       // per iteration — the L2 atomics, not the smem traffic, would bound it)
       if (BWD_DBG(32)) continue;  // profiling: no dQ staging / reduce (wrong dq)
+      if (w * 32 >= D) continue;  // head_dim 64: lanes 64-127 of the M=128 dQ^T MMA are padding
       const uint32_t stg = stg0 + (it % NSTG) * 8192;
       if (lane == 0) tc::bulk_wait_read<NSTG - 1>();  // the slot's previous reduce has read it
       __syncwarp();
@@ -533,12 +510,13 @@ void set_bwd_trace(void* p) { g_bwd_trace = static_cast<long long*>(p); }
 
 bool tc_bwd_q64_supported(const BwdArgs& a) {
   auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
-  return a.d == D && al(a.q) && al(a.k) && al(a.v) && al(a.dout) && al(a.dq_acc) &&
+  return (a.d == 64 || a.d == 128) && al(a.q) && al(a.k) && al(a.v) && al(a.dout) && al(a.dq_acc) &&
          (a.q_row_stride * 2) % 16 == 0 && (a.kv_row_stride * 2) % 16 == 0 &&
          a.o_row_stride == a.q_row_stride && (a.dq_row_stride * 4) % 16 == 0 && a.dkv_row_stride % 4 == 0;
 }
 
-void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
+template <int D>
+void launch_q64_d(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
   ProblemSet ps = in;
   BwdArgs args = a;
 #ifdef SPATTN_PROFILING
@@ -558,9 +536,16 @@ void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t
       !make_tma_2d(&tv, a.v, kw, krows, kw, 128) || !make_tma_2d(&tdo, a.dout, qw, qrows, qw, BQ) ||
       !make_tma_2d_f32(&tdq, a.dq_acc, (uint64_t)a.hm.hq * D, qrows, (uint64_t)a.dq_row_stride, BQ))
     launch_error("attn_bwd_tc_q64", "TMA descriptor encode failed (q/k/v/dout/dq base, strides or extents)");
-  ensure_smem_for(attn_bwd_tc_q64_kernel, SMEM);
-  attn_bwd_tc_q64_kernel<<<dim3(tiles * a.hm.hkv), NTHREADS, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
+  ensure_smem_for(attn_bwd_tc_q64_kernel<D>, Q64<D>::SMEM);
+  attn_bwd_tc_q64_kernel<D><<<dim3(tiles * a.hm.hkv), Roles<D>::NTHREADS, Q64<D>::SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
   note_launch();
+}
+
+void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
+  if (a.d == 64)
+    launch_q64_d<64>(a, in, s);
+  else
+    launch_q64_d<128>(a, in, s);
 }
 
 }  // namespace spattn
