@@ -688,352 +688,5 @@ void launch_attn_fwd_tc(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s) 
   else
     launch_fwd_tc_d<128>(a, ps, s);
 }
-// =================================================================================
-// Backward: one CTA = one 128-row key/value tile x one kv head; it loops over every
-// (query head of the GQA group, 128-row query tile) that sees the tile. Per iteration:
-//   S^T  = K Q^T      (TMEM cols [0,128): lane = key row, col = query)
-//   dP^T = V dO^T     (TMEM cols [128,256))
-//   threads: P^T = exp2(S^T*scale*log2e - lse*log2e) -> bf16 back into TMEM cols [0,64)
-//            dS^T = P^T (dP^T - delta)              -> bf16 smem (128B-swizzled, [key][query])
-//   dV += P^T dO      (A from TMEM)                  TMEM cols [256, 256+D)
-//   dK += dS^T Q      (A = dS^T K-major)             TMEM cols [256+D, 256+2D)
-//   dQ  = dS K        (A = dS^T read MN-major)       TMEM cols [128,128+D) -> fp32 vector
-//                                                    atomics into dq_acc (scaled)
-// dK, dV are reduced into fp32 accumulators once at the end (several problems or ring steps
-// may share key rows). attn_block_backward (attention.cpp:167-216), ds scaled by `scale`.
-namespace {
-
-template <int D>
-struct BwdLayout {
-  static constexpr int QB = D / 64;
-  static constexpr int TILE = 128 * D * 2;
-  static constexpr int K_OFF = 0;
-  static constexpr int V_OFF = TILE;
-  static constexpr int Q_OFF = 2 * TILE;   // 2 stages
-  static constexpr int DO_OFF = 4 * TILE;  // 2 stages
-  static constexpr int DS_OFF = 6 * TILE;  // 128 x 128 bf16
-  static constexpr int LD_OFF = DS_OFF + 32768;
-  static constexpr int BAR_OFF = LD_OFF + 2048;
-  static constexpr int SMEM = BAR_OFF + 128;
-};
-
-enum BwdBar { C_KV = 0, C_QF = 1, C_QE = 3, C_SF = 5, C_DPF = 6, C_PR = 7, C_MD = 8, C_DQF = 9, C_FIN = 10, C_DQS = 11, C_N = 13 };
-
-__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
-
-template <int D>
-__global__ void __launch_bounds__(384, 1)
-    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                       const __grid_constant__ CUtensorMap tmDQ, BwdArgs a, ProblemSet ps) {
-  using Lay = BwdLayout<D>;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const uint32_t sbase = smem_u32(smem);
-  if (sbase & 1023) __trap();  // the swizzled operand tiles need 1024-byte alignment
-  const uint32_t sK = sbase + Lay::K_OFF, sV = sbase + Lay::V_OFF, sQ = sbase + Lay::Q_OFF,
-                 sdO = sbase + Lay::DO_OFF, sdS = sbase + Lay::DS_OFF;
-  float* sL = reinterpret_cast<float*>(smem + Lay::LD_OFF);  // [2][128] lse * log2e
-  float* sDl = sL + 256;                                     // [2][128] delta
-  const uint32_t bars = sbase + Lay::BAR_OFF;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Lay::BAR_OFF + C_N * 8);
-  auto bar = [&](int i) { return bars + 8u * i; };
-
-  const int warp = threadIdx.x / 32;
-  const int pi = find_problem(ps, (int)blockIdx.x);
-  const AttnProblem P = ps.p[pi];
-  const int n0 = (blockIdx.x - ps.tile_prefix[pi]) * 128;
-  const int kvh = blockIdx.y;
-  const HeadMap hm = a.hm;
-  const int g_lo = (kvh + hm.kv_head_base) * hm.rep;
-  const int h_lo = max(0, g_lo - hm.q_head_base);
-  const int h_hi = min(hm.hq, g_lo + hm.rep - hm.q_head_base);
-  int m_begin = 0;
-  if (P.causal) m_begin = max(0, n0 - P.off) / 128 * 128;
-  const bool none = (P.causal && n0 - P.off > P.nq - 1) || h_hi <= h_lo || m_begin >= P.nq;
-  const int nqt = none ? 0 : (P.nq - m_begin + 127) / 128;
-  const int T = none ? 0 : (h_hi - h_lo) * nqt;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < C_N; ++i) tc::mbar_init(bar(i), (i == C_PR || i == C_DQF || i == C_DQS || i == C_DQS + 1) ? 128 : 1);
-    tc::fence_barrier_init();
-  }
-  if (warp == 2) tc::tmem_alloc<512>(smem_u32(tmem_slot));
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 256 + D;
-  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
-
-  if (warp == 0) {
-    if (tc::elect_one() && T > 0) {
-      tc::mbar_expect_tx(bar(C_KV), 2 * Lay::TILE);
-      for (int b = 0; b < Lay::QB; ++b) {
-        tc::tma_load_2d(sK + b * 16384, &tmK, kvh * D + b * 64, P.k_row0 + n0, bar(C_KV));
-        tc::tma_load_2d(sV + b * 16384, &tmV, kvh * D + b * 64, P.k_row0 + n0, bar(C_KV));
-      }
-      for (int it = 0; it < T; ++it) {
-        const int st = it & 1;
-        const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * 128;
-        if (it >= 2) {
-          tc::mbar_wait(bar(C_QE + st), ((it - 2) >> 1) & 1);
-          tc::mbar_wait(bar(C_DQS + st), ((it - 2) >> 1) & 1);  // dQ tile it-2 staged here
-        }
-        tc::mbar_expect_tx(bar(C_QF + st), 2 * Lay::TILE);
-        for (int b = 0; b < Lay::QB; ++b) {
-          tc::tma_load_2d(sQ + st * Lay::TILE + b * 16384, &tmQ, h * D + b * 64, P.q_row0 + m0, bar(C_QF + st));
-          tc::tma_load_2d(sdO + st * Lay::TILE + b * 16384, &tmDO, h * D + b * 64, P.q_row0 + m0, bar(C_QF + st));
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (tc::elect_one() && T > 0) {
-      constexpr uint32_t id_s = tc::idesc_bf16(128, 128, false, false);
-      constexpr uint32_t id_kv = tc::idesc_bf16(128, D, false, true);
-      constexpr uint32_t id_q = tc::idesc_bf16(128, D, true, true);
-      tc::mbar_wait(bar(C_KV), 0);
-      for (int it = 0; it < T; ++it) {
-        const int st = it & 1;
-        const uint32_t q = sQ + st * Lay::TILE, dO = sdO + st * Lay::TILE;
-        tc::mbar_wait(bar(C_QF + st), (it >> 1) & 1);
-        tc::fence_after();
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-          tc::mma_ss(tS, tc::sdesc(sK + off, 16, 1024), tc::sdesc(q + off, 16, 1024), id_s, ks > 0);
-        }
-        tc::commit(bar(C_SF));
-        if (it > 0) {
-          tc::mbar_wait(bar(C_DQF), (it - 1) & 1);
-          tc::fence_after();
-        }
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-          tc::mma_ss(tDP, tc::sdesc(sV + off, 16, 1024), tc::sdesc(dO + off, 16, 1024), id_s, ks > 0);
-        }
-        tc::commit(bar(C_DPF));
-        tc::mbar_wait(bar(C_PR), it & 1);
-        tc::fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::mma_ts(tDV, tS + kk * 8, tc::sdesc(dO + kk * 2048, 16384, 1024), id_kv,
-                     (it > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::mma_ss(tDK, tc::sdesc(sdS + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                     tc::sdesc(q + kk * 2048, 16384, 1024), id_kv, (it > 0 || kk > 0) ? 1u : 0u);
-        tc::commit(bar(C_QE + st));
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::mma_ss(tDP, tc::sdesc(sdS + kk * 2048, 16384, 1024), tc::sdesc(sK + kk * 2048, 16384, 1024),
-                     id_q, kk > 0 ? 1u : 0u);
-        tc::commit(bar(C_MD));
-      }
-      tc::commit(bar(C_FIN));
-    }
-  } else if (warp >= 4 && warp < 8) {
-    // ---- softmax-gradient warpgroup: thread t = key row t (S^T / dP^T lane)
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n");
-    const int t = threadIdx.x - 128;
-    const uint32_t lane_base = (uint32_t)((warp - 4) * 32) << 16;
-    const float sl2 = a.scale * kLog2e;
-    const int c = n0 + t;
-    // lse/delta of the query rows of iteration `it`, prefetched one iteration ahead
-    auto fetch = [&](int it, float& l, float& dl) {
-      l = -INFINITY, dl = 0.f;
-      if (it >= T) return;
-      const int h = h_lo + it / nqt, row = m_begin + (it % nqt) * 128 + t;
-      if (row < P.nq) {
-        const int64_t g = (int64_t)(P.q_row0 + row) * a.lse_row_stride + h;
-        l = __ldg(a.lse + g);
-        dl = __ldg(a.delta + g);
-      }
-    };
-    float nl, ndl;
-    fetch(0, nl, ndl);
-    for (int it = 0; it < T; ++it) {
-      const int m0 = m_begin + (it % nqt) * 128;
-      const int ldb = (it & 1) * 128;
-      sL[ldb + t] = nl == -INFINITY ? INFINITY : nl * kLog2e;  // empty row: p = 0
-      sDl[ldb + t] = ndl;
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      fetch(it + 1, nl, ndl);
-      // admitted queries of key c within this tile: i in [ilo, ihi)
-      int ilo = 0, ihi = min(128, P.nq - m0);
-      if (c >= P.nk) ihi = 0;
-      if (P.causal) ilo = max(0, c - P.off - m0);
-      tc::mbar_wait(bar(C_SF), it & 1);
-      tc::mbar_wait(bar(C_DPF), it & 1);
-      // dS^T smem is free once the previous tile's dK/dQ MMAs are done with it
-      if (it > 0) tc::mbar_wait(bar(C_MD), (it - 1) & 1);
-      tc::fence_after();
-      const bool full = ilo <= 0 && ihi >= 128;
-      // 32 queries at a time: P (fp32) and dS from S^T, dP^T; P^T (bf16 pairs) back into the
-      // already-consumed S^T columns as the A operand of dV += P^T dO
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t rs[32], rp[32];
-        tc::tmem_ld32(tS + lane_base + cc * 32, rs);
-        tc::tmem_ld32(tDP + lane_base + cc * 32, rp);
-        tc::tmem_wait_ld();
-        uint32_t wp[16], wd[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int q0 = cc * 32 + 2 * i;
-          float p0 = fast_exp2(fmaf(__uint_as_float(rs[2 * i]), sl2, -sL[ldb + q0]));
-          float p1 = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), sl2, -sL[ldb + q0 + 1]));
-          if (!full) {
-            p0 = (q0 >= ilo && q0 < ihi) ? p0 : 0.f;
-            p1 = (q0 + 1 >= ilo && q0 + 1 < ihi) ? p1 : 0.f;
-          }
-          wp[i] = pack_bf16(p0, p1);
-          wd[i] = pack_bf16(p0 * (__uint_as_float(rp[2 * i]) - sDl[ldb + q0]),
-                            p1 * (__uint_as_float(rp[2 * i + 1]) - sDl[ldb + q0 + 1]));
-        }
-        tc::tmem_st16(tS + lane_base + cc * 16, wp);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int chunk = cc * 4 + k;  // 16-byte chunk of 8 queries
-          const uint32_t addr = tc::sw128(sdS + (chunk >> 3) * 16384, t, chunk & 7);
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(wd[4 * k]),
-                       "r"(wd[4 * k + 1]), "r"(wd[4 * k + 2]), "r"(wd[4 * k + 3]));
-        }
-      }
-      tc::tmem_wait_st();
-      tc::fence_proxy_async();
-      tc::fence_before();
-      tc::mbar_arrive(bar(C_PR));
-    }
-    if (T > 0) {  // dV epilogue (lane = key row)
-      tc::mbar_wait(bar(C_FIN), 0);
-      tc::fence_after();
-      float* dv = a.dv_acc + (int64_t)(P.k_row0 + c) * a.dkv_row_stride + kvh * D;
-#pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t r[32];
-        tc::tmem_ld32(tDV + lane_base + cc * 32, r);
-        tc::tmem_wait_ld();
-        if (c < P.nk) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            red_add_v4(dv + cc * 32 + 4 * i, __uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                       __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
-        }
-      }
-    }
-  } else if (warp >= 8) {
-    // ---- dQ warpgroup: drains dQ (lane = query row) into fp32 atomics while the softmax
-    // warpgroup already works on the next tile; then the dK epilogue
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n");
-    const int t = threadIdx.x - 256;
-    const uint32_t lane_base = (uint32_t)((warp - 8) * 32) << 16;
-    for (int it = 0; it < T; ++it) {
-      const int h = h_lo + it / nqt, m0 = m_begin + (it % nqt) * 128;
-      tc::mbar_wait(bar(C_MD), it & 1);
-      tc::fence_after();
-      // dQ tile: 4 chunks of 32 columns, each staged (fp32, 128B-swizzled rows) in one half of
-      // this iteration's dO buffer (dead once dV/dK are done; the producer refills it only after
-      // the drain) and reduced into dq_acc by the TMA unit
-      uint32_t r[2][32];
-      tc::tmem_ld32(tDP + lane_base, r[0]);
-#pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) {
-        tc::tmem_wait_ld();
-        if (cc + 1 < D / 32) {
-          tc::tmem_ld32(tDP + lane_base + (cc + 1) * 32, r[(cc + 1) & 1]);
-        } else {
-          tc::fence_before();
-          tc::mbar_arrive(bar(C_DQF));  // TMEM dP/dQ columns free for dP of the next tile
-        }
-        // staging slots of 16 KB (128 rows x 32 fp32): two for D=128, one for D=64
-        constexpr int NSTG = Lay::TILE / 16384;
-        const uint32_t stg = sdO + (it & 1) * Lay::TILE + (cc % NSTG) * 16384;
-        if (cc >= NSTG) {  // the slot is reused: its previous reduce must have read it
-          if (t == 0) tc::bulk_wait_read<NSTG - 1>();
-          asm volatile("bar.sync 2, 128;\n" ::: "memory");
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t addr = tc::sw128(stg, t, k);
-          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr),
-                       "f"(__uint_as_float(r[cc & 1][4 * k]) * a.scale),
-                       "f"(__uint_as_float(r[cc & 1][4 * k + 1]) * a.scale),
-                       "f"(__uint_as_float(r[cc & 1][4 * k + 2]) * a.scale),
-                       "f"(__uint_as_float(r[cc & 1][4 * k + 3]) * a.scale));
-        }
-        tc::fence_proxy_async();
-        asm volatile("bar.sync 2, 128;\n" ::: "memory");
-        if (t == 0) {
-          tc::tma_reduce_add_2d(&tmDQ, stg, h * D + cc * 32, P.q_row0 + m0);
-          tc::bulk_commit();
-        }
-      }
-      if (t == 0) tc::bulk_wait_read<0>();
-      asm volatile("bar.sync 2, 128;\n" ::: "memory");
-      tc::mbar_arrive(bar(C_DQS + (it & 1)));
-    }
-    if (T > 0) {  // dK epilogue (lane = key row)
-      tc::mbar_wait(bar(C_FIN), 0);
-      tc::fence_after();
-      const int c = n0 + t;
-      float* dk = a.dk_acc + (int64_t)(P.k_row0 + c) * a.dkv_row_stride + kvh * D;
-#pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t r[32];
-        tc::tmem_ld32(tDK + lane_base + cc * 32, r);
-        tc::tmem_wait_ld();
-        if (c < P.nk) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            red_add_v4(dk + cc * 32 + 4 * i, __uint_as_float(r[4 * i]) * a.scale,
-                       __uint_as_float(r[4 * i + 1]) * a.scale, __uint_as_float(r[4 * i + 2]) * a.scale,
-                       __uint_as_float(r[4 * i + 3]) * a.scale);
-        }
-      }
-    }
-  }
-  tc::fence_before();
-  __syncthreads();
-  if (warp == 2) tc::tmem_dealloc<512>(tmem);
-}
-
-template <int D>
-void launch_bwd_tc_d(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
-  ProblemSet ps = in;
-  ps.tile_prefix[0] = 0;
-  for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nk + 127) / 128;
-  const int tiles = ps.tile_prefix[ps.n];
-  if (tiles == 0 || a.hm.hq == 0 || a.hm.hkv == 0) return;
-  CUtensorMap tq, tk, tv, tdo, tdq;
-  const uint64_t qw = (uint64_t)a.q_row_stride, kw = (uint64_t)a.kv_row_stride, ow = (uint64_t)a.o_row_stride;
-  const uint64_t qrows = max(1, max_rows(ps, true)), krows = max(1, max_rows(ps, false));
-  if (!make_tma_2d(&tq, a.q, qw, qrows, qw, 128) || !make_tma_2d(&tk, a.k, kw, krows, kw, 128) ||
-      !make_tma_2d(&tv, a.v, kw, krows, kw, 128) || !make_tma_2d(&tdo, a.dout, ow, qrows, ow, 128) ||
-      !make_tma_2d_f32(&tdq, a.dq_acc, (uint64_t)a.hm.hq * a.d, qrows, (uint64_t)a.dq_row_stride, 128))
-    launch_error("attn_bwd_tc", "TMA descriptor encode failed (q/k/v/dout/dq base, strides or extents)");
-  ensure_smem_for(attn_bwd_tc_kernel<D>, BwdLayout<D>::SMEM);
-  attn_bwd_tc_kernel<D><<<dim3(tiles, a.hm.hkv), 384, BwdLayout<D>::SMEM, s>>>(tq, tk, tv, tdo, tdq, a, ps);
-  note_launch();
-}
-
-}  // namespace
-
-bool tc_bwd_supported(const BwdArgs& a) {
-  auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
-  return (a.d == 64 || a.d == 128) && al(a.q) && al(a.k) && al(a.v) && al(a.dout) &&
-         (a.q_row_stride * 2) % 16 == 0 && (a.kv_row_stride * 2) % 16 == 0 &&
-         (a.o_row_stride * 2) % 16 == 0 && a.o_row_stride == a.q_row_stride &&
-         (a.dq_row_stride * 4) % 16 == 0 && al(a.dq_acc) && a.dkv_row_stride % 4 == 0;
-}
-void launch_attn_bwd_tc(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
-  if (a.d == 64)
-    launch_bwd_tc_d<64>(a, ps, s);
-  else
-    launch_bwd_tc_d<128>(a, ps, s);
-}
 
 }  // namespace spattn

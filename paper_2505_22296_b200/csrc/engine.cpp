@@ -248,8 +248,6 @@ void launch_attn_fwd_mma(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s)
 void launch_attn_bwd_mma(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
 bool tc_fwd_supported(const FwdArgs& a);
 void launch_attn_fwd_tc(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s);
-bool tc_bwd_supported(const BwdArgs& a);
-void launch_attn_bwd_tc(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
 void launch_add_tasks_f32(const CopyTaskSet& ts, cudaStream_t s);
 
 bool tc_fwd_pp_supported(const FwdArgs& a);
@@ -287,8 +285,6 @@ void launch_attn_bwd(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
   const bool tc = seqpar::kernel_family() != seqpar::KernelFamily::mma;
   if (bwd_uses_q64(a))
     launch_attn_bwd_tc_q64(a, ps, s);
-  else if (tc && tc_bwd_supported(a))
-    launch_attn_bwd_tc(a, ps, s);
   else if (!tc)
     launch_attn_bwd_mma(a, ps, s);  // selected explicitly (A/B anchor), never a fallback
   else
