@@ -1094,6 +1094,17 @@ void ring_forward(RankCtx& ctx, const CommGroup& grp, const std::vector<std::vec
   cudaEventDestroy(ev_comm);
 }
 
+// Backward ring (attention.cpp:290-339): the block of owner (me - step) visits this rank at
+// step `step` carrying the dk|dv its earlier holders accumulated; this rank adds its
+// contribution and passes it on, and after G hops every block is home. The payload travels
+// SPLIT so that only the short dk|dv chain stays between the steps' kernels:
+//   * k|v (bf16) of step s+1 is exchanged on the comm stream WHILE step s computes (k|v do not
+//     change on the way, so the hop can go early; the home-coming k|v hop is skipped);
+//   * step s's kernel accumulates its contribution into a zeroed local buffer; the incoming
+//     dk|dv partial sum (received on the comm stream meanwhile) is added once the kernel is
+//     done, and the sum is sent on to the next rank while step s+1 computes.
+// The exposed per-step cost is the fp32 add over the rank's dk|dv (an HBM pass) instead of the
+// whole k|v|dk|dv hop.
 void ring_backward(RankCtx& ctx, const CommGroup& grp, const std::vector<std::vector<PosRun>>& runs,
                    const Local& L, int d, bool causal, int64_t bs, int64_t lrows,
                    const Documents* docs, const void* out, const float* lse, const void* dout,
@@ -1101,12 +1112,12 @@ void ring_backward(RankCtx& ctx, const CommGroup& grp, const std::vector<std::ve
   const int G = grp.size(), me = grp.index_of(ctx.rank);
   const int64_t kv_elems = L.rows * L.kv_stride;
   const size_t kvb = static_cast<size_t>(kv_elems * 2), gb = static_cast<size_t>(kv_elems * 4);
-  const size_t total = 2 * kvb + 2 * gb;
-  cudaStream_t s = ctx.stream;
-  DevBuf buf[2] = {DevBuf(total, s), DevBuf(total, s)};
-  SP_CUDA(cudaMemcpyAsync(buf[0].p, L.k, kvb, cudaMemcpyDeviceToDevice, s));
-  SP_CUDA(cudaMemcpyAsync(static_cast<char*>(buf[0].p) + kvb, L.v, kvb, cudaMemcpyDeviceToDevice, s));
-  SP_CUDA(cudaMemsetAsync(static_cast<char*>(buf[0].p) + 2 * kvb, 0, 2 * gb, s));
+  cudaStream_t s = ctx.stream, cs = ctx.comm_stream;
+  DevBuf kvbuf[2] = {DevBuf(2 * kvb, s), DevBuf(G > 1 ? 2 * kvb : 0, s)};
+  DevBuf gacc[2] = {DevBuf(2 * gb, s), DevBuf(G > 1 ? 2 * gb : 0, s)};  // contribution + incoming sum
+  DevBuf grecv(G > 1 ? 2 * gb : 0, s);                                  // partial sum from prev
+  SP_CUDA(cudaMemcpyAsync(kvbuf[0].p, L.k, kvb, cudaMemcpyDeviceToDevice, s));
+  SP_CUDA(cudaMemcpyAsync(static_cast<char*>(kvbuf[0].p) + kvb, L.v, kvb, cudaMemcpyDeviceToDevice, s));
   DevBuf delta(static_cast<size_t>(L.rows * L.hm.hq * 4), s);
   spattn::BwdArgs a{};
   a.q = L.q;
@@ -1128,48 +1139,87 @@ void ring_backward(RankCtx& ctx, const CommGroup& grp, const std::vector<std::ve
     spattn::launch_attn_bwd_pre(a, static_cast<int>(L.rows), s);
     check_launch();
   }
+  // events: ev_kv[b] = k|v of buffer b landed; ev_free[b] = step using kv/gacc buffer b done;
+  // ev_add = this step's sum ready to send; ev_g = the next partial sum landed in grecv
+  cudaEvent_t ev_kv[2], ev_free[2], ev_add, ev_g;
+  for (int i = 0; i < 2; ++i) {
+    SP_CUDA(cudaEventCreateWithFlags(&ev_kv[i], cudaEventDisableTiming));
+    SP_CUDA(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming));
+  }
+  SP_CUDA(cudaEventCreateWithFlags(&ev_add, cudaEventDisableTiming));
+  SP_CUDA(cudaEventCreateWithFlags(&ev_g, cudaEventDisableTiming));
+  const int next = (me + 1) % G, prev = (me - 1 + G) % G;
+  // one neighbour exchange on the comm stream: `send` to next, `recv` from prev
+  auto hop = [&](void* send, void* recv, size_t bytes) {
+    ctx.count(Primitive::p2p, static_cast<int64_t>(bytes));
+    if (ctx.transport->peer_access()) {
+      auto ptrs = ctx.transport->exchange_ptrs(grp, ctx.rank, send, cs);
+      SP_CUDA(cudaMemcpyAsync(recv, ptrs[static_cast<size_t>(prev)], bytes, cudaMemcpyDeviceToDevice, cs));
+      ctx.transport->release(grp, ctx.rank, cs);
+    } else {
+      ctx.transport->send_recv(grp, ctx.rank, {{next, send, bytes}}, {{prev, recv, bytes}}, cs);
+    }
+  };
+  SP_CUDA(cudaEventRecord(ev_free[1], s));  // buffer 1 has no earlier reader
   int64_t pairs_total = 0;
   for (int step = 0; step < G; ++step) {
-    DevBuf& cur = buf[step & 1];
-    DevBuf& nxt = buf[(step + 1) & 1];
+    const int b = step & 1;
+    char* kv = static_cast<char*>(kvbuf[b].p);
+    float* acc = gacc[b].as<float>();
+    if (step + 1 < G) {  // k|v of step + 1 travel while this step computes
+      SP_CUDA(cudaEventRecord(ev_kv[b], s));  // kvbuf[b] complete (copied / received)
+      SP_CUDA(cudaStreamWaitEvent(cs, ev_kv[b], 0));
+      SP_CUDA(cudaStreamWaitEvent(cs, ev_free[b ^ 1], 0));  // step - 1 finished reading kvbuf[b^1]
+      hop(kv, kvbuf[b ^ 1].p, 2 * kvb);
+      SP_CUDA(cudaEventRecord(ev_kv[b ^ 1], cs));
+    }
     const int owner = (me - step + G) % G;
     int64_t pairs = 0;
     auto probs = make_problems(runs[static_cast<size_t>(me)], runs[static_cast<size_t>(owner)],
                                causal, bs, lrows, lrows, docs, &pairs);
     pairs_total += pairs;
-    char* base = static_cast<char*>(cur.p);
-    a.k = base;
-    a.v = base + kvb;
-    a.dk_acc = reinterpret_cast<float*>(base + 2 * kvb);
-    a.dv_acc = reinterpret_cast<float*>(base + 2 * kvb + gb);
+    a.k = kv;
+    a.v = kv + kvb;
+    a.dk_acc = acc;
+    a.dv_acc = acc + kv_elems;
+    SP_CUDA(cudaMemsetAsync(acc, 0, 2 * gb, s));
     if (L.hm.hq > 0 && !probs.empty()) attention_backward(s, a, probs);
     if (G > 1) {
-      ctx.count(Primitive::p2p, static_cast<int64_t>(total));
-      const int next = (me + 1) % G, prev = (me - 1 + G) % G;
-      if (ctx.transport->peer_access()) {
-        auto ptrs = ctx.transport->exchange_ptrs(grp, ctx.rank, cur.p, s);
-        SP_CUDA(cudaMemcpyAsync(nxt.p, ptrs[static_cast<size_t>(prev)], total,
-                                cudaMemcpyDeviceToDevice, s));
-        ctx.transport->release(grp, ctx.rank, s);
-      } else {
-        ctx.transport->send_recv(grp, ctx.rank, {{next, cur.p, total}}, {{prev, nxt.p, total}}, s);
+      if (step > 0) {  // + the partial sum of this block's earlier holders
+        SP_CUDA(cudaStreamWaitEvent(s, ev_g, 0));
+        spattn::launch_f32_add(acc, grecv.as<float>(), 2 * kv_elems, s);
+        check_launch();
       }
+      SP_CUDA(cudaEventRecord(ev_add, s));
+      SP_CUDA(cudaStreamWaitEvent(cs, ev_add, 0));  // the sum is final and grecv is read
+      hop(acc, grecv.p, 2 * gb);
+      SP_CUDA(cudaEventRecord(ev_g, cs));
+      SP_CUDA(cudaEventRecord(ev_free[b], s));
+      if (step + 1 < G) SP_CUDA(cudaStreamWaitEvent(s, ev_kv[b ^ 1], 0));  // next step's k|v
     }
   }
   ctx.add_flops(10 * d * pairs_total * L.hm.hq);
-  // after G shifts the block is home carrying every rank's dk/dv (attention.cpp:323-324)
-  const char* home = static_cast<const char*>(buf[G & 1].p);
-  if (G == 1) home = static_cast<const char*>(buf[0].p);
-  const float* hdk = reinterpret_cast<const float*>(home + 2 * kvb);
-  const float* hdv = reinterpret_cast<const float*>(home + 2 * kvb + gb);
+  // the last hop brought this rank's own block home: its dk|dv summed over every rank
+  // (attention.cpp:323-324)
+  const float* home = G > 1 ? grecv.as<float>() : gacc[0].as<float>();
+  if (G > 1) SP_CUDA(cudaStreamWaitEvent(s, ev_g, 0));
   if (dk_f32) {
-    SP_CUDA(cudaMemcpyAsync(dk_f32, hdk, gb, cudaMemcpyDeviceToDevice, s));
-    SP_CUDA(cudaMemcpyAsync(dv_f32, hdv, gb, cudaMemcpyDeviceToDevice, s));
+    SP_CUDA(cudaMemcpyAsync(dk_f32, home, gb, cudaMemcpyDeviceToDevice, s));
+    SP_CUDA(cudaMemcpyAsync(dv_f32, home + kv_elems, gb, cudaMemcpyDeviceToDevice, s));
   } else {
-    spattn::launch_f32_to_bf16(dk_bf16, hdk, 1.f, kv_elems, s);
-    spattn::launch_f32_to_bf16(dv_bf16, hdv, 1.f, kv_elems, s);
+    spattn::launch_f32_to_bf16(dk_bf16, home, 1.f, kv_elems, s);
+    spattn::launch_f32_to_bf16(dv_bf16, home + kv_elems, 1.f, kv_elems, s);
     check_launch();
   }
+  // the comm stream's last work (the home hop) is joined above; release the events
+  SP_CUDA(cudaEventRecord(ev_g, cs));
+  SP_CUDA(cudaStreamWaitEvent(s, ev_g, 0));
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(ev_kv[i]);
+    cudaEventDestroy(ev_free[i]);
+  }
+  cudaEventDestroy(ev_add);
+  cudaEventDestroy(ev_g);
 }
 
 void validate(RankCtx& ctx, const AttentionConfig& cfg, const ShardLayout& layout,

@@ -49,7 +49,8 @@ __host__ __device__ inline void limb_sub(uint64_t* x, int limb, uint64_t chunk) 
 // |v| = m * 2^(e - 1074) with m < 2^53 an integer: two 64-bit chunks at limb offset e / 64
 __host__ __device__ inline void exact_add(uint64_t* x, double v) {
   if (v == 0.0) return;
-  const uint64_t bits = *reinterpret_cast<const uint64_t*>(&v);
+  uint64_t bits;
+  memcpy(&bits, &v, sizeof(bits));
   const int bexp = static_cast<int>((bits >> 52) & 0x7ff);
   uint64_t m = bits & ((1ull << 52) - 1);
   int e;  // bit offset of m's LSB in units of 2^-1074

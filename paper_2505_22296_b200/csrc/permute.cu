@@ -287,6 +287,26 @@ void launch_f32_to_bf16_2d(void* dst, int64_t dst_stride, const float* src, int6
   note_launch();
 }
 
+__global__ void __launch_bounds__(256) f32_add_v4_kernel(float4* dst, const float4* src, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = dst[i];
+    const float4 b = src[i];
+    a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+    dst[i] = a;
+  }
+}
+
+void launch_f32_add(float* dst, const float* src, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  if (n % 4 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) {
+    f32_add_v4_kernel<<<grid_for(n / 4, 512), 256, 0, s>>>(reinterpret_cast<float4*>(dst),
+                                                           reinterpret_cast<const float4*>(src), n / 4);
+    note_launch();
+  } else {
+    launch_f32_add_2d(dst, n, src, n, 1, n, s);
+  }
+}
+
 void launch_f32_add_2d(float* dst, int64_t dst_stride, const float* src, int64_t src_stride,
                        int64_t rows, int64_t cols, cudaStream_t s) {
   if (rows * cols == 0) return;

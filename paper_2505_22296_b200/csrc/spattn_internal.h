@@ -147,5 +147,7 @@ void launch_f32_to_bf16_2d(void* dst, int64_t dst_stride, const float* src, int6
                            int64_t rows, int64_t cols, float scale, cudaStream_t s);
 void launch_f32_add_2d(float* dst, int64_t dst_stride, const float* src, int64_t src_stride,
                        int64_t rows, int64_t cols, cudaStream_t s);
+// dst[i] += src[i] over n contiguous fp32 (16-byte vectors when aligned)
+void launch_f32_add(float* dst, const float* src, int64_t n, cudaStream_t s);
 
 }  // namespace spattn

@@ -213,7 +213,9 @@ def test_native_bytes_closed_form(P):
     assert got == (sp - 1) * per_peer
     got_r = P.measure_engine_bytes("ring", L, H, Hkv, d, sp)
     Xkv = X * Hkv * d
-    assert got_r == (sp - 1) * 2 * Xkv * 2 + sp * (2 * Xkv * 2 + 2 * Xkv * 4)
+    # fwd: sp-1 k|v hops; bwd: sp-1 k|v hops (the home-coming k|v hop is skipped) and sp dk|dv
+    # (fp32) hops, the last one bringing each rank's block home
+    assert got_r == (sp - 1) * 2 * Xkv * 2 + (sp - 1) * 2 * Xkv * 2 + sp * 2 * Xkv * 4
 
 
 @pytest.mark.parametrize("L,H,Hkv,d,groups", [(256, 8, 4, 128, 0), (256, 8, 4, 64, 2),
