@@ -6,7 +6,9 @@
 //   * the LSE merge (merge_piece, attention.cpp:117-149);
 //   * fp32 <-> bf16 conversions for gradient accumulators.
 // All copies are byte-exact (dtype-agnostic, 16-byte vectorised when alignment allows).
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -31,45 +33,49 @@ struct Vec<2> { using T = uint16_t; };
 template <>
 struct Vec<1> { using T = uint8_t; };
 
-// One warp per (task, row); lanes stride 16-byte (or narrower) vectors across the row.
+// One warp per chunk of up to `rpc` consecutive rows of one task (chunk_prefix counts chunks per
+// task). The chunk's rows x (cols + zero_cols) vectors are flattened and each lane keeps four
+// independent 16-byte (or narrower) loads in flight before their stores, whatever the row
+// length: the all-to-all packs move rows of a few hundred bytes to a few KB, where one row per
+// warp leaves the memory system starved.
 template <int VW>
-__global__ void __launch_bounds__(256) copy_rows_kernel(CopyLaunch L, int elem_bytes) {
+__global__ void __launch_bounds__(256) copy_rows_kernel(CopyLaunch L, int elem_bytes, int rpc) {
   using V = typename Vec<VW>::T;
-  const int64_t total = L.row_prefix[L.ts.n];
+  const int64_t total = L.row_prefix[L.ts.n];  // chunks
   const int lane = threadIdx.x % 32;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; w < total; w += warps) {
-    int ti = 0;
-    while (ti + 1 < L.ts.n && L.row_prefix[ti + 1] <= w) ++ti;
-    const CopyTask& T = L.ts.t[ti];
-    const int64_t r = w - L.row_prefix[ti];
+    int lo = 0, hi = L.ts.n - 1;  // the task of chunk w
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (L.row_prefix[mid + 1] > w) hi = mid; else lo = mid + 1;
+    }
+    const CopyTask& T = L.ts.t[lo];
+    const int64_t r0 = (w - L.row_prefix[lo]) * rpc;
+    const int64_t nr = min((int64_t)rpc, T.rows - r0);
+    const int64_t nv = T.cols * elem_bytes / VW, nz = T.zero_cols * elem_bytes / VW, rv = nv + nz;
     const uint8_t* src = reinterpret_cast<const uint8_t*>(T.src) +
-                         ((T.src_row0 + r) * T.src_row_stride + T.src_col0) * elem_bytes;
-    uint8_t* dst = reinterpret_cast<uint8_t*>(T.dst) +
-                   ((T.dst_row0 + r) * T.dst_row_stride + T.dst_col0) * elem_bytes;
-    const int64_t nv = T.cols * elem_bytes / VW;
-    const V* s = reinterpret_cast<const V*>(src);
-    V* d = reinterpret_cast<V*>(dst);
-    // loads batched ahead of their stores (src and dst may alias as far as the compiler knows,
-    // so a plain loop keeps one load in flight per lane)
-    int64_t i = lane;
-    for (; i + 96 < nv; i += 128) {
-      const V a = s[i], b = s[i + 32], c = s[i + 64], e = s[i + 96];
-      d[i] = a;
-      d[i + 32] = b;
-      d[i + 64] = c;
-      d[i + 96] = e;
-    }
-    for (; i + 32 < nv; i += 64) {
-      const V a = s[i], b = s[i + 32];
-      d[i] = a;
-      d[i + 32] = b;
-    }
-    for (; i < nv; i += 32) d[i] = s[i];
-    const int64_t nz = T.zero_cols * elem_bytes / VW;
+                         ((T.src_row0 + r0) * T.src_row_stride + T.src_col0) * elem_bytes;
+    uint8_t* dst = reinterpret_cast<uint8_t*>(T.dst) + ((T.dst_row0 + r0) * T.dst_row_stride + T.dst_col0) * elem_bytes;
+    const int64_t ss = T.src_row_stride * elem_bytes, ds = T.dst_row_stride * elem_bytes;
+    const int64_t n = nr * rv;
     V z;
     memset(&z, 0, sizeof(V));
-    for (int64_t i = lane; i < nz; i += 32) d[nv + i] = z;
+    for (int64_t i = lane; i < n; i += 128) {
+      V x[4];
+      int64_t off[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t e = i + 32 * k;
+        const int r = (int)e / (int)rv;  // chunk extents fit 32 bits
+        const int64_t c = e - (int64_t)r * rv;
+        off[k] = e < n ? r * ds + c * VW : -1;
+        x[k] = (e < n && c < nv) ? *reinterpret_cast<const V*>(src + r * ss + c * VW) : z;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (off[k] >= 0) *reinterpret_cast<V*>(dst + off[k]) = x[k];
+    }
   }
 }
 
@@ -203,10 +209,17 @@ void launch_copy_tasks(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s) {
   CopyLaunch L;
   L.ts = ts;
   L.row_prefix[0] = 0;
-  int64_t align = 16;
+  int64_t align = 16, bytes = 0, rows = 0;
+  for (int i = 0; i < ts.n; ++i) {
+    bytes += ts.t[i].rows * (ts.t[i].cols + ts.t[i].zero_cols) * elem_bytes;
+    rows += ts.t[i].rows;
+  }
+  // rows per warp chunk: about 4 KB per chunk
+  static const int chunk_bytes = getenv("SPATTN_COPY_CHUNK") ? atoi(getenv("SPATTN_COPY_CHUNK")) : 4096;
+  const int rpc = (int)std::max<int64_t>(1, chunk_bytes / std::max<int64_t>(1, rows ? bytes / rows : 1));
   for (int i = 0; i < ts.n; ++i) {
     const CopyTask& t = ts.t[i];
-    L.row_prefix[i + 1] = L.row_prefix[i] + t.rows;
+    L.row_prefix[i + 1] = L.row_prefix[i] + (t.rows + rpc - 1) / rpc;
     for (int64_t v : {(int64_t)reinterpret_cast<uintptr_t>(t.src), (int64_t)reinterpret_cast<uintptr_t>(t.dst),
                       t.src_row_stride * elem_bytes, t.dst_row_stride * elem_bytes,
                       (t.src_row0 * t.src_row_stride + t.src_col0) * elem_bytes,
@@ -218,17 +231,13 @@ void launch_copy_tasks(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s) {
   if (total == 0) return;
   const int grid = grid_for(total, 8);
   switch (align) {
-    case 16: copy_rows_kernel<16><<<grid, 256, 0, s>>>(L, elem_bytes);
-  note_launch(); break;
-    case 8: copy_rows_kernel<8><<<grid, 256, 0, s>>>(L, elem_bytes);
-  note_launch(); break;
-    case 4: copy_rows_kernel<4><<<grid, 256, 0, s>>>(L, elem_bytes);
-  note_launch(); break;
-    case 2: copy_rows_kernel<2><<<grid, 256, 0, s>>>(L, elem_bytes);
-  note_launch(); break;
-    default: copy_rows_kernel<1><<<grid, 256, 0, s>>>(L, elem_bytes);
-  note_launch(); break;
+    case 16: copy_rows_kernel<16><<<grid, 256, 0, s>>>(L, elem_bytes, rpc); break;
+    case 8: copy_rows_kernel<8><<<grid, 256, 0, s>>>(L, elem_bytes, rpc); break;
+    case 4: copy_rows_kernel<4><<<grid, 256, 0, s>>>(L, elem_bytes, rpc); break;
+    case 2: copy_rows_kernel<2><<<grid, 256, 0, s>>>(L, elem_bytes, rpc); break;
+    default: copy_rows_kernel<1><<<grid, 256, 0, s>>>(L, elem_bytes, rpc); break;
   }
+  note_launch();
 }
 
 void launch_add_tasks_f32(const CopyTaskSet& ts, cudaStream_t s) {
