@@ -137,6 +137,10 @@ void ring_shift(RankCtx& ctx, const CommGroup& group, const void* payload, int64
 // Event timing of the attention kernels (bench.py): ms[0]/n[0] forward, ms[1]/n[1] backward.
 void profile_enable(bool on);
 void profile_read(double* ms, int64_t* n);
+// Ring-step stream timeline (spattn_debug_timeline): kind 0 fwd kernel, 1 bwd kernel, 2 k|v hop,
+// 3 dk|dv add, 4 dk|dv hop; times in ms relative to the enable call.
+void timeline_enable(bool on);
+int64_t timeline_read(double* start_ms, double* end_ms, int* kind, int* rank, int max);
 
 // Host planners behind the engines (exported for multi-process tests of the N>1 logic):
 // per-member query/kv head windows of the head<->sequence moves, and the problem list

@@ -166,6 +166,12 @@ int spattn_debug_bwd_trace(void* device_buffer);
 int spattn_debug_fwd_cta_trace(void* device_buffer);
 int spattn_profile_enable(int on);
 int spattn_profile_read(double ms[2], int64_t n[2]);
+/* Profiling: stream timeline of the ring engines. While on, every ring step records CUDA events
+ * around its attention kernel (kind 0 forward, 1 backward), its k|v hop (2), the dk|dv partial-sum
+ * add (3) and the dk|dv hop (4), tagged with the rank. Read returns up to `max` records as start /
+ * end ms relative to the enable call, plus kind and rank; *n = records available. */
+int spattn_debug_timeline(int on);
+int spattn_debug_timeline_read(double* start_ms, double* end_ms, int* kind, int* rank, int max, int64_t* n);
 
 /* Descriptor self-test of the tcgen05 path: d1 = a . b^T, d2 = a . b_mn (smem operands) and
  * d3 = a . b_mn with a read from TMEM, for 128x128 bf16 row-major tiles through TMA +

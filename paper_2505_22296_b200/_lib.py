@@ -28,7 +28,7 @@ EXPORTS = [
     "spattn_saved_free", "spattn_fabric_fwd", "spattn_fabric_bwd", "spattn_fabric_all_to_all",
     "spattn_block_fwd", "spattn_block_finalize", "spattn_lse_merge", "spattn_block_bwd",
     "spattn_shard_rows", "spattn_gather_rows", "spattn_launch_count", "spattn_profile_enable",
-    "spattn_profile_read", "spattn_selftest_umma", "spattn_plan_heads", "spattn_plan_problems",
+    "spattn_profile_read", "spattn_debug_timeline", "spattn_debug_timeline_read", "spattn_selftest_umma", "spattn_plan_heads", "spattn_plan_problems",
     "spattn_debug_bwd_trace", "spattn_debug_fwd_cta_trace", "spattn_debug_transport_selftest", "spattn_fwd_rope", "spattn_fabric_fwd_rope", "spattn_rope_apply",
     "spattn_step_host", "spattn_pick_step_groups", "spattn_pad_batch",
     "spattn_split_position_map", "spattn_documents_from_segments", "spattn_replicate_packing_mask", "spattn_broadcast_bytes",
@@ -165,6 +165,9 @@ def lib() -> ctypes.CDLL:
                                  _i64p],
         "spattn_selftest_umma": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
         "spattn_profile_read": [ctypes.POINTER(ctypes.c_double), _i64p],
+        "spattn_debug_timeline": [_i32],
+        "spattn_debug_timeline_read": [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), _i32, _i64p],
         "spattn_shard_rows": [_vp, layp, _i32, _i64, _i64, _vp, _vp],
         "spattn_gather_rows": [_vp, layp, _i32, _i64, _i64, _vp, _vp],
     }

@@ -326,6 +326,12 @@ int spattn_profile_enable(int on) {
 int spattn_profile_read(double ms[2], int64_t n[2]) {
   return guard([&] { seqpar::profile_read(ms, n); });
 }
+int spattn_debug_timeline(int on) {
+  return guard([&] { seqpar::timeline_enable(on != 0); });
+}
+int spattn_debug_timeline_read(double* start_ms, double* end_ms, int* kind, int* rank, int max, int64_t* n) {
+  return guard([&] { *n = seqpar::timeline_read(start_ms, end_ms, kind, rank, max); });
+}
 
 namespace {
 std::unique_ptr<seqpar::Rope> rope_of(const int64_t* position_ids, int64_t n, double base) {

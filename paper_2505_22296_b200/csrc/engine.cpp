@@ -325,6 +325,37 @@ struct ProfScope {
   }
 };
 
+// Ring-step stream timeline (spattn_debug_timeline): CUDA events around the steps' kernels,
+// hops and adds on the stream each runs on.
+struct Timeline {
+  std::mutex mu;
+  bool on = false;
+  cudaEvent_t origin = nullptr;
+  struct Rec {
+    int kind, rank;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+} g_tl;
+
+struct TlScope {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  int kind, rank;
+  TlScope(cudaStream_t st, int k, int r) : s(st), kind(k), rank(r) {
+    if (!g_tl.on) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  ~TlScope() {
+    if (!a) return;
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(g_tl.mu);
+    g_tl.recs.push_back({kind, rank, a, b});
+  }
+};
+
 void require_dim(int d) {
   if (d != 64 && d != 128) throw ConfigError("attention kernels support head_dim 64 or 128, got " + std::to_string(d));
 }
@@ -861,6 +892,32 @@ void profile_enable(bool on) {
   g_prof.on = on;
 }
 
+void timeline_enable(bool on) {
+  std::lock_guard<std::mutex> lk(g_tl.mu);
+  if (on) {
+    for (auto& r : g_tl.recs) cudaEventDestroy(r.a), cudaEventDestroy(r.b);
+    g_tl.recs.clear();
+    if (!g_tl.origin) SP_CUDA(cudaEventCreate(&g_tl.origin));
+    SP_CUDA(cudaDeviceSynchronize());
+    SP_CUDA(cudaEventRecord(g_tl.origin, nullptr));
+  }
+  g_tl.on = on;
+}
+
+int64_t timeline_read(double* start_ms, double* end_ms, int* kind, int* rank, int max) {
+  std::lock_guard<std::mutex> lk(g_tl.mu);
+  SP_CUDA(cudaDeviceSynchronize());
+  const int64_t n = static_cast<int64_t>(g_tl.recs.size());
+  for (int64_t i = 0; i < n && i < max; ++i) {
+    const auto& r = g_tl.recs[static_cast<size_t>(i)];
+    float a = 0, b = 0;
+    SP_CUDA(cudaEventElapsedTime(&a, g_tl.origin, r.a));
+    SP_CUDA(cudaEventElapsedTime(&b, g_tl.origin, r.b));
+    start_ms[i] = a, end_ms[i] = b, kind[i] = r.kind, rank[i] = r.rank;
+  }
+  return n;
+}
+
 void profile_read(double* ms, int64_t* n) {
   std::lock_guard<std::mutex> lk(g_prof.mu);
   ms[0] = ms[1] = 0;
@@ -1066,6 +1123,7 @@ void ring_forward(RankCtx& ctx, const CommGroup& grp, const std::vector<std::vec
       SP_CUDA(cudaStreamWaitEvent(cs, ev_main, 0));
       ctx.count(Primitive::p2p, static_cast<int64_t>(2 * kvb));
       const int next = (me + 1) % G, prev = (me - 1 + G) % G;
+      TlScope tl(cs, 2, ctx.rank);
       if (ctx.transport->peer_access()) {
         auto ptrs = ctx.transport->exchange_ptrs(grp, ctx.rank, cur.p, cs);
         SP_CUDA(cudaMemcpyAsync(nxt.p, ptrs[static_cast<size_t>(prev)], 2 * kvb,
@@ -1083,7 +1141,10 @@ void ring_forward(RankCtx& ctx, const CommGroup& grp, const std::vector<std::vec
     pairs_total += pairs;
     a.k = cur.p;
     a.v = static_cast<char*>(cur.p) + kvb;
-    if (L.hm.hq > 0 && !probs.empty()) attention_forward(s, a, probs, true);
+    if (L.hm.hq > 0 && !probs.empty()) {
+      TlScope tl(s, 0, ctx.rank);
+      attention_forward(s, a, probs, true);
+    }
     if (step + 1 < G) SP_CUDA(cudaStreamWaitEvent(s, ev_comm, 0));
   }
   ctx.add_flops(4 * d * pairs_total * L.hm.hq);
@@ -1170,7 +1231,10 @@ void ring_backward(RankCtx& ctx, const CommGroup& grp, const std::vector<std::ve
       SP_CUDA(cudaEventRecord(ev_kv[b], s));  // kvbuf[b] complete (copied / received)
       SP_CUDA(cudaStreamWaitEvent(cs, ev_kv[b], 0));
       SP_CUDA(cudaStreamWaitEvent(cs, ev_free[b ^ 1], 0));  // step - 1 finished reading kvbuf[b^1]
-      hop(kv, kvbuf[b ^ 1].p, 2 * kvb);
+      {
+        TlScope tl(cs, 2, ctx.rank);
+        hop(kv, kvbuf[b ^ 1].p, 2 * kvb);
+      }
       SP_CUDA(cudaEventRecord(ev_kv[b ^ 1], cs));
     }
     const int owner = (me - step + G) % G;
@@ -1183,16 +1247,23 @@ void ring_backward(RankCtx& ctx, const CommGroup& grp, const std::vector<std::ve
     a.dk_acc = acc;
     a.dv_acc = acc + kv_elems;
     SP_CUDA(cudaMemsetAsync(acc, 0, 2 * gb, s));
-    if (L.hm.hq > 0 && !probs.empty()) attention_backward(s, a, probs);
+    if (L.hm.hq > 0 && !probs.empty()) {
+      TlScope tl(s, 1, ctx.rank);
+      attention_backward(s, a, probs);
+    }
     if (G > 1) {
       if (step > 0) {  // + the partial sum of this block's earlier holders
         SP_CUDA(cudaStreamWaitEvent(s, ev_g, 0));
+        TlScope tl(s, 3, ctx.rank);
         spattn::launch_f32_add(acc, grecv.as<float>(), 2 * kv_elems, s);
         check_launch();
       }
       SP_CUDA(cudaEventRecord(ev_add, s));
       SP_CUDA(cudaStreamWaitEvent(cs, ev_add, 0));  // the sum is final and grecv is read
-      hop(acc, grecv.p, 2 * gb);
+      {
+        TlScope tl(cs, 4, ctx.rank);
+        hop(acc, grecv.p, 2 * gb);
+      }
       SP_CUDA(cudaEventRecord(ev_g, cs));
       SP_CUDA(cudaEventRecord(ev_free[b], s));
       if (step + 1 < G) SP_CUDA(cudaStreamWaitEvent(s, ev_kv[b ^ 1], 0));  // next step's k|v

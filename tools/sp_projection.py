@@ -24,6 +24,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import paper_2505_22296_b200 as P  # noqa: E402
 
 NVLINK = 770e9
+HBM = 6.5e12  # measured copy bandwidth order (MEASURED_PEAKS.json hbm_gbs)
 
 
 def c5_docs(total=262144, lo=1024, hi=65536):
@@ -114,24 +115,38 @@ def main():
         t_comp = t_all * share
         t_comm = nbytes[busiest] / NVLINK
         t_rank = t_comp + t_comm
+        # overlap-aware ring estimate (r2 ring engine): the k|v hops of the next step and the
+        # dk|dv hop of the previous one travel during a step's kernel; exposed are the hops that
+        # outlast a step, the sp-1 dk|dv adds (an HBM pass: 12 bytes per kv element) and the
+        # home-coming dk|dv hop
+        t_ovl = t_rank
+        if engine == "ring" and sp > 1:
+            X = L // sp * Hkv * d
+            t_fwd_step, t_bwd_step = t_comp * 4 / 14 / sp, t_comp * 10 / 14 / sp
+            kv_hop, g_hop = 2 * X * 2 / NVLINK, 2 * X * 4 / NVLINK
+            exposed = (sp - 1) * max(0.0, kv_hop - t_fwd_step)
+            exposed += (sp - 1) * max(0.0, kv_hop + g_hop - t_bwd_step)
+            exposed += (sp - 1) * 3 * 2 * X * 4 / HBM + g_hop
+            t_ovl = t_comp + exposed
         real = 14 * d * H * (L * (L + 1) // 2) if dl is None else sum(14 * d * H * n * (n + 1) // 2 for n in dl)
         rows.append(dict(config=name, engine=engine, sp=sp, L=L, heads=f"{H}/{Hkv}", d=d,
                          docs=len(dl) if dl else 0, t_all_ms=t_all * 1e3,
                          busiest_share=share, t_compute_ms=t_comp * 1e3,
                          bytes_busiest=nbytes[busiest], t_comm_ms=t_comm * 1e3,
                          t_step_ms=t_rank * 1e3, tokens_per_s=L / t_rank,
+                         t_step_overlap_ms=t_ovl * 1e3, tokens_per_s_overlap=L / t_ovl,
                          executed_flops=sum(flops), algorithmic_flops=real,
                          achieved_tflops_1gpu=sum(flops) / t_all / 1e12))
         print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
     print("| config | engine | SP | L | heads q/kv | docs | T_all 1-GPU (ms) | busiest share | "
           "t_compute (ms) | bytes/rank (MB) | t_comm@770GB/s (ms) | projected step (ms) | "
-          "projected tokens/s | 1-GPU TFLOP/s (executed) |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+          "projected tokens/s | overlap-aware step (ms) | 1-GPU TFLOP/s (executed) |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for x in rows:
         print(f"| {x['config']} | {x['engine']} | {x['sp']} | {x['L']} | {x['heads']} | {x['docs']} | "
               f"{x['t_all_ms']:.1f} | {x['busiest_share']:.3f} | {x['t_compute_ms']:.2f} | "
               f"{x['bytes_busiest'] / 1e6:.1f} | {x['t_comm_ms']:.2f} | {x['t_step_ms']:.2f} | "
-              f"{x['tokens_per_s']:.3e} | {x['achieved_tflops_1gpu']:.0f} |")
+              f"{x['tokens_per_s']:.3e} | {x['t_step_overlap_ms']:.2f} | {x['achieved_tflops_1gpu']:.0f} |")
     json.dump(rows, open(os.path.join(ROOT, "profiles", "sp_projection.json"), "w"), indent=1)
 
 
