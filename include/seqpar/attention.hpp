@@ -152,8 +152,9 @@ std::vector<std::array<int, 6>> plan_problems(const std::vector<int64_t>& qpos,
                                               const Documents* docs, int64_t* pairs);
 
 // Which attention kernel family the engines launch.
-// tcgen05_pp: two-tile ping-pong forward; tcgen05_pair: CTA-pair (cta_group::2) forward for d=128
-enum class KernelFamily { tcgen05, mma, tcgen05_pp, tcgen05_pair };
+// tcgen05_pp: two-tile ping-pong forward; tcgen05_pair: CTA-pair (cta_group::2) forward for d=128;
+// tcgen05_q128: backward with 128-query tiles (attn_bwd_q128.cu) for d=128
+enum class KernelFamily { tcgen05, mma, tcgen05_pp, tcgen05_pair, tcgen05_q128 };
 void set_kernel_family(KernelFamily f);
 KernelFamily kernel_family();
 

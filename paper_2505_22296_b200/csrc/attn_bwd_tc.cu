@@ -91,45 +91,34 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 }
 
 // Softmax gradient of one 32-query chunk for one key (thread): P = 2^(s*scale*log2e - lse*log2e)
-// and dS = P (dP - delta), both packed to bf16 pairs (attention.cpp:199-209). Packed fp32x2
-// math; one pair in four takes the FMA-pipe exp2 so MUFU and FMA finish together. MASK (only
-// for tiles crossing the causal diagonal or the row end) zeroes queries outside [ilo, ihi).
-// dS is produced already multiplied by the softmax scale (dl2 holds -delta*scale): the dQ and
+// and dS = P (dP - delta), both packed to bf16 pairs (attention.cpp:199-209). MASK (only for
+// tiles crossing the causal diagonal or the row end) zeroes queries outside [ilo, ihi).
+// dS is produced already multiplied by the softmax scale (dl4 holds -delta*scale): the dQ and
 // dK accumulators then need no rescaling (dS scale = scale * P (dP - delta)).
-template <bool MASK, bool PACKED, bool POLY>
-__device__ __forceinline__ void grad_chunk(const uint32_t (&rs)[32], const uint32_t (&rp)[32], const float2* nl2,
-                                           const float2* dl2, uint64_t sl2x2, uint64_t sc2, int ilo, int ihi,
+// The per-query -lse*log2e / -delta*scale come from shared memory as warp-uniform 16-byte loads
+// (four queries per load): this kernel is bound by shared-memory wavefronts (tensor-core
+// operand reads + these loads + the dS^T and dQ stores), and each load instruction is one
+// wavefront whatever its width.
+template <bool MASK>
+__device__ __forceinline__ void grad_chunk(const uint32_t (&rs)[32], const uint32_t (&rp)[32], const float4* nl4,
+                                           const float4* dl4, float sl2, float sc, int ilo, int ihi,
                                            uint32_t (&wp)[16], uint32_t (&wd)[16]) {
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const float2 nl = nl2[i], dl = dl2[i];
-    float2 pp;
-    if (PACKED) {
-      const float2 x = f2_unpack(f2_fma(f2_pack(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1])), sl2x2,
-                                        f2_pack(nl.x, nl.y)));
-      if (POLY && (i & 3) == 3)
-        pp = poly_exp2x2(x.x, x.y);
-      else
-        pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
-    } else {
-      const float sl2 = f2_unpack(sl2x2).x;
-      pp = make_float2(fast_exp2(fmaf(__uint_as_float(rs[2 * i]), sl2, nl.x)),
-                       fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), sl2, nl.y)));
-    }
-    if (MASK) {
-      pp.x = (2 * i >= ilo && 2 * i < ihi) ? pp.x : 0.f;
-      pp.y = (2 * i + 1 >= ilo && 2 * i + 1 < ihi) ? pp.y : 0.f;
-    }
-    wp[i] = pack_bf16(pp.x, pp.y);
-    if (PACKED) {
-      const float2 dsv = f2_unpack(f2_mul(
-          f2_pack(pp.x, pp.y),
-          f2_fma(f2_pack(__uint_as_float(rp[2 * i]), __uint_as_float(rp[2 * i + 1])), sc2, f2_pack(dl.x, dl.y))));
-      wd[i] = pack_bf16(dsv.x, dsv.y);
-    } else {
-      const float sc = f2_unpack(sc2).x;
-      wd[i] = pack_bf16(pp.x * fmaf(__uint_as_float(rp[2 * i]), sc, dl.x),
-                        pp.y * fmaf(__uint_as_float(rp[2 * i + 1]), sc, dl.y));
+  for (int j = 0; j < 8; ++j) {
+    const float4 nl = nl4[j], dl = dl4[j];
+    const float nv[4] = {nl.x, nl.y, nl.z, nl.w}, dv[4] = {dl.x, dl.y, dl.z, dl.w};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = 2 * j + h;
+      float px = fast_exp2(fmaf(__uint_as_float(rs[2 * i]), sl2, nv[2 * h]));
+      float py = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), sl2, nv[2 * h + 1]));
+      if (MASK) {
+        px = (2 * i >= ilo && 2 * i < ihi) ? px : 0.f;
+        py = (2 * i + 1 >= ilo && 2 * i + 1 < ihi) ? py : 0.f;
+      }
+      wp[i] = pack_bf16(px, py);
+      wd[i] = pack_bf16(px * fmaf(__uint_as_float(rp[2 * i]), sc, dv[2 * h]),
+                        py * fmaf(__uint_as_float(rp[2 * i + 1]), sc, dv[2 * h + 1]));
     }
   }
 }
@@ -356,9 +345,8 @@ __global__ void __launch_bounds__(Roles<D>::NTHREADS, 1)
       // chunk c (32 queries) of S^T / dP^T: the first chunk is loaded up front, the second (4
       // warps) after the first is computed; each chunk's P^T / dS^T go back into its own S^T
       // columns, which its loads have already emptied
-      const float2* lse2 = reinterpret_cast<const float2*>(sL + lb);   // -lse*log2e per query
-      const float2* dl2 = reinterpret_cast<const float2*>(sDl + lb);   // -delta*scale per query
-      const uint64_t sl2x2 = f2_pack(sl2, sl2), sc2 = f2_pack(a.scale, a.scale);
+      const float4* lse4 = reinterpret_cast<const float4*>(sL + lb);   // -lse*log2e per query
+      const float4* dl4 = reinterpret_cast<const float4*>(sDl + lb);   // -delta*scale per query
 #pragma unroll
       for (int cc = cc_lo; cc < cc_hi; ++cc) {
         uint32_t rs[32], rp[32];
@@ -372,8 +360,8 @@ __global__ void __launch_bounds__(Roles<D>::NTHREADS, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) wp[i] = rs[i] ^ rp[i], wd[i] = rs[i + 16] ^ rp[i + 16];
         } else {
-          grad_chunk<true, false, false>(rs, rp, lse2 + cc * 16, dl2 + cc * 16, sl2x2, sc2, ilo - cc * 32,
-                                         ihi - cc * 32, wp, wd);
+          grad_chunk<true>(rs, rp, lse4 + cc * 8, dl4 + cc * 8, sl2, a.scale, ilo - cc * 32, ihi - cc * 32, wp,
+                           wd);
         }
         tc::tmem_st16(tmem + lane_base + 64 * b + cc * 32, wp);       // P^T: A operand of dV
         tc::tmem_st16(tmem + lane_base + 64 * b + cc * 32 + 16, wd);  // dS^T: A operand of dK

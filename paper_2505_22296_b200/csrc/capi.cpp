@@ -277,7 +277,7 @@ int spattn_ctx_reset_stats(spattn_ctx* c) {
 }
 int spattn_set_kernel_family(int family) {
   return guard([&] {
-    if (family < 0 || family > 3) throw seqpar::ConfigError("kernel family must be 0, 1, 2 or 3");
+    if (family < 0 || family > 4) throw seqpar::ConfigError("kernel family must be 0 .. 4");
     seqpar::set_kernel_family(static_cast<seqpar::KernelFamily>(family));
   });
 }

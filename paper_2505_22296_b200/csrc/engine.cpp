@@ -274,6 +274,8 @@ void launch_attn_fwd(const FwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
 }
 bool tc_bwd_q64_supported(const BwdArgs& a);
 void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
+bool tc_bwd_q128_supported(const BwdArgs& a);
+void launch_attn_bwd_q128(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
 
 // The backward launch picks the q64 tcgen05 kernel for these arguments (the only one that can
 // write dK / dV directly as bf16).
@@ -283,7 +285,9 @@ bool bwd_uses_q64(const BwdArgs& a) {
 
 void launch_attn_bwd(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
   const bool tc = seqpar::kernel_family() != seqpar::KernelFamily::mma;
-  if (bwd_uses_q64(a))
+  if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05_q128 && tc_bwd_q128_supported(a))
+    launch_attn_bwd_q128(a, ps, s);
+  else if (bwd_uses_q64(a))
     launch_attn_bwd_tc_q64(a, ps, s);
   else if (!tc)
     launch_attn_bwd_mma(a, ps, s);  // selected explicitly (A/B anchor), never a fallback
