@@ -42,7 +42,10 @@ constexpr bool kPolyExp = Q128_POLY;
 constexpr int NCW = 8;                               // softmax-gradient warps
 constexpr int DRAIN0 = NCW, PRODW = DRAIN0 + 4, TALLOCW = PRODW + 1, MMAW = PRODW + 3;
 constexpr int NTHREADS = (PRODW + 4) * 32;           // 512
-// 512 threads: every warp keeps the launch's 128 registers (no setmaxnreg rebalancing)
+// registers per thread after setmaxnreg (the launch gives 128 to all 512 threads): the drain
+// warps hold a whole 128-column dQ row so they release the TMEM columns in one round trip
+constexpr int REG_C = 144, REG_DQ = 168, REG_CTL = 56;
+static_assert(NCW * REG_C + 4 * REG_DQ + 4 * REG_CTL <= 2048, "register budget");
 constexpr int NQ = 2;                                // Q stages (S(i+1) is issued before dK(i))
 constexpr int TILE = 128 * D * 2;                    // 32 KB: two 16 KB 128B-swizzled column blocks
 constexpr int K_OFF = 0, V_OFF = TILE, Q_OFF = 2 * TILE, DO_OFF = Q_OFF + NQ * TILE;
@@ -146,6 +149,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (warp >= PRODW) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_CTL));
 
   if (warp == PRODW) {
     // ------------------------------------------------------------------ TMA producer
@@ -208,8 +212,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       constexpr uint32_t id_s = tc::idesc_bf16(128, BQ, false, false);  // S^T, dP^T
       constexpr uint32_t id_kv = tc::idesc_bf16(128, D, false, true);   // dV, dK (A in TMEM)
       constexpr uint32_t id_q = tc::idesc_bf16(BQ, D, true, true);      // dQ = dS K
+      // (K-step loops are not unrolled: the issuer runs at 56 registers and one MMA per 64
+      // tensor cycles leaves ample issue time)
       auto kxq = [&](uint32_t d_col, uint32_t a_tile, uint32_t b_tile) {  // 128 x 128 x d, both K-major
-#pragma unroll
+#pragma unroll 1
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t o = (ks >> 2) * 16384 + (ks & 3) * 32;
           tc::mma_ss(tmem + d_col, tc::sdesc(a_tile + o, 16, 1024), tc::sdesc(b_tile + o, 16, 1024), id_s, ks > 0);
@@ -217,7 +223,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       };
       // acc (+)= (P^T or dS^T in TMEM cols [a_col + 64c, +32)) . (dO or Q, MN-major), K = 128 queries
       auto tmem_a = [&](uint32_t d_col, uint32_t a_col, uint32_t b_tile, bool first) {
-#pragma unroll
+#pragma unroll 1
         for (int kk = 0; kk < BQ / 16; ++kk)
           tc::mma_ts(tmem + d_col, tmem + a_col + (kk >> 2) * 64 + (kk & 3) * 8,
                      tc::sdesc(b_tile + kk * 2048, 16384, 1024), id_kv, (!first || kk > 0) ? 1u : 0u);
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::commit(bar(E_QE + s));
         // dQ = dS K (M = 128 queries: the dS^T smem tile read MN-major; B = K MN-major) into the
         // dP^T columns, whose dS^T dK has just read
-#pragma unroll
+#pragma unroll 1
         for (int kk = 0; kk < 8; ++kk)
           tc::mma_ss(tmem + T_DP, tc::sdesc(sdS + kk * 2048, 16384, 1024), tc::sdesc(sK + kk * 2048, 16384, 1024),
                      id_q, kk > 0 ? 1u : 0u);
@@ -275,6 +281,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc::commit(bar(E_FIN));
     }
   } else if (warp < NCW) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_C));
     // ----------------------------------- softmax gradient (lane = key, query half c = w >> 2)
     const int qd = warp & 3, c = warp >> 2;
     const int t = qd * 32 + (threadIdx.x & 31);  // key row in the tile == TMEM lane
@@ -412,6 +419,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else if (warp >= DRAIN0 && warp < DRAIN0 + 4) {
     // ------------------------------ dQ drain (lane = query row of the dQ tile) + dK epilogue
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_DQ));
     const int w = warp - DRAIN0, lane = threadIdx.x % 32;
     const uint32_t lb = (uint32_t)(w * 32) << 16;
     const uint32_t slot0 = sStg + w * 2 * 4096;  // 2 x [32 rows x 32 fp32], 128B-swizzled rows
@@ -421,33 +429,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc::fence_after();
       if (w == 0 && lane == 0) TR(7, it);
       if (w == 0 && lane == 0) TC(14, it);
+      // the whole 128-column row first: dP(i+1) waits for these columns
+      uint32_t r[4][32];
 #pragma unroll
-      for (int pr = 0; pr < 2; ++pr) {  // head-dim columns [64pr, 64pr+64)
-        uint32_t r[2][32];
-        tc::tmem_ld32(tmem + lb + T_DP + 64 * pr, r[0]);
-        tc::tmem_ld32(tmem + lb + T_DP + 64 * pr + 32, r[1]);
-        tc::tmem_wait_ld();
-        if (pr == 1) {
-          tc::fence_before();
-          tc::mbar_arrive(bar(E_DQF));
-          if (w == 0 && lane == 0) TR(8, it);
-          if (w == 0 && lane == 0) TC(15, it);
-        }
+      for (int j = 0; j < 4; ++j) tc::tmem_ld32(tmem + lb + T_DP + 32 * j, r[j]);
+      tc::tmem_wait_ld();
+      tc::fence_before();
+      tc::mbar_arrive(bar(E_DQF));
+      if (w == 0 && lane == 0) TR(8, it);
+      if (w == 0 && lane == 0) TC(15, it);
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const uint32_t slot = slot0 + j * 4096;
-          if (lane == 0) tc::bulk_wait_read<1>();  // the reduce issued two chunks ago has read it
-          __syncwarp();
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t slot = slot0 + (j & 1) * 4096;
+        if (lane == 0) tc::bulk_wait_read<1>();  // the reduce issued two chunks ago has read it
+        __syncwarp();
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(tc::sw128(slot, lane, k)), "r"(r[j][4 * k]),
-                         "r"(r[j][4 * k + 1]), "r"(r[j][4 * k + 2]), "r"(r[j][4 * k + 3]));
-          tc::fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
-            tc::tma_reduce_add_2d(&tmDQ, slot, h * D + 64 * pr + 32 * j, P.q_row0 + m0 + 32 * w);
-            tc::bulk_commit();
-          }
+        for (int k = 0; k < 8; ++k)
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(tc::sw128(slot, lane, k)), "r"(r[j][4 * k]),
+                       "r"(r[j][4 * k + 1]), "r"(r[j][4 * k + 2]), "r"(r[j][4 * k + 3]));
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tc::tma_reduce_add_2d(&tmDQ, slot, h * D + 32 * j, P.q_row0 + m0 + 32 * w);
+          tc::bulk_commit();
         }
       }
     }

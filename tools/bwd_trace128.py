@@ -9,6 +9,8 @@ sys.path.insert(0, ".")
 import paper_2505_22296_b200 as P  # noqa: E402
 from paper_2505_22296_b200 import _lib as C  # noqa: E402
 
+P.set_kernel_family("tcgen05_q128")
+
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 H, Hkv, d = 32, 8, 128
 buf = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")

@@ -2,6 +2,7 @@
 Ulysses SP=8 at c2: L=32768, 4 q heads, 1 kv head), via the library's CUDA-event profiler.
     python tools/shape_bench.py L H Hkv [d] [reps]"""
 import ctypes
+import os
 import sys
 
 import torch
@@ -9,6 +10,8 @@ import torch
 sys.path.insert(0, ".")
 import paper_2505_22296_b200 as P  # noqa: E402
 from paper_2505_22296_b200 import _lib as C  # noqa: E402
+
+P.set_kernel_family(os.environ.get("FAMILY", "tcgen05"))
 
 L, H, Hkv = (int(x) for x in sys.argv[1:4])
 d = int(sys.argv[4]) if len(sys.argv) > 4 else 128
