@@ -182,7 +182,7 @@ def main():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--engine", default=None)
     ap.add_argument("--seq-len", type=int, default=None)
-    ap.add_argument("--family", default="tcgen05", choices=["tcgen05", "mma", "tcgen05_pp", "tcgen05_pair", "tcgen05_q128"])
+    ap.add_argument("--family", default="tcgen05", choices=["tcgen05", "mma", "tcgen05_pp", "tcgen05_pair", "tcgen05_q64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-groups", type=int, default=0,

@@ -153,8 +153,9 @@ std::vector<std::array<int, 6>> plan_problems(const std::vector<int64_t>& qpos,
 
 // Which attention kernel family the engines launch.
 // tcgen05_pp: two-tile ping-pong forward; tcgen05_pair: CTA-pair (cta_group::2) forward for d=128;
-// tcgen05_q128: backward with 128-query tiles (attn_bwd_q128.cu) for d=128
-enum class KernelFamily { tcgen05, mma, tcgen05_pp, tcgen05_pair, tcgen05_q128 };
+// tcgen05_q64: the 64-query-tile backward (attn_bwd_tc.cu) also for d=128, where the default
+// family runs the 128-query-tile backward (attn_bwd_q128.cu)
+enum class KernelFamily { tcgen05, mma, tcgen05_pp, tcgen05_pair, tcgen05_q64 };
 void set_kernel_family(KernelFamily f);
 KernelFamily kernel_family();
 

@@ -151,8 +151,8 @@ int spattn_ctx_flops(spattn_ctx* ctx, int64_t* flops);
 int spattn_ctx_reset_stats(spattn_ctx* ctx);
 /* 0 = tcgen05/TMEM kernels (default where supported), 1 = mma.sync kernels,
  * 2 = tcgen05 with the two-tile ping-pong forward, 3 = tcgen05 with the CTA-pair
- * (cta_group::2, M=256) forward for head_dim 128, 4 = tcgen05 with the 128-query-tile
- * backward for head_dim 128 */
+ * (cta_group::2, M=256) forward for head_dim 128, 4 = tcgen05 with the 64-query-tile
+ * backward for head_dim 128 too (the default runs the 128-query-tile backward there) */
 int spattn_set_kernel_family(int family);
 int spattn_get_kernel_family(void);
 

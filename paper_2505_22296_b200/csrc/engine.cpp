@@ -277,17 +277,17 @@ void launch_attn_bwd_tc_q64(const BwdArgs& a, const ProblemSet& ps, cudaStream_t
 bool tc_bwd_q128_supported(const BwdArgs& a);
 void launch_attn_bwd_q128(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s);
 
-// The backward launch picks the q64 tcgen05 kernel for these arguments (the only one that can
-// write dK / dV directly as bf16).
-bool bwd_uses_q64(const BwdArgs& a) {
+// The backward launch picks a tcgen05 kernel for these arguments (q128 for head_dim 128, q64
+// otherwise or when selected); both can write dK / dV directly as bf16.
+bool bwd_uses_tcgen05(const BwdArgs& a) {
   return seqpar::kernel_family() != seqpar::KernelFamily::mma && tc_bwd_q64_supported(a);
 }
 
 void launch_attn_bwd(const BwdArgs& a, const ProblemSet& ps, cudaStream_t s) {
   const bool tc = seqpar::kernel_family() != seqpar::KernelFamily::mma;
-  if (seqpar::kernel_family() == seqpar::KernelFamily::tcgen05_q128 && tc_bwd_q128_supported(a))
+  if (tc && seqpar::kernel_family() != seqpar::KernelFamily::tcgen05_q64 && tc_bwd_q128_supported(a))
     launch_attn_bwd_q128(a, ps, s);
-  else if (bwd_uses_q64(a))
+  else if (bwd_uses_tcgen05(a))
     launch_attn_bwd_tc_q64(a, ps, s);
   else if (!tc)
     launch_attn_bwd_mma(a, ps, s);  // selected explicitly (A/B anchor), never a fallback
@@ -1040,7 +1040,7 @@ bool direct_dkv_ok(const Local& L, int d, const std::vector<AttnProblem>& probs,
   probe.dout = L.q, probe.dq_acc = reinterpret_cast<float*>(const_cast<void*>(L.q));  // alignment probe only
   probe.q_row_stride = L.q_stride, probe.kv_row_stride = L.kv_stride, probe.o_row_stride = L.q_stride;
   probe.dq_row_stride = L.q_stride, probe.dkv_row_stride = L.kv_stride;
-  return spattn::bwd_uses_q64(probe) && keys_exclusive(probs, L.rows) &&
+  return spattn::bwd_uses_tcgen05(probe) && keys_exclusive(probs, L.rows) &&
          reinterpret_cast<uintptr_t>(dk_bf16) % 16 == 0 && reinterpret_cast<uintptr_t>(dv_bf16) % 16 == 0 &&
          (L.kv_stride * 2) % 16 == 0;
 }
@@ -1073,7 +1073,7 @@ bool plain_backward(RankCtx& ctx, const Local& L, int d, const std::vector<AttnP
   a.d = d;
   a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
   a.hm = L.hm;
-  const bool direct = direct_dkv_ok(L, d, probs, dk_bf16, dv_bf16) && spattn::bwd_uses_q64(a);
+  const bool direct = direct_dkv_ok(L, d, probs, dk_bf16, dv_bf16) && spattn::bwd_uses_tcgen05(a);
   if (direct) {
     a.dk_bf16 = dk_bf16;
     a.dv_bf16 = dv_bf16;

@@ -192,14 +192,14 @@ def document_position_ids(doc_lens: Sequence[int]) -> list[int]:
 
 def set_kernel_family(name: str) -> None:
     """'tcgen05' (default where supported), 'mma', 'tcgen05_pp' (two-tile forward) or
-    'tcgen05_pair' (CTA-pair cta_group::2 forward, d=128), 'tcgen05_q128' (backward with
-    128-query tiles and single-buffered TMEM, d=128)."""
+    'tcgen05_pair' (CTA-pair cta_group::2 forward, d=128), 'tcgen05_q64' (the 64-query-tile
+    backward for d=128 too; the default runs the 128-query-tile backward there)."""
     C.check(C.lib().spattn_set_kernel_family(
-        {"tcgen05": 0, "mma": 1, "tcgen05_pp": 2, "tcgen05_pair": 3, "tcgen05_q128": 4}[name]))
+        {"tcgen05": 0, "mma": 1, "tcgen05_pp": 2, "tcgen05_pair": 3, "tcgen05_q64": 4}[name]))
 
 
 def kernel_family() -> str:
-    return ["tcgen05", "mma", "tcgen05_pp", "tcgen05_pair", "tcgen05_q128"][C.lib().spattn_get_kernel_family()]
+    return ["tcgen05", "mma", "tcgen05_pp", "tcgen05_pair", "tcgen05_q64"][C.lib().spattn_get_kernel_family()]
 
 
 def _stream() -> int:

@@ -34,7 +34,7 @@ def check(res, q, k, v, R, causal=True, docs=None, ds_rel=None):
         assert_close(key, res[key], orc[key], ref[key])
 
 
-@pytest.mark.parametrize("family", ["tcgen05", "tcgen05_pp", "tcgen05_q128", "mma"])
+@pytest.mark.parametrize("family", ["tcgen05", "tcgen05_pp", "tcgen05_q64", "mma"])
 @pytest.mark.parametrize("L,causal", [(1, True), (2, True), (17, True), (63, False), (129, True),
                                       (255, False), (257, True)])
 def test_short_and_off_boundary_lengths(P, family, L, causal):
@@ -49,7 +49,7 @@ def test_short_and_off_boundary_lengths(P, family, L, causal):
               ds_rel=2e-2 if L == 2 else None)
 
 
-@pytest.mark.parametrize("family", ["tcgen05", "tcgen05_pp", "tcgen05_q128"])
+@pytest.mark.parametrize("family", ["tcgen05", "tcgen05_pp", "tcgen05_q64"])
 @pytest.mark.parametrize("docs", [[1, 1, 126], [1] * 8 + [120], [127, 1, 128], [3, 253]])
 def test_ragged_documents(P, family, docs):
     P.set_kernel_family(family)

@@ -9,7 +9,7 @@ from gpu_util import assert_close, np_, oracle_all, parity_inputs, to_dev, torch
 
 pytestmark = pytest.mark.gpu
 
-FAMILIES = ["tcgen05", "mma", "tcgen05_pp", "tcgen05_pair", "tcgen05_q128"]
+FAMILIES = ["tcgen05", "mma", "tcgen05_pp", "tcgen05_pair", "tcgen05_q64"]
 
 
 @pytest.fixture(scope="module")

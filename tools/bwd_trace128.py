@@ -9,7 +9,7 @@ sys.path.insert(0, ".")
 import paper_2505_22296_b200 as P  # noqa: E402
 from paper_2505_22296_b200 import _lib as C  # noqa: E402
 
-P.set_kernel_family("tcgen05_q128")
+P.set_kernel_family("tcgen05")
 
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 H, Hkv, d = 32, 8, 128
