@@ -2,28 +2,28 @@
 // attn_block_backward (attention.cpp:167-216): delta = rowsum(dO * O); P = exp(S*scale - lse);
 // dV += P^T dO; dS = P (dP - delta) * scale; dQ += dS K; dK += dS^T Q.
 //
-// Why 128-row query tiles: this kernel is bound by the SM's shared-memory port (tensor-core
+// Why 128-row query tiles: the backward is bound by the SM's shared-memory port (tensor-core
 // operand reads plus LSU traffic, one 128-byte wavefront per clock; profiles/r2_bwd.md). With
-// N = 128 every MMA reads its A operand once per 128 queries instead of once per 64: the five
-// products move 256 KB of operands per 128x128 block (352 KB with 64-row tiles).
+// N = 128 every MMA reads its A operand once per 128 queries instead of once per 64.
 //
 // One CTA = one 128-row key/value tile x one kv head; it loops over every (query head of the
 // GQA group, 128-row query tile) that sees the tile. TMEM (512 columns) holds ONE buffer per
 // product, so the softmax-gradient work is split into two phases that each overlap MMAs:
 //   [0, 128)    S^T (lane = key, col = query); phase A writes P^T (bf16) over cols
-//               [64c, 64c+32) of query half c
+//               [64c, 64c+32) of query half c (A operand of dV)
 //   [128, 256)  dV accumulator
-//   [256, 384)  dP^T; phase B writes dS^T (bf16) over [256+64c, +32); dQ (lane = QUERY,
-//               col = head dim) reuses the columns once dK has read dS^T
+//   [256, 384)  dP^T; dQ (lane = QUERY, col = head dim) reuses the columns once phase B has
+//               read dP^T
 //   [384, 512)  dK accumulator
-// Phase A(i): P = exp2(S*scale*log2e - lse*log2e) -> P^T in TMEM (A operand of dV); P stays in
-// registers. Phase B(i): dS = P (dP - delta) -> dS^T in TMEM (A operand of dK) and in smem
-// (A operand of dQ = dS K, read MN-major). MMA issue order per iteration i:
-//   S(i+1)  dK(i)  dQ(i)  dV(i+1)  dP(i+1)
-// so phase A(i+1) runs under dK(i) + dQ(i), phase B(i+1) under S(i+2), and the dQ drain under
-// dV(i+1). Eight softmax warps (two per TMEM lane quadrant, one 64-query half each), four dQ
-// drain warps (lane = query row: 16-byte staging stores, TMA reduce-add in 32-column boxes), a
-// TMA producer and the MMA issuer.
+// Phase A(i): P = exp2(S*scale*log2e - lse*log2e) -> P^T in TMEM; P stays in registers (fp32).
+// Phase B(i): dS = P (dP - delta) -> dS^T to one smem tile, read MN-major as the A operand of
+// dQ = dS K and K-major as the A operand of dK += dS^T Q. MMA issue order per iteration i:
+//   S(i+1)  dQ(i)  dK(i)  dP(i+1)  dV(i+1)
+// dQ goes first so its drain (lane = query: the four drain warps load a whole 128-column row,
+// release the columns, then stage 16-byte rows for the TMA reduce-add) overlaps dK(i); phase
+// B(i+1) starts as soon as dP(i+1) lands, and dV(i+1), which waits for phase A, is off that
+// chain. Eight softmax warps (two per TMEM lane quadrant, one 64-query half each; 144
+// registers), four drain warps (168), producer / allocator / MMA issuer (56).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc::commit(bar(E_DOE));
       for (int it = 0; it < T; ++it) {
         const int s = it % NQ;
-        TR(0, it);
+        TC(0, it);
         if (it + 1 < T) {  // S^T(i+1): P^T(i) was read by dV(i), issued before
           tc::mbar_wait(bar(E_QF + (it + 1) % NQ), ((it + 1) / NQ) & 1);
           tc::fence_after();
@@ -253,27 +253,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         tc::mbar_wait(bar(E_DSR), it & 1);
         tc::fence_after();
-        TR(1, it);
-        tmem_a(T_DK, T_DP, sQ + s * TILE, it == 0);  // dK += dS^T Q
-        tc::commit(bar(E_QE + s));
-        // dQ = dS K (M = 128 queries: the dS^T smem tile read MN-major; B = K MN-major) into the
-        // dP^T columns, whose dS^T dK has just read
+        TC(1, it);
+        // dQ = dS K first (M = 128 queries: the dS^T smem tile read MN-major; B = K MN-major) into
+        // the dP^T columns phase B has consumed, so its drain starts one product earlier
 #pragma unroll 1
         for (int kk = 0; kk < 8; ++kk)
           tc::mma_ss(tmem + T_DP, tc::sdesc(sdS + kk * 2048, 16384, 1024), tc::sdesc(sK + kk * 2048, 16384, 1024),
                      id_q, kk > 0 ? 1u : 0u);
         tc::commit(bar(E_MD));
+        // dK += dS^T Q with dS^T read K-major from the same smem tile (queries 64c.. in block c)
+#pragma unroll 1
+        for (int kk = 0; kk < BQ / 16; ++kk)
+          tc::mma_ss(tmem + T_DK, tc::sdesc(sdS + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                     tc::sdesc(sQ + s * TILE + kk * 2048, 16384, 1024), id_kv, (it > 0 || kk > 0) ? 1u : 0u);
+        tc::commit(bar(E_QE + s));  // Q(i) and the dS^T smem tile are free
         if (it + 1 < T) {
           // dP(i+1) first: phase B(i+1) is on the critical path, dV(i+1) (after phase A) is not
           tc::mbar_wait(bar(E_DOF), (it + 1) & 1);
           tc::mbar_wait(bar(E_DQF), it & 1);  // dQ(i) left the dP^T columns
           tc::fence_after();
-          TR(3, it);
+          TC(3, it);
           kxq(T_DP, sV, sdO);
           tc::commit(bar(E_DPR));
           tc::mbar_wait(bar(E_PR), (it + 1) & 1);  // P^T(i+1)
           tc::fence_after();
-          TR(2, it);
+          TC(2, it);
           tmem_a(T_DV, T_S, sdO, false);  // dV += P^T dO
           tc::commit(bar(E_DOE));
         }
@@ -349,7 +353,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (warp == 0 && t == 0) TC(11, it);
       // phase B: dS = P (dP*scale - delta*scale) -> dS^T to TMEM (dK) and smem (dQ)
       tc::mbar_wait(bar(E_DPR), it & 1);
-      if (it >= 1) tc::mbar_wait(bar(E_MD), (it - 1) & 1);  // dQ(i-1) has read the dS^T smem tile
+      if (it >= 1) tc::mbar_wait(bar(E_QE + (it - 1) % NQ), ((it - 1) / NQ) & 1);  // dQ / dK(i-1) read dS^T
       tc::fence_after();
       if (warp == 0 && t == 0) TR(5, it);
       if (warp == 0 && t == 0) TC(12, it);
@@ -372,15 +376,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                pf[q + 1] * fmaf(__uint_as_float(rp[4 * j + e + 1]), a.scale, dv[e + 1]));
           }
         }
-        tc::tmem_st16(tmem + lb + T_DP + 64 * c + 16 * h2, wd);  // dS^T: A operand of dK
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // dS^T rows of the smem tile: A operand of dQ (MN-major)
+        for (int k = 0; k < 4; ++k) {  // dS^T rows of the smem tile: A of dQ (MN-major) and of dK (K-major)
           const uint32_t addr = tc::sw128(sdS + c * 16384, t, 4 * h2 + k);
           asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(wd[4 * k]), "r"(wd[4 * k + 1]),
                        "r"(wd[4 * k + 2]), "r"(wd[4 * k + 3]));
         }
       }
-      tc::tmem_wait_st();
       tc::fence_proxy_async();
       tc::fence_before();
       tc::mbar_arrive(bar(E_DSR));

@@ -43,3 +43,6 @@ print("median ns: iter->dsr_ok", med(0, 1), " dsr_ok->pr_ok", med(1, 2), " pr_ok
 print("cycles (clock64, same warp): phase A", med(10, 11), " wait A->B", med(11, 12), " phase B", med(12, 13),
       " B end -> next A start", statistics.median([(t[i + 1, 10] - t[i, 13]).item() for i in range(lo + 1, n - 2)]),
       " drain md->dqf", med(14, 15))
+print("MMA thread cycles (clock64): per iteration", (t[n - 1, 0] - t[lo, 0]).item() / (n - 1 - lo),
+      " iter->dsr_ok(B done)", med(0, 1), " dsr_ok->dqf_ok(drain done)", med(1, 3), " dqf_ok->pr_ok", med(3, 2),
+      " pr_ok->next iter", statistics.median([(t[i + 1, 0] - t[i, 2]).item() for i in range(lo + 1, n - 2)]))
