@@ -61,6 +61,19 @@ bool make_tma_2d(CUtensorMap* m, const void* base, uint64_t width, uint64_t rows
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_tma_rows_u64(CUtensorMap* m, const void* base, uint64_t width_u64, uint64_t rows,
+                       uint64_t row_stride_bytes, uint32_t box_w_u64, uint32_t box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {width_u64, rows};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_w_u64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_tma_2d_f32(CUtensorMap* m, const void* base, uint64_t width, uint64_t rows,
                      uint64_t row_stride_elems, uint32_t box_rows) {
   EncodeFn fn = encode_fn();

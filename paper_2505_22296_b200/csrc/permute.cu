@@ -10,7 +10,7 @@
 #include <atomic>
 #include <cstdlib>
 
-#include "common.cuh"
+#include "tc.cuh"
 
 namespace spattn {
 namespace {
@@ -77,6 +77,69 @@ __global__ void __launch_bounds__(256) copy_rows_kernel(CopyLaunch L, int elem_b
         if (off[k] >= 0) *reinterpret_cast<V*>(dst + off[k]) = x[k];
     }
   }
+}
+
+// ----------------------------------------------------------- TMA-staged row copier
+// Plain row copies (every all-to-all pack / unpack without padding or RoPE, shard / gather
+// rows, ring payloads) move as 2-D TMA boxes: per task a source and a destination tensor map
+// over its rows (8-byte elements, no swizzle), boxes of up to 256 x 2 KB (32 KB) staged through
+// shared memory — TMA load into a slot, TMA store out of it — by one issuing lane per CTA with
+// kTmaAhead loads and kTmaSlots - kTmaAhead stores in flight. A box covers many rows, so the
+// ~1 KB rows of an SP=8 pack no longer cost one copy operation each.
+constexpr int kTmaTasks = 48;  // 2 maps + scalars per task in the 32 KB parameter space
+constexpr int kTmaSlots = 7, kTmaAhead = 4, kTmaSlotBytes = 32768;
+constexpr int kTmaSmem = kTmaSlots * kTmaSlotBytes + kTmaSlots * 8;
+struct TmaTask {
+  CUtensorMap src, dst;
+  int br, ncb;  // box rows, column boxes per row block
+};
+struct TmaLaunch {
+  TmaTask t[kTmaTasks];
+  int64_t unit_prefix[kTmaTasks + 1];  // cumulative row blocks x column boxes
+  int box_bytes[kTmaTasks];            // bytes one full box moves (expect_tx; OOB parts count too)
+  int n;
+};
+static_assert(sizeof(TmaLaunch) <= 32000, "kernel parameter space");
+
+__global__ void __launch_bounds__(32, 1) copy_rows_tma_kernel(const __grid_constant__ TmaLaunch L) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t slots = smem_u32(smem), bars = slots + kTmaSlots * kTmaSlotBytes;
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < kTmaSlots; ++i) tc::mbar_init(bars + 8 * i, 1);
+  tc::fence_barrier_init();
+  const int64_t total = L.unit_prefix[L.n];
+  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t u0 = min(total, (int64_t)blockIdx.x * per), u1 = min(total, u0 + per);
+  const int64_t n = u1 - u0;
+  if (n <= 0) return;
+  int tl = 0, ts = 0;  // task cursors of the load and store walks (units only move forward)
+  auto locate = [&](int64_t u, int& t, int& x, int& y) {
+    while (t + 1 < L.n && L.unit_prefix[t + 1] <= u) ++t;
+    const int64_t k = u - L.unit_prefix[t];
+    x = (int)(k % L.t[t].ncb) * 256;
+    y = (int)(k / L.t[t].ncb) * L.t[t].br;
+  };
+  auto load = [&](int64_t j) {
+    int x, y;
+    locate(u0 + j, tl, x, y);
+    const int sl = (int)(j % kTmaSlots);
+    tc::mbar_expect_tx(bars + 8 * sl, (uint32_t)L.box_bytes[tl]);
+    tc::tma_load_2d(slots + sl * kTmaSlotBytes, &L.t[tl].src, x, y, bars + 8 * sl);
+  };
+  for (int64_t j = 0; j < n && j < kTmaAhead; ++j) load(j);
+  for (int64_t j = 0; j < n; ++j) {
+    const int sl = (int)(j % kTmaSlots);
+    int x, y;
+    locate(u0 + j, ts, x, y);
+    tc::mbar_wait(bars + 8 * sl, (uint32_t)((j / kTmaSlots) & 1));
+    tc::tma_store_2d(&L.t[ts].dst, slots + sl * kTmaSlotBytes, x, y);
+    tc::bulk_commit();
+    if (j + kTmaAhead < n) {
+      tc::bulk_wait_read<kTmaSlots - kTmaAhead - 1>();  // store j + kTmaAhead - kTmaSlots read its slot
+      load(j + kTmaAhead);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // stores complete before exit
 }
 
 // fp32 variant that accumulates: dst += src (the repeat_heads backward group sum,
@@ -204,8 +267,48 @@ std::atomic<long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+// TMA path for a task set: every row run 16-byte aligned with a 16-byte-multiple width, no
+// padding columns, at most kTmaTasks tasks; false = use the warp copier.
+bool launch_copy_tasks_tma(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s) {
+  if (ts.n > kTmaTasks) return false;
+  TmaLaunch L;
+  L.n = ts.n;
+  L.unit_prefix[0] = 0;
+  int64_t bytes = 0;
+  for (int i = 0; i < ts.n; ++i) {
+    const CopyTask& t = ts.t[i];
+    const int64_t rb = t.cols * elem_bytes;
+    const char* src = static_cast<const char*>(t.src) + (t.src_row0 * t.src_row_stride + t.src_col0) * elem_bytes;
+    char* dst = static_cast<char*>(t.dst) + (t.dst_row0 * t.dst_row_stride + t.dst_col0) * elem_bytes;
+    if (t.zero_cols || rb <= 0 || rb % 16 || reinterpret_cast<uintptr_t>(src) % 16 ||
+        reinterpret_cast<uintptr_t>(dst) % 16 || (t.src_row_stride * elem_bytes) % 16 ||
+        (t.dst_row_stride * elem_bytes) % 16 || t.rows <= 0 || t.rows > (int64_t)1 << 31)
+      return false;
+    const int64_t w8 = rb / 8, bw = std::min<int64_t>(256, w8);
+    const int br = (int)std::max<int64_t>(1, std::min<int64_t>(256, kTmaSlotBytes / (bw * 8)));
+    if (!make_tma_rows_u64(&L.t[i].src, src, w8, t.rows, t.src_row_stride * elem_bytes, (uint32_t)bw, br) ||
+        !make_tma_rows_u64(&L.t[i].dst, dst, w8, t.rows, t.dst_row_stride * elem_bytes, (uint32_t)bw, br))
+      return false;
+    L.t[i].br = br;
+    L.t[i].ncb = (int)((w8 + 255) / 256);
+    L.box_bytes[i] = (int)(bw * 8 * br);
+    L.unit_prefix[i + 1] = L.unit_prefix[i] + ((t.rows + br - 1) / br) * L.t[i].ncb;
+    bytes += t.rows * rb;
+  }
+  const int64_t total = L.unit_prefix[ts.n];
+  if (total == 0) return true;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148, total));
+  ensure_smem_for(copy_rows_tma_kernel, kTmaSmem);
+  copy_rows_tma_kernel<<<grid, 32, kTmaSmem, s>>>(L);
+  note_launch();
+  (void)bytes;
+  return true;
+}
+
 void launch_copy_tasks(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s) {
   if (ts.n > 0 && ts.t[0].rope) return launch_copy_tasks_rope(ts, s);
+  static const bool no_tma = getenv("SPATTN_NO_TMA_COPY") != nullptr;  // A/B switch (same bytes)
+  if (!no_tma && launch_copy_tasks_tma(ts, elem_bytes, s)) return;
   CopyLaunch L;
   L.ts = ts;
   L.row_prefix[0] = 0;

@@ -72,6 +72,13 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* m, uint32_t
       "r"(x), "r"(y), "r"(src)
       : "memory");
 }
+// 2-D tile store (TMA) of a shared tile to global memory, tracked by the bulk group.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(x), "r"(y), "r"(src)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -296,5 +303,9 @@ bool make_tma_2d(CUtensorMap* m, const void* base, uint64_t width, uint64_t rows
 // fp32 variant (box [box_rows, 32] = 128-byte rows, 128-byte swizzle) for reduce-add stores.
 bool make_tma_2d_f32(CUtensorMap* m, const void* base, uint64_t width, uint64_t rows,
                      uint64_t row_stride_elems, uint32_t box_rows);
+// Row-copy map: rows of `width_u64` 8-byte units at `row_stride_bytes`, no swizzle, box
+// [box_w_u64, box_rows] (the TMA-staged row copier of permute.cu).
+bool make_tma_rows_u64(CUtensorMap* m, const void* base, uint64_t width_u64, uint64_t rows,
+                       uint64_t row_stride_bytes, uint32_t box_w_u64, uint32_t box_rows);
 
 }  // namespace spattn
