@@ -123,8 +123,13 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
     if (cs2) HS_CUDA(cudaStreamWaitEvent(cs2, ready, 0));
     cudaEventDestroy(ready);
 
-    // profiling (wrong results): SPATTN_STEP_NOCOPY=1 skips H2D and D2H, 2 only D2H, 3 only H2D
+    // profiling (wrong results), -DSPATTN_PROFILING builds only: SPATTN_STEP_NOCOPY=1 skips H2D
+    // and D2H, 2 only D2H, 3 only H2D
+#ifdef SPATTN_PROFILING
     static const int nocopy = getenv("SPATTN_STEP_NOCOPY") ? atoi(getenv("SPATTN_STEP_NOCOPY")) : 0;
+#else
+    constexpr int nocopy = 0;
+#endif
     auto h2d = [&](void* dst, const void* src, size_t col_bytes, size_t width, size_t pitch) {
       if (nocopy == 1 || nocopy == 3) return;
       HS_CUDA(cudaMemcpy2DAsync(dst, width, static_cast<const char*>(src) + col_bytes, pitch, width,

@@ -318,7 +318,7 @@ void launch_copy_tasks(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s) {
     rows += ts.t[i].rows;
   }
   // rows per warp chunk: about 4 KB per chunk
-  static const int chunk_bytes = getenv("SPATTN_COPY_CHUNK") ? atoi(getenv("SPATTN_COPY_CHUNK")) : 4096;
+  constexpr int chunk_bytes = 4096;  // measured best of 1 row / 4 KB / 16 KB per warp (profiles/r2/copy_kernels.md)
   const int rpc = (int)std::max<int64_t>(1, chunk_bytes / std::max<int64_t>(1, rows ? bytes / rows : 1));
   for (int i = 0; i < ts.n; ++i) {
     const CopyTask& t = ts.t[i];
