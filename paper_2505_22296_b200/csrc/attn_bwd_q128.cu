@@ -36,7 +36,7 @@ namespace {
 
 constexpr int D = 128, BQ = 128;
 #ifndef Q128_POLY
-#define Q128_POLY 1
+#define Q128_POLY 0
 #endif
 constexpr bool kPolyExp = Q128_POLY;
 constexpr int NCW = 8;                               // softmax-gradient warps
