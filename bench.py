@@ -104,8 +104,9 @@ class Clocks:
 # ------------------------------------------------------------------------- CPU baseline
 def cpu_reference_sample(heads, kv, d, L, threads=None, engine="ulysses"):
     """Time the UNMODIFIED reference (oracle/_ref/ref_driver, built from /root/reference by
-    oracle/Makefile) on a bounded sample of the workload: same head_dim and GQA ratio, 8 query
-    heads, seq 4096, Ulysses over `threads` rank threads (comm.cpp:197-222); extrapolated to the
+    oracle/Makefile) on a bounded sample of the workload: the config's engine, same head_dim and
+    GQA ratio, 8 query heads, seq 2048, over `threads` rank threads (comm.cpp:197-222) — a few
+    seconds per sample, so a 20-step reference arm ends in about a minute; extrapolated to the
     full workload by exact causal pair count x heads."""
     ncpu = os.cpu_count() or 1
     sp = 1
@@ -113,7 +114,7 @@ def cpu_reference_sample(heads, kv, d, L, threads=None, engine="ulysses"):
         sp *= 2
     if threads:
         sp = threads
-    s_heads, s_kv, s_L = 8, max(1, 8 * kv // heads), 4096
+    s_heads, s_kv, s_L = 8, max(1, 8 * kv // heads), 2048
     drv = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
     if os.path.exists(drv):
         out = subprocess.run([drv, "bench", engine, str(sp), str(s_L), str(s_heads), str(s_kv),
