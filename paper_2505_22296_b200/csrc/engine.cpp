@@ -479,12 +479,7 @@ void move_forward_messages(RankCtx& ctx, const CommGroup& g, const std::vector<F
   std::vector<Plan> plans(moves.size());
   std::vector<CopyTask> pack_plain, pack_rope, unpack;
   int elem = 0;
-  bool same_elem = true;
-  for (size_t k = 0; k < moves.size(); ++k) {
-    const MoveSpec& m = *moves[k].m;
-    same_elem &= (elem == 0 || elem == m.elem);
-    elem = m.elem;
-  }
+  for (size_t k = 0; k < moves.size(); ++k) elem = moves[k].m->elem;
   for (size_t k = 0; k < moves.size(); ++k) {
     const MoveSpec& m = *moves[k].m;
     const RopeMove* rope = moves[k].rope;
@@ -515,18 +510,19 @@ void move_forward_messages(RankCtx& ctx, const CommGroup& g, const std::vector<F
                       0, rows, wj.n, 0});
       if (rope) set_rope(pack.back(), rope->table, 0, m.lloc, rope->dim, rope->sign);
     }
-    if (!same_elem)
-      run_tasks(pack, m.elem, false, s);
-    else if (rope)  // rotating packs share one launch of the RoPE copier
+    for (CopyTask& t : pack) t.elem = m.elem;  // plain copies of any dtype share one launch
+    if (rope)  // rotating packs share one launch of the RoPE copier
       pack_rope.insert(pack_rope.end(), pack.begin(), pack.end());
     else
       pack_plain.insert(pack_plain.end(), pack.begin(), pack.end());
+    const size_t first_unpack = unpack.size();
     for (int i = 0; i < G; ++i) {
       if ((w.n == 0 && w.pad == 0) || pl.in_place[i]) continue;
       for (int64_t b = 0; b < m.bs; ++b)
         for (const auto& r : m.runs[static_cast<size_t>(i)])
           unpack.push_back({static_cast<char*>(pl.rbuf.p) + pl.roff[i] * m.elem, moves[k].y, w.n, yw,
                             b * m.lloc + r.row0, b * m.lg + r.pos0, 0, w.ycol, r.n, w.n, w.pad});
+    for (size_t t = first_unpack; t < unpack.size(); ++t) unpack[t].elem = m.elem;
     }
   }
   run_tasks(pack_rope, elem, false, s);
@@ -548,15 +544,7 @@ void move_forward_messages(RankCtx& ctx, const CommGroup& g, const std::vector<F
                          static_cast<size_t>((pl.roff[j + 1] - pl.roff[j]) * m.elem)});
     }
   ctx.transport->send_recv(g, ctx.rank, sends, recvs, s);
-  if (same_elem) {
-    run_tasks(unpack, elem, false, s);
-  } else {
-    for (size_t k = 0, t0 = 0; k < moves.size(); ++k) {  // unpack tasks are in move order
-      std::vector<CopyTask> mine;
-      while (t0 < unpack.size() && unpack[t0].dst == moves[k].y) mine.push_back(unpack[t0++]);
-      run_tasks(mine, moves[k].m->elem, false, s);
-    }
-  }
+  run_tasks(unpack, elem, false, s);  // tasks carry their element sizes
 }
 
 void move_forward(RankCtx& ctx, const CommGroup& g, const MoveSpec& m, const void* x, void* y,
@@ -721,6 +709,7 @@ void move_reverse_messages(RankCtx& ctx, const CommGroup& g, const std::vector<R
   };
   std::vector<Plan> plans(moves.size());
   std::vector<Msg> sends, recvs;
+  std::vector<CopyTask> all_pack;
   for (size_t k = 0; k < moves.size(); ++k) {
     const MoveSpec& m = *moves[k].m;
     Plan& pl = plans[k];
@@ -747,8 +736,10 @@ void move_reverse_messages(RankCtx& ctx, const CommGroup& g, const std::vector<R
             pack.push_back({moves[k].y, dst, ywm, wm.n, b * m.lg + r.pos0, b * m.lloc + r.row0, wm.ycol, 0, r.n,
                             wm.n, 0});
       }
-    run_tasks(pack, m.elem, false, s);
+    for (CopyTask& t : pack) t.elem = m.elem;  // every move's packs share one launch
+    all_pack.insert(all_pack.end(), pack.begin(), pack.end());
   }
+  run_tasks(all_pack, moves.empty() ? 2 : moves[0].m->elem, false, s);
   for (int i = 0; i < G; ++i)
     for (size_t k = 0; k < moves.size(); ++k) {
       const MoveSpec& m = *moves[k].m;
@@ -763,7 +754,7 @@ void move_reverse_messages(RankCtx& ctx, const CommGroup& g, const std::vector<R
                        static_cast<size_t>((pl.roff[i + 1] - pl.roff[i]) * m.elem)});
     }
   ctx.transport->send_recv(g, ctx.rank, sends, recvs, s);
-  // unpacks: rotating ones share one launch, plain ones another (per element size)
+  // unpacks: rotating ones share one launch, plain ones (any element sizes) another
   std::vector<CopyTask> un_rope, un_plain;
   int elem = moves.empty() ? 2 : moves[0].m->elem;
   for (size_t k = 0; k < moves.size(); ++k) {
@@ -778,7 +769,8 @@ void move_reverse_messages(RankCtx& ctx, const CommGroup& g, const std::vector<R
                        m.bs * m.lloc, wj.n, 0});
       if (rope) set_rope(tasks.back(), rope->table, 0, m.lloc, rope->dim, rope->sign);
     }
-    if (m.elem != elem) {
+    for (CopyTask& t : tasks) t.elem = m.elem;
+    if (rope && m.elem != elem) {
       run_tasks(tasks, m.elem, false, s);
       continue;
     }

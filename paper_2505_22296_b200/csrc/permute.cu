@@ -84,11 +84,13 @@ __global__ void __launch_bounds__(256) copy_rows_kernel(CopyLaunch L, int elem_b
 // rows, ring payloads) move as 2-D TMA boxes: per task a source and a destination tensor map
 // over its rows (8-byte elements, no swizzle), boxes of up to 256 x 2 KB (32 KB) staged through
 // shared memory — TMA load into a slot, TMA store out of it — by one issuing lane per CTA with
-// kTmaAhead loads and kTmaSlots - kTmaAhead stores in flight. A box covers many rows, so the
+// several loads and stores in flight (TmaLaunch::slots / ahead). A box covers many rows, so the
 // ~1 KB rows of an SP=8 pack no longer cost one copy operation each.
 constexpr int kTmaTasks = 48;  // 2 maps + scalars per task in the 32 KB parameter space
-constexpr int kTmaSlots = 7, kTmaAhead = 4, kTmaSlotBytes = 32768;
-constexpr int kTmaSmem = kTmaSlots * kTmaSlotBytes + kTmaSlots * 8;
+// Shared memory: kTmaStage bytes split into slots of one box each (32 KB boxes: 7 slots, 4 loads
+// ahead; the kernel takes the slot geometry as a launch parameter).
+constexpr int kTmaMaxSlots = 28, kTmaStage = 7 * 32768;
+constexpr int kTmaSmem = kTmaStage + kTmaMaxSlots * 8;
 struct TmaTask {
   CUtensorMap src, dst;
   int br, ncb;  // box rows, column boxes per row block
@@ -98,14 +100,16 @@ struct TmaLaunch {
   int64_t unit_prefix[kTmaTasks + 1];  // cumulative row blocks x column boxes
   int box_bytes[kTmaTasks];            // bytes one full box moves (expect_tx; OOB parts count too)
   int n;
+  int slots, ahead, slot_bytes;
 };
 static_assert(sizeof(TmaLaunch) <= 32000, "kernel parameter space");
 
 __global__ void __launch_bounds__(32, 1) copy_rows_tma_kernel(const __grid_constant__ TmaLaunch L) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const uint32_t slots = smem_u32(smem), bars = slots + kTmaSlots * kTmaSlotBytes;
+  const uint32_t slots = smem_u32(smem), bars = slots + kTmaStage;
   if (threadIdx.x != 0) return;
-  for (int i = 0; i < kTmaSlots; ++i) tc::mbar_init(bars + 8 * i, 1);
+  const int NS = L.slots, NA = L.ahead, SB = L.slot_bytes;
+  for (int i = 0; i < NS; ++i) tc::mbar_init(bars + 8 * i, 1);
   tc::fence_barrier_init();
   const int64_t total = L.unit_prefix[L.n];
   const int64_t per = (total + gridDim.x - 1) / gridDim.x;
@@ -122,21 +126,28 @@ __global__ void __launch_bounds__(32, 1) copy_rows_tma_kernel(const __grid_const
   auto load = [&](int64_t j) {
     int x, y;
     locate(u0 + j, tl, x, y);
-    const int sl = (int)(j % kTmaSlots);
+    const int sl = (int)(j % NS);
     tc::mbar_expect_tx(bars + 8 * sl, (uint32_t)L.box_bytes[tl]);
-    tc::tma_load_2d(slots + sl * kTmaSlotBytes, &L.t[tl].src, x, y, bars + 8 * sl);
+    tc::tma_load_2d(slots + sl * SB, &L.t[tl].src, x, y, bars + 8 * sl);
   };
-  for (int64_t j = 0; j < n && j < kTmaAhead; ++j) load(j);
+  for (int64_t j = 0; j < n && j < NA; ++j) load(j);
   for (int64_t j = 0; j < n; ++j) {
-    const int sl = (int)(j % kTmaSlots);
+    const int sl = (int)(j % NS);
     int x, y;
     locate(u0 + j, ts, x, y);
-    tc::mbar_wait(bars + 8 * sl, (uint32_t)((j / kTmaSlots) & 1));
-    tc::tma_store_2d(&L.t[ts].dst, slots + sl * kTmaSlotBytes, x, y);
+    tc::mbar_wait(bars + 8 * sl, (uint32_t)((j / NS) & 1));
+    tc::tma_store_2d(&L.t[ts].dst, slots + sl * SB, x, y);
     tc::bulk_commit();
-    if (j + kTmaAhead < n) {
-      tc::bulk_wait_read<kTmaSlots - kTmaAhead - 1>();  // store j + kTmaAhead - kTmaSlots read its slot
-      load(j + kTmaAhead);
+    if (j + NA < n) {
+      // the store that last used slot (j + NA) % NS, j + NA - NS, has read it once at most
+      // NS - NA later stores are pending
+      switch (NS - NA) {
+        case 12: tc::bulk_wait_read<12>(); break;
+        case 6: tc::bulk_wait_read<6>(); break;
+        case 3: tc::bulk_wait_read<3>(); break;
+        default: tc::bulk_wait_read<0>(); break;
+      }
+      load(j + NA);
     }
   }
   asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // stores complete before exit
@@ -268,7 +279,8 @@ void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 // TMA path for a task set: every row run 16-byte aligned with a 16-byte-multiple width, no
-// padding columns, at most kTmaTasks tasks; false = use the warp copier.
+// padding columns, at most kTmaTasks tasks; false = use the warp copier. Tasks may carry their
+// own element size (CopyTask::elem), so moves of different dtypes share one launch.
 bool launch_copy_tasks_tma(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s) {
   if (ts.n > kTmaTasks) return false;
   TmaLaunch L;
@@ -277,23 +289,34 @@ bool launch_copy_tasks_tma(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s
   int64_t bytes = 0;
   for (int i = 0; i < ts.n; ++i) {
     const CopyTask& t = ts.t[i];
-    const int64_t rb = t.cols * elem_bytes;
-    const char* src = static_cast<const char*>(t.src) + (t.src_row0 * t.src_row_stride + t.src_col0) * elem_bytes;
-    char* dst = static_cast<char*>(t.dst) + (t.dst_row0 * t.dst_row_stride + t.dst_col0) * elem_bytes;
-    if (t.zero_cols || rb <= 0 || rb % 16 || reinterpret_cast<uintptr_t>(src) % 16 ||
-        reinterpret_cast<uintptr_t>(dst) % 16 || (t.src_row_stride * elem_bytes) % 16 ||
-        (t.dst_row_stride * elem_bytes) % 16 || t.rows <= 0 || t.rows > (int64_t)1 << 31)
+    const int64_t eb = t.elem ? t.elem : elem_bytes;
+    if (t.zero_cols || t.cols <= 0 || (t.cols * eb) % 16 || t.rows <= 0 || t.rows > (int64_t)1 << 31) return false;
+    bytes += t.rows * t.cols * eb;
+  }
+  // box size: 32 KB (smaller boxes measured slower even for 16 MB launches of 256-byte rows:
+  // the TMA unit's cost follows the rows, not the boxes; profiles/r2/copy_kernels.md)
+  constexpr int box = 32768;
+  L.slot_bytes = box;
+  L.slots = std::min(kTmaMaxSlots, kTmaStage / box);
+  L.ahead = std::max(1, L.slots * 4 / 7);
+  for (int i = 0; i < ts.n; ++i) {
+    const CopyTask& t = ts.t[i];
+    const int64_t eb = t.elem ? t.elem : elem_bytes;
+    const int64_t rb = t.cols * eb;
+    const char* src = static_cast<const char*>(t.src) + (t.src_row0 * t.src_row_stride + t.src_col0) * eb;
+    char* dst = static_cast<char*>(t.dst) + (t.dst_row0 * t.dst_row_stride + t.dst_col0) * eb;
+    if (reinterpret_cast<uintptr_t>(src) % 16 || reinterpret_cast<uintptr_t>(dst) % 16 ||
+        (t.src_row_stride * eb) % 16 || (t.dst_row_stride * eb) % 16)
       return false;
     const int64_t w8 = rb / 8, bw = std::min<int64_t>(256, w8);
-    const int br = (int)std::max<int64_t>(1, std::min<int64_t>(256, kTmaSlotBytes / (bw * 8)));
-    if (!make_tma_rows_u64(&L.t[i].src, src, w8, t.rows, t.src_row_stride * elem_bytes, (uint32_t)bw, br) ||
-        !make_tma_rows_u64(&L.t[i].dst, dst, w8, t.rows, t.dst_row_stride * elem_bytes, (uint32_t)bw, br))
+    const int br = (int)std::max<int64_t>(1, std::min<int64_t>(256, box / (bw * 8)));
+    if (!make_tma_rows_u64(&L.t[i].src, src, w8, t.rows, t.src_row_stride * eb, (uint32_t)bw, br) ||
+        !make_tma_rows_u64(&L.t[i].dst, dst, w8, t.rows, t.dst_row_stride * eb, (uint32_t)bw, br))
       return false;
     L.t[i].br = br;
     L.t[i].ncb = (int)((w8 + 255) / 256);
     L.box_bytes[i] = (int)(bw * 8 * br);
     L.unit_prefix[i + 1] = L.unit_prefix[i] + ((t.rows + br - 1) / br) * L.t[i].ncb;
-    bytes += t.rows * rb;
   }
   const int64_t total = L.unit_prefix[ts.n];
   if (total == 0) return true;
@@ -301,7 +324,6 @@ bool launch_copy_tasks_tma(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s
   ensure_smem_for(copy_rows_tma_kernel, kTmaSmem);
   copy_rows_tma_kernel<<<grid, 32, kTmaSmem, s>>>(L);
   note_launch();
-  (void)bytes;
   return true;
 }
 
@@ -309,6 +331,24 @@ void launch_copy_tasks(const CopyTaskSet& ts, int elem_bytes, cudaStream_t s) {
   if (ts.n > 0 && ts.t[0].rope) return launch_copy_tasks_rope(ts, s);
   static const bool no_tma = getenv("SPATTN_NO_TMA_COPY") != nullptr;  // A/B switch (same bytes)
   if (!no_tma && launch_copy_tasks_tma(ts, elem_bytes, s)) return;
+  bool mixed = false;
+  for (int i = 0; i < ts.n; ++i) mixed |= ts.t[i].elem != 0 && ts.t[i].elem != elem_bytes;
+  if (mixed) {  // the warp copier takes one element size per launch: one launch per size
+    for (int i = 0; i < ts.n; ++i) {
+      const int e = ts.t[i].elem ? ts.t[i].elem : elem_bytes;
+      bool first = true;
+      for (int j = 0; j < i; ++j) first &= (ts.t[j].elem ? ts.t[j].elem : elem_bytes) != e;
+      if (!first) continue;
+      CopyTaskSet sub{};
+      for (int j = 0; j < ts.n; ++j)
+        if ((ts.t[j].elem ? ts.t[j].elem : elem_bytes) == e) {
+          sub.t[sub.n] = ts.t[j];
+          sub.t[sub.n++].elem = 0;
+        }
+      launch_copy_tasks(sub, e, s);
+    }
+    return;
+  }
   CopyLaunch L;
   L.ts = ts;
   L.row_prefix[0] = 0;

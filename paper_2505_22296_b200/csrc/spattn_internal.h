@@ -121,6 +121,9 @@ struct CopyTask {
   const float2* rope = nullptr;
   int64_t rope_row0 = 0, rope_mod = 1;
   int rope_dim = 0, rope_sign = 1;
+  // element size of this task in bytes (0: the launch's); tasks of different sizes share a launch
+  // on the TMA copier (the warp copier splits them by size)
+  int elem = 0;
 };
 constexpr int kMaxCopyTasks = 64;
 struct CopyTaskSet {
