@@ -36,6 +36,13 @@ struct ShardLayout {
   static ShardLayout make_naive(int64_t len, int sp);    // partition.cpp:37-51
   static ShardLayout make_zigzag(int64_t len, int sp);   // partition.cpp:53-73
   static ShardLayout make_usp(int64_t len, int ulysses_degree, int ring_degree);  // :75-103
+  // Extension (not in the reference): the sequence cut into `blocks` equal blocks, each split
+  // zigzag over 2*sp chunks (rank i owns chunks i and 2*sp-1-i of every block). blocks = 1 is
+  // make_zigzag. Mode stays zigzag (the ring engine's layout); for neat-packed batches whose
+  // documents are shorter than the sequence it balances every rank's causal work within each
+  // document, which the single zigzag does not (config c5).
+  static ShardLayout make_zigzag_blocks(int64_t len, int sp, int blocks);
+  int blocks = 1;  // zigzag blocks (1 for every reference layout)
 
   int64_t local_len() const { return global_len / sp; }
   const std::vector<int64_t>& positions_of(int index) const;

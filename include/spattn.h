@@ -27,7 +27,10 @@ enum {
 
 /* Engine (attention.hpp:14) and SplitMode (partition.hpp:14) enumerations, same order. */
 enum { SPATTN_ORACLE = 0, SPATTN_ULYSSES, SPATTN_DUMMY_HEAD, SPATTN_XTUNER, SPATTN_RING, SPATTN_USP };
-enum { SPATTN_NAIVE = 0, SPATTN_ZIGZAG, SPATTN_SPLIT_USP };
+enum { SPATTN_NAIVE = 0, SPATTN_ZIGZAG, SPATTN_SPLIT_USP,
+       /* extension (no reference counterpart): ShardLayout::make_zigzag_blocks with the block
+          count in u_degree — zigzag within each of u_degree equal blocks (mode zigzag) */
+       SPATTN_ZIGZAG_BLOCKS };
 /* Primitive (comm.hpp:19) */
 enum { SPATTN_ALL_TO_ALL = 0, SPATTN_ALL_GATHER, SPATTN_P2P, SPATTN_ALL_REDUCE, SPATTN_BROADCAST };
 

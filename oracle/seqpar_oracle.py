@@ -135,6 +135,22 @@ def layout_owned(mode: str, length: int, sp: int, u: int = 0, r: int = 0) -> lis
         chunk = length // (2 * sp)
         return [np.concatenate([np.arange(c * chunk, (c + 1) * chunk, dtype=np.int64)
                                 for c in (i, 2 * sp - 1 - i)]) for i in range(sp)]
+    if mode.startswith("zigzag:"):
+        # extension with no reference counterpart (the repo's make_zigzag_blocks): zigzag within
+        # each of B equal blocks; B = 1 is the reference zigzag above
+        blocks = int(mode.split(":", 1)[1])
+        if blocks <= 0:
+            raise ConfigError("zigzag blocks: block count must be positive")
+        if blocks == 1:
+            return layout_owned("zigzag", length, sp)
+        _check_divisible(length, sp, "zigzag split")
+        if length % (2 * sp * blocks):
+            raise ConfigError(f"zigzag blocks: length {length} not divisible by 2*sp*blocks = "
+                              f"{2 * sp * blocks}")
+        chunk, bl = length // (2 * sp * blocks), length // blocks
+        return [np.concatenate([np.arange(b * bl + c * chunk, b * bl + (c + 1) * chunk, dtype=np.int64)
+                                for b in range(blocks) for c in (i, 2 * sp - 1 - i)])
+                for i in range(sp)]
     if mode == "usp":
         if u <= 0 or r <= 0:
             raise ConfigError("usp split: degrees must be positive")

@@ -187,7 +187,16 @@ def check(status: int) -> None:
         status, StateError)(msg)
 
 
+ZIGZAG_BLOCKS = 3  # SPATTN_ZIGZAG_BLOCKS (extension): "zigzag:B" = zigzag within each of B blocks
+
+
 def make_layout(mode: str, length: int, sp: int, u: int = 0, r: int = 0) -> SpattnLayout:
+    if mode.startswith("zigzag:"):
+        try:
+            blocks = int(mode.split(":", 1)[1])
+        except ValueError:
+            raise ConfigError(f"unknown split mode '{mode}'") from None
+        return SpattnLayout(ZIGZAG_BLOCKS, sp, length, blocks, 0)
     if mode not in SPLITS:
         raise ConfigError(f"unknown split mode '{mode}'")
     return SpattnLayout(SPLITS.index(mode), sp, length, u, r)

@@ -55,6 +55,7 @@ seqpar::ShardLayout make_layout(const spattn_layout* l) {
   switch (l->mode) {
     case SPATTN_NAIVE: return seqpar::ShardLayout::make_naive(l->global_len, l->sp);
     case SPATTN_ZIGZAG: return seqpar::ShardLayout::make_zigzag(l->global_len, l->sp);
+    case SPATTN_ZIGZAG_BLOCKS: return seqpar::ShardLayout::make_zigzag_blocks(l->global_len, l->sp, l->u_degree);
     case SPATTN_SPLIT_USP: {
       auto L = seqpar::ShardLayout::make_usp(l->global_len, l->u_degree, l->r_degree);
       if (L.sp != l->sp) throw seqpar::ConfigError("usp layout: u*r != sp");

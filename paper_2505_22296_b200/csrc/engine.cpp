@@ -153,50 +153,90 @@ std::vector<SubRun> split_by_docs(const std::vector<PosRun>& runs, const Documen
 // Pairs every query run with every key run of the same document. A pair is skipped when no
 // key is admitted, marked full when every key is admitted, else causal with c <= a + off.
 // Consecutive key runs of one query run are fused when the earlier one is fully admitted
-// (zigzag ring steps and Ulysses both collapse to one problem per query run this way).
+// (zigzag ring steps and Ulysses both collapse to one problem per query run this way): the
+// forward's lists, one problem per query run, so the query-disjoint launches stay few.
+// fuse_q (the backward's lists) fuses the other way: consecutive query runs of one key run,
+// when every row of the later runs admits the whole key run — one problem per key run, so each
+// key tile's backward CTA sweeps all its query tiles once (one dK / dV partial per tile).
 std::vector<AttnProblem> make_problems(const std::vector<PosRun>& qruns,
                                        const std::vector<PosRun>& kruns, bool causal, int64_t bs,
                                        int64_t q_rows_b, int64_t k_rows_b, const Documents* docs,
-                                       int64_t* pairs) {
+                                       int64_t* pairs, bool fuse_q = false) {
   const auto qs = split_by_docs(qruns, docs), ks = split_by_docs(kruns, docs);
-  std::vector<AttnProblem> one;
-  for (const auto& Q : qs) {
-    std::vector<AttnProblem> row;
-    for (const auto& K : ks) {
-      if (K.doc != Q.doc) continue;
-      AttnProblem p{static_cast<int>(Q.row0), static_cast<int>(Q.n), static_cast<int>(K.row0),
+  auto pair_of = [&](const SubRun& Q, const SubRun& K, AttnProblem& p) {
+    p = AttnProblem{static_cast<int>(Q.row0), static_cast<int>(Q.n), static_cast<int>(K.row0),
                     static_cast<int>(K.n), 0, 0};
-      if (causal) {
-        const int64_t off = Q.pos0 - K.pos0;
-        if (off + Q.n - 1 < 0) continue;
-        if (off < K.n - 1) {
-          p.causal = 1;
-          p.off = static_cast<int>(off);
-        }
+    if (causal) {
+      const int64_t off = Q.pos0 - K.pos0;
+      if (off + Q.n - 1 < 0) return false;
+      if (off < K.n - 1) {
+        p.causal = 1;
+        p.off = static_cast<int>(off);
       }
-      row.push_back(p);
     }
-    std::sort(row.begin(), row.end(),
-              [](const AttnProblem& a, const AttnProblem& b) { return a.k_row0 < b.k_row0; });
-    std::vector<AttnProblem> fused;
-    for (const auto& p : row) {
-      if (!fused.empty()) {
-        AttnProblem& f = fused.back();
-        const bool adjacent = f.k_row0 + f.nk == p.k_row0;
-        if (adjacent && !f.causal && (!p.causal || p.off >= -1)) {
-          const int shift = f.nk;
-          f.nk += p.nk;
-          if (p.causal) {
-            f.causal = 1;
-            f.off = p.off + shift;
+    return true;
+  };
+  std::vector<AttnProblem> one;
+  if (!fuse_q) {
+    for (const auto& Q : qs) {
+      std::vector<AttnProblem> row;
+      for (const auto& K : ks) {
+        AttnProblem p;
+        if (K.doc == Q.doc && pair_of(Q, K, p)) row.push_back(p);
+      }
+      std::sort(row.begin(), row.end(),
+                [](const AttnProblem& a, const AttnProblem& b) { return a.k_row0 < b.k_row0; });
+      std::vector<AttnProblem> fused;
+      for (const auto& p : row) {
+        if (!fused.empty()) {
+          AttnProblem& f = fused.back();
+          const bool adjacent = f.k_row0 + f.nk == p.k_row0;
+          if (adjacent && !f.causal && (!p.causal || p.off >= -1)) {
+            const int shift = f.nk;
+            f.nk += p.nk;
+            if (p.causal) {
+              f.causal = 1;
+              f.off = p.off + shift;
+            }
+            continue;
           }
-          continue;
         }
+        fused.push_back(p);
       }
-      fused.push_back(p);
+      one.insert(one.end(), fused.begin(), fused.end());
     }
-    one.insert(one.end(), fused.begin(), fused.end());
+  } else {
+    for (const auto& K : ks) {
+      std::vector<AttnProblem> col;
+      for (const auto& Q : qs) {
+        AttnProblem p;
+        if (K.doc == Q.doc && pair_of(Q, K, p)) col.push_back(p);
+      }
+      std::sort(col.begin(), col.end(),
+                [](const AttnProblem& a, const AttnProblem& b) { return a.q_row0 < b.q_row0; });
+      std::vector<AttnProblem> fused;
+      for (const auto& p : col) {
+        if (!fused.empty()) {
+          AttnProblem& f = fused.back();
+          // rows a >= f.nq of the fused problem admit keys c <= a + f.off: all nk of them when
+          // f.nq + f.off >= nk - 1 (always when f is full)
+          const bool adjacent = f.q_row0 + f.nq == p.q_row0;
+          if (adjacent && !p.causal && (!f.causal || f.nq + f.off >= f.nk - 1)) {
+            f.nq += p.nq;
+            continue;
+          }
+        }
+        fused.push_back(p);
+      }
+      one.insert(one.end(), fused.begin(), fused.end());
+    }
   }
+  // longest CTAs first across the whole launch (a CTA sweeps its problem's key range in the
+  // forward, its query range in the backward): many short runs per rank (block-wise zigzag,
+  // packed documents) would otherwise leave the heavy CTAs for the tail
+  std::stable_sort(one.begin(), one.end(), [&](const AttnProblem& a, const AttnProblem& b) {
+    return fuse_q ? a.nq > b.nq : a.nk > b.nk;
+  });
   std::vector<AttnProblem> all;
   int64_t total = 0;
   for (int64_t b = 0; b < bs; ++b)
@@ -1236,7 +1276,7 @@ void ring_backward(RankCtx& ctx, const CommGroup& grp, const std::vector<std::ve
     const int owner = (me - step + G) % G;
     int64_t pairs = 0;
     auto probs = make_problems(runs[static_cast<size_t>(me)], runs[static_cast<size_t>(owner)],
-                               causal, bs, lrows, lrows, docs, &pairs);
+                               causal, bs, lrows, lrows, docs, &pairs, /*fuse_q=*/true);
     pairs_total += pairs;
     a.k = kv;
     a.v = kv + kvb;

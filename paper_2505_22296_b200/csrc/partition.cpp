@@ -64,6 +64,31 @@ ShardLayout ShardLayout::make_zigzag(int64_t len, int sp) {
   return L;
 }
 
+ShardLayout ShardLayout::make_zigzag_blocks(int64_t len, int sp, int blocks) {
+  if (blocks <= 0) throw ConfigError("zigzag blocks: block count must be positive");
+  if (blocks == 1) return make_zigzag(len, sp);
+  require_split(len, sp, "zigzag split", sp);
+  const int64_t parts = 2 * static_cast<int64_t>(sp) * blocks;
+  if (len % parts) {
+    throw ConfigError("zigzag blocks: length " + std::to_string(len) + " not divisible by 2*sp*blocks = " +
+                      std::to_string(parts));
+  }
+  ShardLayout L;
+  L.mode = SplitMode::zigzag;
+  L.sp = sp;
+  L.global_len = len;
+  L.blocks = blocks;
+  const int64_t c = len / parts, bl = len / blocks;
+  L.owned.resize(static_cast<size_t>(sp));
+  for (int i = 0; i < sp; ++i)
+    for (int b = 0; b < blocks; ++b)
+      for (int64_t ch : {static_cast<int64_t>(i), 2 * static_cast<int64_t>(sp) - 1 - i}) {
+        auto run = span_of(b * bl + ch * c, c);
+        L.owned[static_cast<size_t>(i)].insert(L.owned[static_cast<size_t>(i)].end(), run.begin(), run.end());
+      }
+  return L;
+}
+
 ShardLayout ShardLayout::make_usp(int64_t len, int u, int r) {
   if (u <= 0 || r <= 0) throw ConfigError("usp split: degrees must be positive");
   const ShardLayout ring = make_zigzag(len, r);
@@ -96,7 +121,7 @@ const std::vector<int64_t>& ShardLayout::positions_of(int index) const {
 }
 
 bool ShardLayout::operator==(const ShardLayout& o) const {
-  return mode == o.mode && sp == o.sp && global_len == o.global_len && owned == o.owned;
+  return mode == o.mode && sp == o.sp && global_len == o.global_len && blocks == o.blocks && owned == o.owned;
 }
 
 int64_t causal_pair_count(const ShardLayout& layout, int index) {

@@ -12,6 +12,7 @@ import dataclasses
 import weakref
 from typing import Optional, Sequence
 
+import numpy as np
 import torch
 
 from . import _lib as C
@@ -54,6 +55,31 @@ def pad_length(len: int, sp: int, cutoff_len: int, pad_to_cutoff: bool = False) 
     out = _i64()
     C.check(C.lib().spattn_pad_length(len, sp, cutoff_len, int(pad_to_cutoff), out))
     return out[0]
+
+
+def balanced_zigzag_layout(docs: Sequence[int], sp: int, min_chunk: int = 1024) -> str:
+    """Layout string for the ring over a neat-packed sequence (extension, no reference
+    counterpart): "zigzag:B" with the fewest blocks B (a power of two, L divisible by 2*sp*B,
+    chunks of at least ``min_chunk`` tokens: shorter chunks cost kernel efficiency) whose busiest
+    rank carries within 2 % of the least share of the causal work those B reach (each query
+    attends to the earlier keys of its own document). B = 1 is the reference zigzag."""
+    lens = np.asarray(list(docs), dtype=np.int64)
+    L = int(lens.sum())
+    if sp <= 0 or L <= 0 or (lens <= 0).any():
+        raise ConfigError("balanced_zigzag_layout: documents and sp must be positive")
+    start = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    work = np.arange(L, dtype=np.int64) - np.repeat(start, lens) + 1
+    best = []
+    b = 1
+    while L % (2 * sp * b) == 0 and (b == 1 or L // (2 * sp * b) >= min_chunk):
+        share = max(int(work[np.asarray(shard_positions(f"zigzag:{b}", L, sp, i))].sum())
+                    for i in range(sp)) / int(work.sum())
+        best.append((share, b))
+        b *= 2
+    if not best:
+        raise ConfigError(f"balanced_zigzag_layout: length {L} not divisible by 2*sp = {2 * sp}")
+    lo = min(x for x, _ in best)
+    return f"zigzag:{min(b for x, b in best if x <= lo * 1.02)}"
 
 
 def pick_xtuner_insp(heads: int, sp: int, head_dim: int) -> int:

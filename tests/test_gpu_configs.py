@@ -154,3 +154,27 @@ def test_more_documents_than_one_launch_holds(P):
     docs = (3,) * 1365 + (1,)
     inputs, orc, ref = case(14, sum(docs), 2, 1, 64, docs)
     check(run(P, "oracle", inputs, 1, docs=list(docs)), orc, ref)
+
+
+# ---------------------------------------- block-wise zigzag (extension) for packed batches
+@pytest.mark.parametrize("sp,blocks", [(2, 4), (4, 2), (8, 4)])
+@pytest.mark.parametrize("messages", [False, True])
+def test_c5_ring_zigzag_blocks(P, sp, blocks, messages):
+    """The ring over the block-wise zigzag layout (make_zigzag_blocks): key-major backward
+    problem lists, several runs per rank and document, on both transports."""
+    docs = c5_docs()
+    inputs, orc, ref = case(5, 4096, 32, 8, 128, docs)
+    check(run(P, "ring", inputs, sp, docs=list(docs), layout=f"zigzag:{blocks}",
+              force_messages=messages), orc, ref)
+
+
+@pytest.mark.parametrize("engine,sp", [("ring", 2), ("ring", 4), ("ulysses", 4)])
+def test_zigzag_blocks_dense_and_ragged(P, engine, sp):
+    """No documents (one causal sequence split into 2*sp*blocks chunks) and hundreds of ragged
+    documents crossing the chunk boundaries."""
+    inputs, orc, ref = case(4, 2048, 8, 2, 64)
+    lay = "zigzag:8"
+    check(run(P, engine, inputs, sp, layout=lay), orc, ref)
+    docs = many_docs(2048, 240, 11)
+    inputs, orc, ref = case(13, 2048, 8, 2, 64, docs)
+    check(run(P, engine, inputs, sp, docs=list(docs), layout=lay), orc, ref)

@@ -46,7 +46,7 @@ def c5_docs(total=262144, lo=1024, hi=65536):
     return docs
 
 
-def run(engine, sp, L, H, Hkv, d, docs=None, u=0, r=0, reps=2):
+def run(engine, sp, L, H, Hkv, d, docs=None, u=0, r=0, reps=2, layout="auto"):
     g = torch.Generator(device="cuda").manual_seed(0)
     q = torch.randn(1, L, H, d, device="cuda", generator=g).bfloat16().requires_grad_(True)
     k = torch.randn(1, L, Hkv, d, device="cuda", generator=g).bfloat16().requires_grad_(True)
@@ -60,7 +60,7 @@ def run(engine, sp, L, H, Hkv, d, docs=None, u=0, r=0, reps=2):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         out = P.engine_attention(engine, q, k, v, sp, docs=docs, fabric=fab, ulysses_degree=u,
-                                 ring_degree=r)
+                                 ring_degree=r, layout=layout)
         out.backward(dout)
         torch.cuda.synchronize()
         if rep:  # first run warms up
@@ -102,13 +102,18 @@ def main():
         ("c4", "usp", 8, 131072, 32, 8, 128, None, 2, 4),
         ("c5", "ulysses", 8, 262144, 32, 8, 128, "docs", 0, 0),
         ("c5", "ring", 8, 262144, 32, 8, 128, "docs", 0, 0),
-    ]
+    ] + [("c5", "ring", 8, 262144, 32, 8, 128, "docs", 0, 0, f"zigzag:{b}")
+         for b in next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--c5-blocks=")), "16").split(",")]
+    only = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--only=")]
+    if only:
+        scen = [x for x in scen if x[0] in only[0].split(",")]
+    scen = [x if len(x) == 11 else x + ("auto",) for x in scen]
     if quick:
         scen = [s[:3] + (min(s[3], 16384),) + s[4:] for s in scen if s[0] in ("c1", "c3", "c4")][:5]
     rows = []
-    for name, engine, sp, L, H, Hkv, d, docs, u, r in scen:
+    for name, engine, sp, L, H, Hkv, d, docs, u, r, layout in scen:
         dl = c5_docs(L) if docs == "docs" else None
-        t_all, flops, nbytes = run(engine, sp, L, H, Hkv, d, dl, u, r)
+        t_all, flops, nbytes = run(engine, sp, L, H, Hkv, d, dl, u, r, layout=layout)
         t_all -= shard_overhead(L, H, Hkv, d, sp) if sp > 1 else 0.0
         busiest = max(range(sp), key=lambda i: flops[i])
         share = flops[busiest] / max(1, sum(flops))
@@ -129,7 +134,7 @@ def main():
             exposed += (sp - 1) * 3 * 2 * X * 4 / HBM + g_hop
             t_ovl = t_comp + exposed
         real = 14 * d * H * (L * (L + 1) // 2) if dl is None else sum(14 * d * H * n * (n + 1) // 2 for n in dl)
-        rows.append(dict(config=name, engine=engine, sp=sp, L=L, heads=f"{H}/{Hkv}", d=d,
+        rows.append(dict(config=name, engine=engine if layout == "auto" else f"{engine} ({layout})", sp=sp, L=L, heads=f"{H}/{Hkv}", d=d,
                          docs=len(dl) if dl else 0, t_all_ms=t_all * 1e3,
                          busiest_share=share, t_compute_ms=t_comp * 1e3,
                          bytes_busiest=nbytes[busiest], t_comm_ms=t_comm * 1e3,
