@@ -163,8 +163,9 @@ def run_reference(args, cfg):
             "extrapolated": {"from": samples[-1]["sample"], "full_step_ms": 1000.0 * L / v},
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference Rng uniform(-2,2))", "impl": "reference",
-            "config": {"workload": f"{cfg}: {heads}q/{kv}kv heads d={d} seq {L} causal, bs 1",
-                       "engine": engine, "parallelism": f"sp{args.gpus}"},
+            "config": {"workload": f"{cfg}: {MODEL_OF[cfg]} attention {heads}q/{kv}kv heads "
+                                   f"d={d} seq {L} causal bs 1", "engine": engine,
+                       "parallelism": f"sp{args.gpus}", "global_batch": 1, "seq_len": L},
             "cpu_baseline": {k: samples[-1][k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
