@@ -62,6 +62,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(352, 1)
   const uint32_t rank = tc::cluster_ctarank();
   const bool leader = rank == 0;
   auto lbar = [&](int i) { return tc::mapa(bar(i), 0); };  // the leader's barrier i
+#ifdef FWD_PAIR_RELEASE
+  auto publish = [&](int i) { tc::mbar_arrive_cluster(lbar(i)); };
+#else
+  // local arrive on the leader, relaxed cluster-scope arrive from the peer (its data is ordered
+  // by the tcgen05 / proxy fences before it)
+  auto publish = [&](int i) {
+    if (leader)
+      tc::mbar_arrive(bar(i));
+    else
+      tc::mbar_arrive_cluster_relaxed(lbar(i));
+  };
+#endif
 
   const int warp = threadIdx.x / 32;
   // ---- pair decode (heavy causal pairs first; one head's pairs run together)
@@ -189,7 +201,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(352, 1)
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive_cluster(lbar(B_SFREE + g));
+      if (lane == 0) publish(B_SFREE + g);
       const int n0 = j * 128;
       const bool need_mask = (n0 + 128 > P.nk) || (P.causal && n0 + 127 > m0 + P.off);
       if (need_mask) {
@@ -259,7 +271,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(352, 1)
       tc::fence_before();
       tc::fence_proxy_async();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive_cluster(lbar(B_PF + g));
+      if (lane == 0) publish(B_PF + g);
     }
     // ---- epilogue: merge the two streams; group g writes output columns [g*D/2, (g+1)*D/2)
     const bool valid = qa < P.nq;

@@ -234,6 +234,12 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar) : "memory");
 }
+// relaxed cluster-scope arrive: no release of this thread's prior memory operations (a release at
+// cluster scope waits for every outstanding access of the thread, measured 0.5-2 K cycles);
+// callers order their data with tcgen05 waits / proxy fences first
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar) : "memory");
+}
 // 2-D tile load into this CTA's smem whose completion bytes land on a barrier of the pair's
 // leader (shared::cluster address), as the pair's MMA waits there
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* m, int x, int y,
