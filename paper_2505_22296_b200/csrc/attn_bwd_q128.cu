@@ -95,10 +95,11 @@ __device__ __forceinline__ long long gtimer() {
   return t;
 }
 
+template <class PS>
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_bwd_q128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                         const __grid_constant__ CUtensorMap tmDQ, BwdArgs a, ProblemSet ps) {
+                         const __grid_constant__ CUtensorMap tmDQ, BwdArgs a, PS ps) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   if (sbase & 1023) __trap();
@@ -512,7 +513,8 @@ bool tc_bwd_q128_supported(const BwdArgs& a) {
 }
 
 void launch_attn_bwd_q128(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
-  ProblemSet ps = in;
+  ProblemSet ps;
+  copy_problems(ps, in);
   BwdArgs args = a;
   args.debug = 0;
   args.trace = g_bwd_trace;
@@ -527,8 +529,11 @@ void launch_attn_bwd_q128(const BwdArgs& a, const ProblemSet& in, cudaStream_t s
       !make_tma_2d(&tv, a.v, kw, krows, kw, 128) || !make_tma_2d(&tdo, a.dout, qw, qrows, qw, BQ) ||
       !make_tma_2d_f32(&tdq, a.dq_acc, (uint64_t)a.hm.hq * D, qrows, (uint64_t)a.dq_row_stride, 32))
     launch_error("attn_bwd_q128", "TMA descriptor encode failed (q/k/v/dout/dq base, strides or extents)");
-  ensure_smem_for(attn_bwd_q128_kernel, SMEM);
-  attn_bwd_q128_kernel<<<dim3(tiles * a.hm.hkv), NTHREADS, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
+  with_problem_set(ps, [&](const auto& set) {
+    using PS = std::decay_t<decltype(set)>;
+    ensure_smem_for(attn_bwd_q128_kernel<PS>, SMEM);
+    attn_bwd_q128_kernel<PS><<<dim3(tiles * a.hm.hkv), NTHREADS, SMEM, s>>>(tq, tk, tv, tdo, tdq, args, set);
+  });
   note_launch();
 }
 

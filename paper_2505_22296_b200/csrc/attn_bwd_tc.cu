@@ -130,11 +130,11 @@ __device__ __forceinline__ void grad_chunk(const uint32_t (&rs)[32], const uint3
 #define BWD_DBG(bit) false
 #endif
 
-template <int D>
+template <int D, class PS>
 __global__ void __launch_bounds__(Roles<D>::NTHREADS, 1)
     attn_bwd_tc_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                           const __grid_constant__ CUtensorMap tmDQ, BwdArgs a, ProblemSet ps) {
+                           const __grid_constant__ CUtensorMap tmDQ, BwdArgs a, PS ps) {
   using L = Q64<D>;
   using R = Roles<D>;
   constexpr int NSMW = R::NSMW, DRAIN0 = R::DRAIN0, PRODW = R::PRODW, TALLOCW = R::TALLOCW, MMAW = R::MMAW,
@@ -505,7 +505,8 @@ bool tc_bwd_q64_supported(const BwdArgs& a) {
 
 template <int D>
 void launch_q64_d(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
-  ProblemSet ps = in;
+  ProblemSet ps;
+  copy_problems(ps, in);
   BwdArgs args = a;
 #ifdef SPATTN_PROFILING
   args.debug = getenv("SPATTN_DEBUG") ? atoi(getenv("SPATTN_DEBUG")) : 0;
@@ -524,8 +525,12 @@ void launch_q64_d(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
       !make_tma_2d(&tv, a.v, kw, krows, kw, 128) || !make_tma_2d(&tdo, a.dout, qw, qrows, qw, BQ) ||
       !make_tma_2d_f32(&tdq, a.dq_acc, (uint64_t)a.hm.hq * D, qrows, (uint64_t)a.dq_row_stride, BQ))
     launch_error("attn_bwd_tc_q64", "TMA descriptor encode failed (q/k/v/dout/dq base, strides or extents)");
-  ensure_smem_for(attn_bwd_tc_q64_kernel<D>, Q64<D>::SMEM);
-  attn_bwd_tc_q64_kernel<D><<<dim3(tiles * a.hm.hkv), Roles<D>::NTHREADS, Q64<D>::SMEM, s>>>(tq, tk, tv, tdo, tdq, args, ps);
+  with_problem_set(ps, [&](const auto& set) {
+    using PS = std::decay_t<decltype(set)>;
+    ensure_smem_for(attn_bwd_tc_q64_kernel<D, PS>, Q64<D>::SMEM);
+    attn_bwd_tc_q64_kernel<D, PS><<<dim3(tiles * a.hm.hkv), Roles<D>::NTHREADS, Q64<D>::SMEM, s>>>(tq, tk, tv, tdo, tdq, args,
+                                                                                                   set);
+  });
   note_launch();
 }
 

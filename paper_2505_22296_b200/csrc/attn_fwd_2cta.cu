@@ -49,9 +49,10 @@ constexpr int SMEM = XCH_OFF + 2 * 2 * 128 * 4;
 enum Bar { B_Q = 0, B_KF = 1, B_VF = B_KF + KST, B_SF = B_VF + KST, B_SFREE = B_SF + 2, B_PF = B_SFREE + 2,
            B_PV = B_PF + 2, B_N = B_PV + 2 };
 
+template <class PS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(352, 1)
     attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                         const __grid_constant__ CUtensorMap tmV, FwdArgs a, ProblemSet ps) {
+                         const __grid_constant__ CUtensorMap tmV, FwdArgs a, PS ps) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   if (sbase & 1023) __trap();
@@ -374,7 +375,8 @@ bool tc_fwd_pair_supported(const FwdArgs& a) {
 }
 
 void launch_attn_fwd_pair(const FwdArgs& a, const ProblemSet& in, cudaStream_t s) {
-  ProblemSet ps = in;
+  ProblemSet ps;
+  copy_problems(ps, in);
   ps.tile_prefix[0] = 0;
   for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nq + 255) / 256;
   const int pairs = ps.tile_prefix[ps.n];
@@ -385,8 +387,11 @@ void launch_attn_fwd_pair(const FwdArgs& a, const ProblemSet& in, cudaStream_t s
   if (!make_tma_2d(&tq, a.q, qw, max_rows2(ps, true), qw, 128) || !make_tma_2d(&tk, a.k, kw, krows, kw, 64) ||
       !make_tma_2d(&tv, a.v, kw, krows, kw, 128))
     launch_error("attn_fwd_pair", "TMA descriptor encode failed");
-  ensure_smem_for(attn_fwd_pair_kernel, SMEM);
-  attn_fwd_pair_kernel<<<dim3(2 * pairs, a.hm.hq), 352, SMEM, s>>>(tq, tk, tv, a, ps);
+  with_problem_set(ps, [&](const auto& set) {
+    using PS = std::decay_t<decltype(set)>;
+    ensure_smem_for(attn_fwd_pair_kernel<PS>, SMEM);
+    attn_fwd_pair_kernel<PS><<<dim3(2 * pairs, a.hm.hq), 352, SMEM, s>>>(tq, tk, tv, a, set);
+  });
   note_launch();
 }
 

@@ -66,10 +66,10 @@ __device__ __forceinline__ long long pp_gtimer() {
   return t;
 }
 
-template <int D>
+template <int D, class PS>
 __global__ void __launch_bounds__(352, 1)
     attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                       const __grid_constant__ CUtensorMap tmV, FwdArgs a, ProblemSet ps) {
+                       const __grid_constant__ CUtensorMap tmV, FwdArgs a, PS ps) {
   using Lay = PPLayout<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
@@ -397,7 +397,8 @@ int max_rows_pp(const ProblemSet& ps, bool q) {
 
 template <int D>
 void launch_pp_d(const FwdArgs& a, const ProblemSet& in, cudaStream_t s) {
-  ProblemSet ps = in;
+  ProblemSet ps;
+  copy_problems(ps, in);
   ps.tile_prefix[0] = 0;
   for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nq + 255) / 256;
   const int tiles = ps.tile_prefix[ps.n];
@@ -408,8 +409,11 @@ void launch_pp_d(const FwdArgs& a, const ProblemSet& in, cudaStream_t s) {
       !make_tma_2d(&tk, a.k, kw, max(1, max_rows_pp(ps, false)), kw, 128) ||
       !make_tma_2d(&tv, a.v, kw, max(1, max_rows_pp(ps, false)), kw, 128))
     launch_error("attn_fwd_pp", "TMA descriptor encode failed");
-  ensure_smem_for(attn_fwd_pp_kernel<D>, PPLayout<D>::SMEM);
-  attn_fwd_pp_kernel<D><<<dim3(tiles, a.hm.hq), 352, PPLayout<D>::SMEM, s>>>(tq, tk, tv, a, ps);
+  with_problem_set(ps, [&](const auto& set) {
+    using PS = std::decay_t<decltype(set)>;
+    ensure_smem_for(attn_fwd_pp_kernel<D, PS>, PPLayout<D>::SMEM);
+    attn_fwd_pp_kernel<D, PS><<<dim3(tiles, a.hm.hq), 352, PPLayout<D>::SMEM, s>>>(tq, tk, tv, a, set);
+  });
   note_launch();
 }
 

@@ -34,8 +34,8 @@ __device__ __forceinline__ void load_tile(uint32_t sbase, const __nv_bfloat16* g
 }
 
 // ---------------------------------------------------------------------------------- forward
-template <int D>
-__global__ void __launch_bounds__(kThreads) attn_fwd_mma(FwdArgs a, ProblemSet ps) {
+template <int D, class PS>
+__global__ void __launch_bounds__(kThreads) attn_fwd_mma(FwdArgs a, PS ps) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TILE = kBN * D * 2;
   const uint32_t sQ = smem_u32(smem);
@@ -290,8 +290,8 @@ __global__ void attn_bwd_pre(BwdArgs a, int rows) {
   if (lane == 0) a.delta[(int64_t)row * a.lse_row_stride + h] = acc;
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads) attn_bwd_mma(BwdArgs a, ProblemSet ps) {
+template <int D, class PS>
+__global__ void __launch_bounds__(kThreads) attn_bwd_mma(BwdArgs a, PS ps) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int TILE = kBN * D * 2;
   const uint32_t sK = smem_u32(smem), sV = sK + TILE, sQ = sK + 2 * TILE, sdO = sK + 3 * TILE;
@@ -486,7 +486,8 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_mma(BwdArgs a, ProblemSet p
 }
 
 ProblemSet with_prefix(const ProblemSet& in, int block) {
-  ProblemSet ps = in;
+  ProblemSet ps;
+  copy_problems(ps, in);
   ps.tile_prefix[0] = 0;
   for (int i = 0; i < ps.n; ++i) {
     const int n = (i < ps.n) ? ps.p[i].nq : 0;
@@ -502,16 +503,18 @@ void launch_attn_fwd_mma(const FwdArgs& a, const ProblemSet& in, cudaStream_t s)
   const int tiles = ps.tile_prefix[ps.n];
   if (tiles == 0 || a.hm.hq == 0) return;
   dim3 grid(tiles, a.hm.hq);
-  if (a.d == 64) {
-    const int sm = 5 * kBN * 64 * 2;
-    attn_fwd_mma<64><<<grid, kThreads, sm, s>>>(a, ps);
+  with_problem_set(ps, [&](const auto& set) {
+    using PS = std::decay_t<decltype(set)>;
+    if (a.d == 64) {
+      const int sm = 5 * kBN * 64 * 2;
+      attn_fwd_mma<64, PS><<<grid, kThreads, sm, s>>>(a, set);
+    } else {
+      const int sm = 5 * kBN * 128 * 2;
+      ensure_smem_for(attn_fwd_mma<128, PS>, sm);
+      attn_fwd_mma<128, PS><<<grid, kThreads, sm, s>>>(a, set);
+    }
     note_launch();
-  } else {
-    const int sm = 5 * kBN * 128 * 2;
-    ensure_smem_for(attn_fwd_mma<128>, sm);
-    attn_fwd_mma<128><<<grid, kThreads, sm, s>>>(a, ps);
-    note_launch();
-  }
+  });
 }
 
 // delta with 16-byte loads: TPH = d/8 lanes per (row, head), 32/TPH (row, head) pairs per warp
@@ -559,22 +562,25 @@ void launch_attn_bwd_pre(const BwdArgs& a, int rows, cudaStream_t s) {
 }
 
 void launch_attn_bwd_mma(const BwdArgs& a, const ProblemSet& in, cudaStream_t s) {
-  ProblemSet ps = in;
+  ProblemSet ps;
+  copy_problems(ps, in);
   ps.tile_prefix[0] = 0;
   for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nk + kBN - 1) / kBN;
   const int tiles = ps.tile_prefix[ps.n];
   if (tiles == 0 || a.hm.hkv == 0 || a.hm.hq == 0) return;
   dim3 grid(tiles, a.hm.hkv);
-  if (a.d == 64) {
-    const int sm = 4 * kBN * 64 * 2 + kBN * kBM * 2 + 2 * kBM * 4;
-    attn_bwd_mma<64><<<grid, kThreads, sm, s>>>(a, ps);
+  with_problem_set(ps, [&](const auto& set) {
+    using PS = std::decay_t<decltype(set)>;
+    if (a.d == 64) {
+      const int sm = 4 * kBN * 64 * 2 + kBN * kBM * 2 + 2 * kBM * 4;
+      attn_bwd_mma<64, PS><<<grid, kThreads, sm, s>>>(a, set);
+    } else {
+      const int sm = 4 * kBN * 128 * 2 + kBN * kBM * 2 + 2 * kBM * 4;
+      ensure_smem_for(attn_bwd_mma<128, PS>, sm);
+      attn_bwd_mma<128, PS><<<grid, kThreads, sm, s>>>(a, set);
+    }
     note_launch();
-  } else {
-    const int sm = 4 * kBN * 128 * 2 + kBN * kBM * 2 + 2 * kBM * 4;
-    ensure_smem_for(attn_bwd_mma<128>, sm);
-    attn_bwd_mma<128><<<grid, kThreads, sm, s>>>(a, ps);
-    note_launch();
-  }
+  });
 }
 
 }  // namespace spattn

@@ -270,10 +270,10 @@ enum FwdBar { B_Q = 0, B_KF = 1, B_VF = 3, B_SF = 5, B_SFREE = 7, B_PF = 9, B_PV
 // (1564 with one issuer), so the single issuer is the default.
 constexpr int kFwdThreads = SPATTN_FWD_DUAL_ISSUE ? 384 : 352;
 
-template <int D>
+template <int D, class PS>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                       const __grid_constant__ CUtensorMap tmV, FwdArgs a, ProblemSet ps) {
+                       const __grid_constant__ CUtensorMap tmV, FwdArgs a, PS ps) {
   using Lay = FwdLayout<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
@@ -671,7 +671,8 @@ int max_rows(const ProblemSet& ps, bool q) {
 
 template <int D>
 void launch_fwd_tc_d(const FwdArgs& a, const ProblemSet& in, cudaStream_t s) {
-  ProblemSet ps = in;
+  ProblemSet ps;
+  copy_problems(ps, in);
   ps.tile_prefix[0] = 0;
   for (int i = 0; i < ps.n; ++i) ps.tile_prefix[i + 1] = ps.tile_prefix[i] + (ps.p[i].nq + 127) / 128;
   const int tiles = ps.tile_prefix[ps.n];
@@ -682,8 +683,11 @@ void launch_fwd_tc_d(const FwdArgs& a, const ProblemSet& in, cudaStream_t s) {
       !make_tma_2d(&tk, a.k, kw, max(1, max_rows(ps, false)), kw, 128) ||
       !make_tma_2d(&tv, a.v, kw, max(1, max_rows(ps, false)), kw, 128))
     launch_error("attn_fwd_tc", "TMA descriptor encode failed (q/k/v base, strides or extents)");
-  ensure_smem_for(attn_fwd_tc_kernel<D>, FwdLayout<D>::SMEM);
-  attn_fwd_tc_kernel<D><<<dim3(tiles, a.hm.hq), kFwdThreads, FwdLayout<D>::SMEM, s>>>(tq, tk, tv, a, ps);
+  with_problem_set(ps, [&](const auto& set) {
+    using PS = std::decay_t<decltype(set)>;
+    ensure_smem_for(attn_fwd_tc_kernel<D, PS>, FwdLayout<D>::SMEM);
+    attn_fwd_tc_kernel<D, PS><<<dim3(tiles, a.hm.hq), kFwdThreads, FwdLayout<D>::SMEM, s>>>(tq, tk, tv, a, set);
+  });
   note_launch();
 }
 

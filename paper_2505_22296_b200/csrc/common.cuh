@@ -10,7 +10,8 @@ namespace spattn {
 
 // The problem a launch's tile (or tile pair) index belongs to: the first pi in [0, n) with
 // tile_prefix[pi + 1] > tile (binary search over up to kMaxProblems prefix sums).
-__device__ __forceinline__ int find_problem(const ProblemSet& ps, int tile) {
+template <class PS>
+__device__ __forceinline__ int find_problem(const PS& ps, int tile) {
   int lo = 0, hi = ps.n - 1;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;

@@ -272,7 +272,7 @@ std::vector<std::vector<AttnProblem>> q_disjoint_waves(const std::vector<AttnPro
 }
 
 spattn::ProblemSet to_set(const std::vector<AttnProblem>& v, size_t from, size_t n) {
-  spattn::ProblemSet ps{};
+  spattn::ProblemSet ps;  // only the n problems are set (the struct is 28 KB)
   ps.n = static_cast<int>(n);
   for (size_t i = 0; i < n; ++i) ps.p[i] = v[from + i];
   return ps;

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace spattn {
 
 // One rectangular attention problem in the flattened [rows, heads, dim] row space.
@@ -17,18 +19,49 @@ struct AttnProblem {
   int causal;
 };
 
-// Problems per launch. ProblemSet travels by value in the kernel parameters (CUDA 12.1+ allows
-// 32764 bytes); 1000 problems keep every kernel's parameters (ProblemSet + args + up to five
+// Problems per launch. A problem set travels by value in the kernel parameters (CUDA 12.1+ allows
+// 32764 bytes); 1000 problems keep every kernel's parameters (ProblemSet + args + up to seven
 // 128-byte tensor maps) under that limit, enough for a neat-packed batch of hundreds of
-// documents per launch (larger problem lists are split into several launches).
-constexpr int kMaxProblems = 1000;
+// documents per launch (larger problem lists are split into several launches). The parameter
+// block is copied at every launch, and 28 KB of it costs ~40 us of launch latency (measured at
+// the c1 shape: 82 -> 45 us per forward launch), so every kernel is also instantiated for a
+// 16-problem set, which launches with the one, two or few problems most calls carry.
+#ifndef SPATTN_MAX_PROBLEMS
+#define SPATTN_MAX_PROBLEMS 1000
+#endif
+constexpr int kMaxProblems = SPATTN_MAX_PROBLEMS;
+constexpr int kSmallProblems = 16;
 
-struct ProblemSet {
-  AttnProblem p[kMaxProblems];
-  int tile_prefix[kMaxProblems + 1];  // cumulative q tiles (of the launching kernel's BLOCK_M)
+template <int CAP>
+struct ProblemSetT {
+  static constexpr int kCapacity = CAP;
+  AttnProblem p[CAP];
+  int tile_prefix[CAP + 1];  // cumulative q tiles (of the launching kernel's BLOCK_M)
   int n;
 };
-static_assert(sizeof(ProblemSet) + 5 * 128 + 512 <= 32764, "kernel parameter space");
+using ProblemSet = ProblemSetT<kMaxProblems>;
+using SmallProblemSet = ProblemSetT<kSmallProblems>;
+static_assert(sizeof(ProblemSet) + 7 * 128 + 512 <= 32764, "kernel parameter space");
+
+// Copies the used part of a problem set (the n problems; the prefix is rebuilt by the launcher).
+inline void copy_problems(ProblemSet& out, const ProblemSet& in) {
+  out.n = in.n;
+  for (int i = 0; i < in.n; ++i) out.p[i] = in.p[i];
+}
+
+// Calls f(set) with the smallest problem-set type that holds ps (its n problems and prefix).
+template <class F>
+void with_problem_set(const ProblemSet& ps, F&& f) {
+  if (ps.n <= kSmallProblems) {
+    SmallProblemSet sm;
+    sm.n = ps.n;
+    for (int i = 0; i < ps.n; ++i) sm.p[i] = ps.p[i];
+    for (int i = 0; i <= ps.n; ++i) sm.tile_prefix[i] = ps.tile_prefix[i];
+    f(sm);
+  } else {
+    f(ps);
+  }
+}
 
 // Head mapping of a rank's local tensors: local q head h is global head q_head_base + h; it
 // reads kv head (q_head_base + h) / rep - kv_head_base of the local kv tensor. This indexes
