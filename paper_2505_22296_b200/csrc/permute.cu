@@ -86,7 +86,10 @@ __global__ void __launch_bounds__(256) copy_rows_kernel(CopyLaunch L, int elem_b
 // shared memory — TMA load into a slot, TMA store out of it — by one issuing lane per CTA with
 // several loads and stores in flight (TmaLaunch::slots / ahead). A box covers many rows, so the
 // ~1 KB rows of an SP=8 pack no longer cost one copy operation each.
-constexpr int kTmaTasks = 48;  // 2 maps + scalars per task in the 32 KB parameter space
+#ifndef SPATTN_TMA_TASKS
+#define SPATTN_TMA_TASKS 48
+#endif
+constexpr int kTmaTasks = SPATTN_TMA_TASKS;  // 2 maps + scalars per task in the 32 KB parameter space
 // Shared memory: kTmaStage bytes split into slots of one box each (32 KB boxes: 7 slots, 4 loads
 // ahead; the kernel takes the slot geometry as a launch parameter).
 constexpr int kTmaMaxSlots = 28, kTmaStage = 7 * 32768;

@@ -158,7 +158,10 @@ struct CopyTask {
   // on the TMA copier (the warp copier splits them by size)
   int elem = 0;
 };
-constexpr int kMaxCopyTasks = 64;
+#ifndef SPATTN_MAX_COPY_TASKS
+#define SPATTN_MAX_COPY_TASKS 64
+#endif
+constexpr int kMaxCopyTasks = SPATTN_MAX_COPY_TASKS;
 struct CopyTaskSet {
   CopyTask t[kMaxCopyTasks];
   int n;
