@@ -25,6 +25,11 @@
 #include <mutex>
 
 #include "seqpar/attention.hpp"
+#ifdef SPATTN_PROFILING
+#include <cstdio>
+
+#include <nvtx3/nvToolsExt.h>
+#endif
 #include "spattn_internal.h"
 
 namespace seqpar {
@@ -448,6 +453,21 @@ void attention_backward(cudaStream_t s, const spattn::BwdArgs& base,
 }
 
 void run_tasks(const std::vector<CopyTask>& tasks, int elem, bool add, cudaStream_t s) {
+#ifdef SPATTN_PROFILING
+  if (getenv("SPATTN_TRACE_COPIES")) {  // profiling builds: one line per copy launch
+    int64_t bytes = 0;
+    for (const auto& t : tasks) bytes += t.rows * (t.cols + t.zero_cols) * (t.elem ? t.elem : elem);
+    fprintf(stderr, "copies: %zu tasks, %.1f MB, rows %lld x cols %lld (first), add %d, caller %s\n", tasks.size(),
+            bytes / 1e6, tasks.empty() ? 0LL : (long long)tasks[0].rows, tasks.empty() ? 0LL : (long long)tasks[0].cols,
+            (int)add, getenv("SPATTN_TRACE_TAG") ? getenv("SPATTN_TRACE_TAG") : "");
+  }
+  // profiling builds: the engine's own packs / unpacks under one NVTX range name, so ncu can
+  // select them (--nvtx --nvtx-include "spattn_move/") apart from harness copies
+  struct NvtxRange {
+    NvtxRange() { nvtxRangePushA("spattn_move"); }
+    ~NvtxRange() { nvtxRangePop(); }
+  } nvtx_range;
+#endif
   for (size_t i = 0; i < tasks.size(); i += spattn::kMaxCopyTasks) {
     spattn::CopyTaskSet ts{};
     ts.n = static_cast<int>(std::min<size_t>(spattn::kMaxCopyTasks, tasks.size() - i));
