@@ -1483,8 +1483,10 @@ SavedPtr run_attention_engine(RankCtx& ctx, Engine engine, const AttentionConfig
   if (!lse_local) lse_local = static_cast<float*>(keep(static_cast<size_t>(bs * lloc * H * 4)));
   S->lse = lse_local;
 
-  const bool single = engine == Engine::oracle || (engine != Engine::usp && engine != Engine::xtuner &&
-                                                   engine != Engine::ring && G == 1);
+  // one member: every engine but USP / XTuner is the single block (a one-member ring is its
+  // diagonal step alone, attention.cpp:279-291), run without the ring's fp32 dK/dV accumulators,
+  // rounding passes and k|v staging copy
+  const bool single = engine == Engine::oracle || (engine != Engine::usp && engine != Engine::xtuner && G == 1);
   // RoPE with the caller's global position ids (Model::forward, model.cpp:342-343). Ulysses,
   // Dummy-Head and USP rotate q and k inside the sequence->head copy of the all-to-all; the
   // other engines rotate into a workspace copy first.
