@@ -67,6 +67,20 @@ def test_engines_match_oracle(P, engine, sp, L, H, Hkv, d, messages):
     check_all(res, oracle_all(q, k, v, R), torch_ref(q, k, v, R))
 
 
+@pytest.mark.parametrize("engine", ["ring", "ulysses", "dummy_head"])
+def test_one_member_engines_are_the_single_block(P, engine):
+    # a one-member ring is its diagonal step alone (attention.cpp:279-291): the engines take the
+    # single-block path (bf16 dK / dV, no ring accumulators) and agree with the oracle engine
+    # bit for bit, and with the CPU oracle
+    P.set_kernel_family("tcgen05")
+    q, k, v, R = parity_inputs(41, 384, 8, 2, 128)
+    a = run_engine(P, engine, q, k, v, R, 1)
+    b = run_engine(P, "oracle", q, k, v, R, 1)
+    for key in a:
+        assert np.array_equal(a[key], b[key]), key
+    check_all(a, oracle_all(q, k, v, R), torch_ref(q, k, v, R))
+
+
 def test_dummy_head_equals_ulysses_bitwise_when_divisible(P):
     # tests/test_attention.cpp:455-468
     q, k, v, R = parity_inputs(3, 256, 8, 4, 64)
