@@ -81,8 +81,8 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
   const size_t qw = static_cast<size_t>(hg) * d * 2, kw = static_cast<size_t>(kg) * d * 2;
 
   // Single-device steps alternate groups over two compute streams so one group's backward tail
-  // overlaps the next group's forward; with collectives (sp > 1) one stream keeps every rank's
-  // NCCL calls in the same order.
+  // overlaps the next group's forward (the last group runs after its predecessor); with
+  // collectives (sp > 1) one stream keeps every rank's NCCL calls in the same order.
   cudaStream_t cs = ctx.stream, cs2 = nullptr, up = nullptr, down = nullptr;
   const bool dual = sp == 1 && ng > 1 && !getenv("SPATTN_STEP_SINGLE");  // (profiling switch)
   HS_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
@@ -173,7 +173,10 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
     for (int g = 0; g < ng; ++g) {
       if (g + 1 < ng) load_t(g + 1);
       Slot& s = slots[static_cast<size_t>(g % nslots)];
-      cudaStream_t gs = (dual && (g & 1)) ? cs2 : cs;
+      // the last group follows the one before it on the same stream: two groups that run side
+      // by side finish together and their D2H copies would queue behind each other at the end
+      // of the step (profiles/r2_s3.md: 9.6 -> ~5 ms exposed at 128K)
+      cudaStream_t gs = (dual && (g & 1) && g + 1 < ng) ? cs2 : cs;
       ctx.stream = gs;
       HS_CUDA(cudaStreamWaitEvent(gs, s.loaded, 0));
       tl[static_cast<size_t>(g)][2] = mark(gs);

@@ -1,5 +1,2 @@
-mkdir -p gpurun_out/ct
-SPATTN_LIB=libprof.so timeout 300 ncu --nvtx --nvtx-include "spattn_move/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none -k regex:copy_rows --csv --log-file gpurun_out/ct/msg_only.csv python tools/copy_kernels.py > /dev/null 2>&1
-python tools/ncu_copy_launches.py gpurun_out/ct/msg_only.csv; python tools/ncu_copy_summary.py gpurun_out/ct/msg_only.csv 2>/dev/null | tail -2
-SPATTN_NO_TMA_COPY=1 SPATTN_LIB=libprof.so timeout 300 ncu --nvtx --nvtx-include "spattn_move/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none -k regex:copy_rows --csv --log-file gpurun_out/ct/msg_only_lsu.csv python tools/copy_kernels.py > /dev/null 2>&1
-python tools/ncu_copy_launches.py gpurun_out/ct/msg_only_lsu.csv; python tools/ncu_copy_summary.py gpurun_out/ct/msg_only_lsu.csv 2>/dev/null | tail -2
+SPATTN_STEP_TRACE=1 timeout 300 python tools/step_trace.py 2>&1 | tail -8
+for r in 1 2; do timeout 600 python bench.py --no-secondary --no-cpu-baseline --steps 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value', d['value'], 'e2e', d['e2e']['value'], d['e2e']['ms_per_step'], d['ms_per_step'])"; done
