@@ -227,8 +227,17 @@ namespace {
 #ifndef SPATTN_FWD_POLY_PAIRS
 #define SPATTN_FWD_POLY_PAIRS 0x8
 #endif
-// bit e set: the e-th exponential pair of every 8 columns uses poly_exp2x2 instead of the MUFU
-constexpr int kFwdPolyPairs = SPATTN_FWD_POLY_PAIRS;
+#ifndef SPATTN_FWD_POLY_PAIRS_D64
+#define SPATTN_FWD_POLY_PAIRS_D64 0x0
+#endif
+// bit e set: the e-th exponential pair of every 8 columns uses poly_exp2x2 instead of the MUFU.
+// head_dim 128: one pair in four (the measured optimum); head_dim 64: none — its half-size MMAs
+// leave the MUFU less loaded relative to the chain, and any share on the FMA pipe measured
+// slower (L=32K, 8 heads: 1.51-1.52 ms with none, 1.60-1.64 with 1/4, 1.73 with 1/2).
+template <int D>
+constexpr int fwd_poly_pairs() {
+  return D == 64 ? SPATTN_FWD_POLY_PAIRS_D64 : SPATTN_FWD_POLY_PAIRS;
+}
 
 template <int D>
 struct FwdLayout {
@@ -528,13 +537,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
       for (int e = 0; e < 64; ++e) {
         const float2 av = f2_unpack(f2_fma(f2_pack(x[2 * e], x[2 * e + 1]), sc2, nm2));
-        // pairs in kFwdPolyPairs run on the FMA pipe instead of the MUFU (16/clk/SM)
+        // pairs in fwd_poly_pairs<D>() run on the FMA pipe instead of the MUFU (16/clk/SM)
         float2 pv;
 #ifdef SPATTN_FWD_PROBE_NOEXP
         pv = av;  // profiling probe: no exponentials (wrong results)
         if (false) {
 #else
-        if ((kFwdPolyPairs >> (e & 3)) & 1) {
+        if ((fwd_poly_pairs<D>() >> (e & 3)) & 1) {
 #endif
           pv = poly_exp2x2(av.x, av.y);
         } else {

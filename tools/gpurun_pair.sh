@@ -1,2 +1,2 @@
-SPATTN_STEP_TRACE=1 timeout 300 python tools/step_trace.py 2>&1 | tail -8
-for r in 1 2; do timeout 600 python bench.py --no-secondary --no-cpu-baseline --steps 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value', d['value'], 'e2e', d['e2e']['value'], d['e2e']['ms_per_step'], d['ms_per_step'])"; done
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edges.py tests/test_gpu_configs.py -q -m gpu -x 2>&1 | tail -1
+for shape in "32768 8 8 64 5" "4096 4 4 64 50" "4096 8 8 64 50"; do timeout 120 python tools/shape_bench.py $shape 2>&1 | tail -1; done
