@@ -95,6 +95,9 @@ def main():
         ("c2", "ulysses", 8, 32768, 32, 8, 128, None, 0, 0),
         ("c3", "dummy_head", 8, 65536, 28, 4, 128, None, 0, 0),
         ("c3", "xtuner", 8, 65536, 28, 4, 128, None, 0, 0),
+        # USP with an inner Ulysses degree that divides the 28 heads: no dummy heads, no idle rank
+        ("c3", "usp", 8, 65536, 28, 4, 128, None, 4, 2),
+        ("c3", "usp", 8, 65536, 28, 4, 128, None, 2, 4),
         ("c4", "ring", 2, 131072, 32, 8, 128, None, 0, 0),
         ("c4", "ring", 4, 131072, 32, 8, 128, None, 0, 0),
         ("c4", "ring", 8, 131072, 32, 8, 128, None, 0, 0),
