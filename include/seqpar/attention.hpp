@@ -7,6 +7,7 @@
 
 #include <array>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -86,6 +87,26 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
                              const void* hv, const void* hdout, void* hout, float* hlse, void* hdq,
                              void* hdk, void* hdv, const Documents* docs, int groups);
 int pick_step_groups(Engine e, const AttentionConfig& cfg, int sp);
+
+// Library-internal (host_step.cpp): the single-device causal step (sp = 1, bs = 1, one
+// document) cut along the sequence, so a host pipeline can start computing on the first rows
+// that arrived and copy out the first rows that are final. Forward chunk c covers query rows
+// [r0, r1) against keys [0, r1) and is issued after before_fwd_chunk(c, r1); backward chunk c
+// covers keys [r0, r1) against queries [r0, L) — afterwards dq / dk / dv rows [r0, r1) are final
+// (bf16) and after_bwd_chunk(c, r0, r1) runs. Same math as run_attention_engine + backward.
+struct SequenceChunks {
+  int fwd_chunks = 4, bwd_chunks = 4;
+  std::function<void(int, int64_t)> before_fwd_chunk;
+  std::function<void()> before_backward;
+  std::function<void(int, int64_t, int64_t)> after_bwd_chunk;
+};
+bool single_step_chunkable(RankCtx& ctx, Engine e, const AttentionConfig& cfg, const ShardLayout& layout,
+                           int64_t bs, const Documents* docs);
+void run_single_step_chunked(RankCtx& ctx, Engine e, const AttentionConfig& cfg, const ShardLayout& layout,
+                             const DeviceTensor& q, const DeviceTensor& k, const DeviceTensor& v,
+                             const DeviceTensor& out, float* lse, const DeviceTensor& dout,
+                             const DeviceTensor& dq, const DeviceTensor& dk, const DeviceTensor& dv,
+                             const SequenceChunks& hooks);
 
 // rope_apply (tensor.cpp:548-607) on a bf16 [bs, len, heads, dim] device tensor (inverse:
 // the backward's rotation, tensor.cpp:589-600); out may alias x.

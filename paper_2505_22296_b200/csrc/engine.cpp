@@ -1849,6 +1849,106 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& S, const DeviceTens
   check_launch();
 }
 
+// ------------------------------------------- single-device step cut along the sequence
+bool single_step_chunkable(RankCtx& ctx, Engine e, const AttentionConfig& cfg, const ShardLayout& layout,
+                           int64_t bs, const Documents* docs) {
+  if (layout.sp != 1 || e == Engine::usp || e == Engine::xtuner || !cfg.causal || bs != 1) return false;
+  if (docs && docs->lengths.size() > 1) return false;
+  if (ctx.sp_group.size() != 1 || kernel_family() == KernelFamily::mma) return false;
+  const auto runs = concat_runs(layout, 0, 1);
+  return runs.size() == 1 && runs[0].row0 == 0 && runs[0].pos0 == 0;
+}
+
+void run_single_step_chunked(RankCtx& ctx, Engine e, const AttentionConfig& cfg, const ShardLayout& layout,
+                             const DeviceTensor& q, const DeviceTensor& k, const DeviceTensor& v,
+                             const DeviceTensor& out, float* lse, const DeviceTensor& dout,
+                             const DeviceTensor& dq, const DeviceTensor& dk, const DeviceTensor& dv,
+                             const SequenceChunks& hooks) {
+  validate(ctx, cfg, layout, q, k, v);
+  if (!single_step_chunkable(ctx, e, cfg, layout, q.bs, nullptr))
+    throw StateError("run_single_step_chunked: not a single-device causal step");
+  const int H = cfg.heads, Hkv = cfg.kv_heads > 0 ? cfg.kv_heads : cfg.heads, d = cfg.head_dim;
+  const int64_t L = q.len;
+  cudaStream_t s = ctx.stream;
+  const Local Lc{q.data, k.data, v.data, L, static_cast<int64_t>(H) * d, static_cast<int64_t>(Hkv) * d,
+                 {H, Hkv, 0, 0, H / Hkv}};
+  // chunk boundaries on 128-row tiles
+  auto bounds = [&](int n) {
+    std::vector<int64_t> b{0};
+    const int64_t step = std::max<int64_t>(128, (L / std::max(1, n) + 127) / 128 * 128);
+    while (b.back() < L) b.push_back(std::min(L, b.back() + step));
+    return b;
+  };
+  // forward: query rows [r0, r1) against keys [0, r1) (causal, off = r0); the chunks cover
+  // every row, so no empty-row fill is needed (plain_forward would fill the rows outside ITS
+  // problems, i.e. the earlier chunks' output)
+  spattn::FwdArgs fa{};
+  fa.q = q.data, fa.k = k.data, fa.v = v.data, fa.o = out.data, fa.lse = lse, fa.acc_o = nullptr;
+  fa.q_row_stride = Lc.q_stride, fa.kv_row_stride = Lc.kv_stride, fa.o_row_stride = Lc.q_stride;
+  fa.lse_row_stride = H;
+  fa.d = d;
+  fa.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+  fa.hm = Lc.hm;
+  const auto fb = bounds(hooks.fwd_chunks);
+  int64_t pairs = 0;
+  for (size_t c = 0; c + 1 < fb.size(); ++c) {
+    const int64_t r0 = fb[c], r1 = fb[c + 1];
+    if (hooks.before_fwd_chunk) hooks.before_fwd_chunk(static_cast<int>(c), r1);
+    const std::vector<AttnProblem> probs{{static_cast<int>(r0), static_cast<int>(r1 - r0), 0, static_cast<int>(r1),
+                                          static_cast<int>(r0), 1}};
+    pairs += admitted_pairs(probs[0]);
+    attention_forward(s, fa, probs, false);
+  }
+  ctx.add_flops(4 * d * pairs * H);
+  if (hooks.before_backward) hooks.before_backward();
+  // backward: keys [r0, r1) against queries [r0, L); dq rows [r0, r1) see no later key, so they
+  // are final after chunk c, as are the chunk's dk / dv rows
+  spattn::BwdArgs a{};
+  DevBuf delta(static_cast<size_t>(L * H * 4), s), dqa(static_cast<size_t>(L * H * d * 4), s);
+  dqa.zero();
+  a.q = q.data, a.k = k.data, a.v = v.data, a.o = out.data, a.dout = dout.data, a.lse = lse;
+  a.delta = delta.as<float>();
+  a.dq_acc = dqa.as<float>();
+  a.q_row_stride = Lc.q_stride, a.kv_row_stride = Lc.kv_stride, a.o_row_stride = Lc.q_stride;
+  a.dq_row_stride = Lc.q_stride, a.dkv_row_stride = Lc.kv_stride;
+  a.lse_row_stride = H;
+  a.d = d;
+  a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+  a.hm = Lc.hm;
+  const std::vector<AttnProblem> whole{{0, static_cast<int>(L), 0, static_cast<int>(L), 0, 1}};
+  const bool direct = direct_dkv_ok(Lc, d, whole, dk.data, dv.data) && spattn::bwd_uses_tcgen05(a);
+  DevBuf dka, dva;
+  if (direct) {
+    a.dk_bf16 = dk.data, a.dv_bf16 = dv.data, a.dkv_bf16_row_stride = Lc.kv_stride;
+  } else {
+    dka = DevBuf(static_cast<size_t>(L * Hkv * d * 4), s), dva = DevBuf(static_cast<size_t>(L * Hkv * d * 4), s);
+    dka.zero(), dva.zero();
+    a.dk_acc = dka.as<float>(), a.dv_acc = dva.as<float>();
+  }
+  spattn::launch_attn_bwd_pre(a, static_cast<int>(L), s);
+  check_launch();
+  const auto bb = bounds(hooks.bwd_chunks);
+  for (size_t c = 0; c + 1 < bb.size(); ++c) {
+    const int64_t r0 = bb[c], r1 = bb[c + 1];
+    const std::vector<AttnProblem> probs{{static_cast<int>(r0), static_cast<int>(L - r0), static_cast<int>(r0),
+                                          static_cast<int>(r1 - r0), 0, 1}};
+    attention_backward(s, a, probs);
+    const int64_t qe = Lc.q_stride, ke = Lc.kv_stride;
+    spattn::launch_f32_to_bf16(static_cast<char*>(dq.data) + r0 * qe * 2, dqa.as<float>() + r0 * qe, 1.f,
+                               (r1 - r0) * qe, s);
+    if (!direct) {
+      spattn::launch_f32_to_bf16(static_cast<char*>(dk.data) + r0 * ke * 2, dka.as<float>() + r0 * ke, 1.f,
+                                 (r1 - r0) * ke, s);
+      spattn::launch_f32_to_bf16(static_cast<char*>(dv.data) + r0 * ke * 2, dva.as<float>() + r0 * ke, 1.f,
+                                 (r1 - r0) * ke, s);
+    }
+    check_launch();
+    if (hooks.after_bwd_chunk) hooks.after_bwd_chunk(static_cast<int>(c), r0, r1);
+  }
+  ctx.add_flops(10 * d * pairs * H);
+}
+
+
 // ========================================================================= kernel-level API
 void block_forward_merge(cudaStream_t s, int64_t bs, int heads, int kv_heads, int dim,
                          const void* q, const std::vector<int64_t>& qpos, const void* k,

@@ -90,7 +90,9 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
   if (dual) HS_CUDA(cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking));
   const int nslots = std::min(ng, dual ? 4 : 2);
   std::vector<Slot> slots(static_cast<size_t>(nslots));
+  std::vector<std::pair<int64_t, cudaEvent_t>> rows_landed;  // chunked first group: (row end, event)
   auto cleanup = [&] {
+    for (auto& re : rows_landed) cudaEventDestroy(re.second);
     // copies in flight (also on an error path) finish before the slots go back to the pool
     cudaStreamSynchronize(up);
     cudaStreamSynchronize(down);
@@ -140,12 +142,47 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
       HS_CUDA(cudaMemcpy2DAsync(static_cast<char*>(dst) + col_bytes, pitch, src, width, width,
                                 static_cast<size_t>(rows), cudaMemcpyDeviceToHost, down));
     };
+    // row-range copies (the sequence-chunked first / last group)
+    auto h2d_rows = [&](void* dst, const void* src, size_t col_bytes, size_t width, size_t pitch, int64_t r0,
+                        int64_t r1) {
+      if (nocopy == 1 || nocopy == 3) return;
+      HS_CUDA(cudaMemcpy2DAsync(static_cast<char*>(dst) + static_cast<size_t>(r0) * width, width,
+                                static_cast<const char*>(src) + static_cast<size_t>(r0) * pitch + col_bytes, pitch,
+                                width, static_cast<size_t>(r1 - r0), cudaMemcpyHostToDevice, up));
+    };
+    auto d2h_rows = [&](void* dst, const void* src, size_t col_bytes, size_t width, size_t pitch, int64_t r0,
+                        int64_t r1) {
+      if (nocopy == 1 || nocopy == 2) return;
+      HS_CUDA(cudaMemcpy2DAsync(static_cast<char*>(dst) + static_cast<size_t>(r0) * pitch + col_bytes, pitch,
+                                static_cast<const char*>(src) + static_cast<size_t>(r0) * width, width, width,
+                                static_cast<size_t>(r1 - r0), cudaMemcpyDeviceToHost, down));
+    };
+    // The single-device causal step can run its first group's forward on the first rows that
+    // landed and copy out its last group's first final rows while the rest computes
+    // (run_single_step_chunked): the step no longer waits for a whole group's H2D at the start
+    // nor for a whole group's D2H at the end.
+    const bool chunked = single_step_chunkable(ctx, engine, gc, layout, bs, docs) && !getenv("SPATTN_STEP_NO_CHUNKS");
+    constexpr int kChunks = 4;
     auto load = [&](int g) {
       Slot& s = slots[static_cast<size_t>(g % nslots)];
       if (g >= nslots) HS_CUDA(cudaStreamWaitEvent(up, s.drained, 0));  // slot's last use done
-      h2d(s.q, hq, g * qw, qw, qpitch);
-      h2d(s.k, hk, g * kw, kw, kpitch);
-      h2d(s.v, hv, g * kw, kw, kpitch);
+      if (chunked && g == 0) {
+        const int64_t step = std::max<int64_t>(128, (rows / kChunks + 127) / 128 * 128);
+        for (int64_t r0 = 0; r0 < rows; r0 += step) {
+          const int64_t r1 = std::min(rows, r0 + step);
+          h2d_rows(s.q, hq, g * qw, qw, qpitch, r0, r1);
+          h2d_rows(s.k, hk, g * kw, kw, kpitch, r0, r1);
+          h2d_rows(s.v, hv, g * kw, kw, kpitch, r0, r1);
+          cudaEvent_t e;
+          HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          HS_CUDA(cudaEventRecord(e, up));
+          rows_landed.emplace_back(r1, e);
+        }
+      } else {
+        h2d(s.q, hq, g * qw, qw, qpitch);
+        h2d(s.k, hk, g * kw, kw, kpitch);
+        h2d(s.v, hv, g * kw, kw, kpitch);
+      }
       HS_CUDA(cudaEventRecord(s.loaded, up));  // the forward starts while dout is in flight
       h2d(s.dout, hdout, g * qw, qw, qpitch);
       HS_CUDA(cudaEventRecord(s.dout_loaded, up));
@@ -178,24 +215,55 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
       // of the step (profiles/r2_s3.md: 9.6 -> ~5 ms exposed at 128K)
       cudaStream_t gs = (dual && (g & 1) && g + 1 < ng) ? cs2 : cs;
       ctx.stream = gs;
-      HS_CUDA(cudaStreamWaitEvent(gs, s.loaded, 0));
+      const bool first_chunked = chunked && g == 0, last_chunked = chunked && g + 1 == ng;
+      if (!first_chunked) HS_CUDA(cudaStreamWaitEvent(gs, s.loaded, 0));
       tl[static_cast<size_t>(g)][2] = mark(gs);
       const DeviceTensor tq{s.q, bs, lloc, hg, d}, tk{s.k, bs, lloc, kg, d}, tv{s.v, bs, lloc, kg, d};
       const DeviceTensor to{s.out, bs, lloc, hg, d};
-      SavedPtr saved = run_attention_engine(ctx, engine, gc, layout, tq, tk, tv, to, s.lse, docs);
-      HS_CUDA(cudaStreamWaitEvent(gs, s.dout_loaded, 0));
-      run_attention_engine_backward(ctx, *saved, DeviceTensor{s.dout, bs, lloc, hg, d},
-                                    DeviceTensor{s.dq, bs, lloc, hg, d}, DeviceTensor{s.dk, bs, lloc, kg, d},
-                                    DeviceTensor{s.dv, bs, lloc, kg, d});
-      saved.reset();
+      const DeviceTensor tdo{s.dout, bs, lloc, hg, d}, tdq{s.dq, bs, lloc, hg, d}, tdk{s.dk, bs, lloc, kg, d},
+          tdv{s.dv, bs, lloc, kg, d};
+      int64_t drained_rows = 0;  // rows of dq / dk / dv already on their way out
+      if (first_chunked || last_chunked) {
+        SequenceChunks hk_;
+        hk_.fwd_chunks = first_chunked ? kChunks : 1;
+        hk_.bwd_chunks = last_chunked ? kChunks : 1;
+        hk_.before_fwd_chunk = [&](int, int64_t row_end) {
+          if (!first_chunked) return;
+          for (const auto& re : rows_landed)
+            if (re.first >= row_end) {
+              HS_CUDA(cudaStreamWaitEvent(gs, re.second, 0));
+              return;
+            }
+          HS_CUDA(cudaStreamWaitEvent(gs, s.loaded, 0));
+        };
+        hk_.before_backward = [&] { HS_CUDA(cudaStreamWaitEvent(gs, s.dout_loaded, 0)); };
+        hk_.after_bwd_chunk = [&](int, int64_t r0, int64_t r1) {
+          if (!last_chunked || r1 == rows) return;  // the final rows go out below with the rest
+          cudaEvent_t e;
+          HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          HS_CUDA(cudaEventRecord(e, gs));
+          HS_CUDA(cudaStreamWaitEvent(down, e, 0));
+          cudaEventDestroy(e);  // the wait is enqueued; the event can go
+          d2h_rows(hdq, s.dq, g * qw, qw, qpitch, r0, r1);
+          d2h_rows(hdk, s.dk, g * kw, kw, kpitch, r0, r1);
+          d2h_rows(hdv, s.dv, g * kw, kw, kpitch, r0, r1);
+          drained_rows = r1;
+        };
+        run_single_step_chunked(ctx, engine, gc, layout, tq, tk, tv, to, s.lse, tdo, tdq, tdk, tdv, hk_);
+      } else {
+        SavedPtr saved = run_attention_engine(ctx, engine, gc, layout, tq, tk, tv, to, s.lse, docs);
+        HS_CUDA(cudaStreamWaitEvent(gs, s.dout_loaded, 0));
+        run_attention_engine_backward(ctx, *saved, tdo, tdq, tdk, tdv);
+        saved.reset();
+      }
       ctx.stream = cs;
       tl[static_cast<size_t>(g)][3] = mark(gs);
       HS_CUDA(cudaEventRecord(s.computed, gs));
       HS_CUDA(cudaStreamWaitEvent(down, s.computed, 0));
       tl[static_cast<size_t>(g)][4] = mark(down);
-      d2h(hdq, s.dq, g * qw, qw, qpitch);
-      d2h(hdk, s.dk, g * kw, kw, kpitch);
-      d2h(hdv, s.dv, g * kw, kw, kpitch);
+      d2h_rows(hdq, s.dq, g * qw, qw, qpitch, drained_rows, rows);
+      d2h_rows(hdk, s.dk, g * kw, kw, kpitch, drained_rows, rows);
+      d2h_rows(hdv, s.dv, g * kw, kw, kpitch, drained_rows, rows);
       if (hout) d2h(hout, s.out, g * qw, qw, qpitch);
       if (hlse)
         HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(hlse) + static_cast<size_t>(g) * hg * 4,

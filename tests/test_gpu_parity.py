@@ -233,10 +233,13 @@ def test_native_bytes_closed_form(P):
 
 
 @pytest.mark.parametrize("L,H,Hkv,d,groups", [(256, 8, 4, 128, 0), (256, 8, 4, 64, 2),
-                                              (192, 4, 2, 128, 1), (320, 8, 8, 64, 4)])
+                                              (192, 4, 2, 128, 1), (320, 8, 8, 64, 4),
+                                              (1000, 8, 2, 128, 1), (1000, 8, 2, 128, 2),
+                                              (640, 4, 4, 64, 4)])
 def test_host_step_matches_oracle(P, L, H, Hkv, d, groups):
     """spattn_step_host: host buffers in, host gradients out, copies pipelined over kv-head
-    groups — the same math as the device path."""
+    groups — the same math as the device path (the first and last groups run cut along the
+    sequence: run_single_step_chunked)."""
     P.set_kernel_family("tcgen05")
     q, k, v, R = parity_inputs(500 + L + groups, L, H, Hkv, d)
     cpu = lambda x: torch.from_numpy(x).to(torch.bfloat16)  # noqa: E731
