@@ -92,11 +92,11 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
   std::vector<Slot> slots(static_cast<size_t>(nslots));
   std::vector<std::pair<int64_t, cudaEvent_t>> rows_landed;  // chunked first group: (row end, event)
   auto cleanup = [&] {
-    for (auto& re : rows_landed) cudaEventDestroy(re.second);
     // copies in flight (also on an error path) finish before the slots go back to the pool
     cudaStreamSynchronize(up);
     cudaStreamSynchronize(down);
     if (cs2) cudaStreamSynchronize(cs2);
+    for (auto& re : rows_landed) cudaEventDestroy(re.second);
     ctx.stream = cs;
     for (auto& s : slots) {
       for (void* p : {s.q, s.k, s.v, s.dout, s.out, s.dq, s.dk, s.dv, static_cast<void*>(s.lse)})
