@@ -441,10 +441,50 @@ void attention_forward(cudaStream_t s, const spattn::FwdArgs& base,
   }
 }
 
+// The backward runs one CTA per (128-key tile, kv head). A launch of few, equally long CTAs (a
+// ring step's off-diagonal block at SP=8: 64 key tiles x 8 kv heads = 512 CTAs = 3.46 waves on
+// 148 SMs) leaves SMs idle in its last wave; when dK / dV accumulate in fp32 (no direct bf16
+// rows), each fully admitted problem's query range is cut into pieces on 128-row boundaries
+// (key c of query a is admitted iff c <= a + off, so the piece starting q0 rows later has
+// off + q0), and the pieces' dK / dV partial sums meet in the fp32 accumulators. Measured on the
+// c4 SP=8 step block (16K queries x 8K keys, tools/step_shape.py): 5.15 -> 4.74 ms.
+std::vector<AttnProblem> split_query_ranges(const std::vector<AttnProblem>& probs, int hkv) {
+  static const int forced = getenv("SPATTN_BWD_SPLIT") ? atoi(getenv("SPATTN_BWD_SPLIT")) : 0;
+  int64_t ctas = 0;
+  for (const auto& p : probs) ctas += (p.nk + 127) / 128 * static_cast<int64_t>(hkv);
+  const int64_t target = 6 * 148;  // waves enough for a small last-wave share
+  int parts = forced > 0 ? forced : (ctas > 0 && ctas < target ? static_cast<int>((target + ctas - 1) / ctas) : 1);
+  parts = std::min(parts, 4);
+  if (parts <= 1) return probs;
+  std::vector<AttnProblem> out;
+  for (const auto& p : probs) {
+    const int tiles = (p.nq + 127) / 128;
+    // only fully admitted blocks (a ring step's off-diagonal runs): causal ones already balance
+    // through the heavy-first CTA order, and their pieces would be uneven
+    const bool full = !p.causal || p.off >= p.nk - 1;
+    const int np = full ? std::min(parts, std::max(1, tiles / 4)) : 1;  // >= 4 query tiles per piece
+    if (np <= 1) {
+      out.push_back(p);
+      continue;
+    }
+    for (int i = 0; i < np; ++i) {
+      const int t0 = tiles * i / np, t1 = tiles * (i + 1) / np;
+      AttnProblem q = p;
+      q.q_row0 = p.q_row0 + 128 * t0;
+      q.nq = std::min(p.nq, 128 * t1) - 128 * t0;
+      q.off = p.off + 128 * t0;
+      if (q.nq > 0) out.push_back(q);
+    }
+  }
+  return out;
+}
+
 void attention_backward(cudaStream_t s, const spattn::BwdArgs& base,
-                        const std::vector<AttnProblem>& probs) {
+                        const std::vector<AttnProblem>& in) {
   require_dim(base.d);
   ProfScope prof(s, 1);
+  const std::vector<AttnProblem> probs =
+      base.dk_bf16 || getenv("SPATTN_BWD_NO_SPLIT") ? in : split_query_ranges(in, base.hm.hkv);
   for (size_t i = 0; i < probs.size(); i += spattn::kMaxProblems) {
     const size_t n = std::min<size_t>(spattn::kMaxProblems, probs.size() - i);
     spattn::launch_attn_bwd(base, to_set(probs, i, n), s);
