@@ -308,7 +308,7 @@ def main():
         ems = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
         h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hdo))
         d2h = sum(x.numel() * x.element_size() for x in (hdq, hdk, hdv))
-        groups = args.e2e_groups or C.lib().spattn_pick_step_groups(eid, ctypes.byref(cfg), sp)
+        groups = args.e2e_groups or C.lib().spattn_pick_step_groups_len(eid, ctypes.byref(cfg), sp, lloc)
         return {"value": L / (ems / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ems,
                 "api": "spattn_step_host (C ABI, pinned host buffers)", "head_groups": groups}

@@ -81,12 +81,13 @@ void run_attention_engine_backward(RankCtx& ctx, SavedState& saved, const Device
 // run_attention_engine + tape.backward on host tensors, with the H2D / D2H traffic of
 // independent kv-head groups overlapped with compute. All buffers are [bs, local_len, heads,
 // dim] bf16 (lse fp32 [bs, local_len, heads]); out / lse may be null. groups <= 0 picks the
-// largest of 8, 4, 2, 1 the engine's head constraints allow (pick_step_groups).
+// largest of 8, 4, 2, 1 the engine's head constraints allow — for a multi-rank ring, the
+// largest whose step kernels still fill the GPU (pick_step_groups).
 void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig& cfg,
                              const ShardLayout& layout, int64_t bs, const void* hq, const void* hk,
                              const void* hv, const void* hdout, void* hout, float* hlse, void* hdq,
                              void* hdk, void* hdv, const Documents* docs, int groups);
-int pick_step_groups(Engine e, const AttentionConfig& cfg, int sp);
+int pick_step_groups(Engine e, const AttentionConfig& cfg, int sp, int64_t local_len = 0);
 
 // Library-internal (host_step.cpp): the single-device causal step (sp = 1, bs = 1, one
 // document) cut along the sequence, so a host pipeline can start computing on the first rows

@@ -214,8 +214,10 @@ int spattn_step_host(spattn_ctx* ctx, int engine, const spattn_config* cfg,
                      const void* v, const void* dout, void* out, float* lse, void* dq, void* dk,
                      void* dv, const int64_t* doc_lens, int n_docs, int groups);
 
-/* The head-group count spattn_step_host uses when groups = 0. */
+/* The head-group count spattn_step_host uses when groups = 0 (without the local length: the
+ * head constraints only; with it: as spattn_step_host decides for a multi-rank ring). */
 int spattn_pick_step_groups(int engine, const spattn_config* cfg, int sp);
+int spattn_pick_step_groups_len(int engine, const spattn_config* cfg, int sp, int64_t local_len);
 
 /* Loopback group drivers: one call runs every rank on its own thread (arrays of world
  * pointers), returning when all ranks' streams are idle. */

@@ -30,7 +30,7 @@ EXPORTS = [
     "spattn_shard_rows", "spattn_gather_rows", "spattn_launch_count", "spattn_profile_enable",
     "spattn_profile_read", "spattn_debug_timeline", "spattn_debug_timeline_read", "spattn_selftest_umma", "spattn_plan_heads", "spattn_plan_problems",
     "spattn_debug_bwd_trace", "spattn_debug_fwd_cta_trace", "spattn_debug_transport_selftest", "spattn_fwd_rope", "spattn_fabric_fwd_rope", "spattn_rope_apply",
-    "spattn_step_host", "spattn_pick_step_groups", "spattn_pad_batch",
+    "spattn_step_host", "spattn_pick_step_groups", "spattn_pick_step_groups_len", "spattn_pad_batch",
     "spattn_split_position_map", "spattn_documents_from_segments", "spattn_replicate_packing_mask", "spattn_broadcast_bytes",
     "spattn_fabric_replicate_packing_mask", "spattn_logprob_fwd", "spattn_logprob_bwd",
     "spattn_exact_sum_device", "spattn_exact_sum_host", "spattn_exact_merge", "spattn_exact_round",
@@ -123,6 +123,7 @@ def lib() -> ctypes.CDLL:
                                    ctypes.POINTER(_vp), _i64p, _i32, ctypes.POINTER(_i64p),
                                    ctypes.c_double, ctypes.POINTER(_vp)],
         "spattn_pick_step_groups": [_i32, cfgp, _i32],
+        "spattn_pick_step_groups_len": [_i32, cfgp, _i32, _i64],
         "spattn_logprob_fwd": [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp],
         "spattn_logprob_bwd": [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _i32],
         "spattn_exact_sum_device": [_vp, _vp, _i64, _vp],

@@ -538,6 +538,13 @@ extern "C" int spattn_pick_step_groups(int engine, const spattn_config* cfg, int
     return 1;
   }
 }
+extern "C" int spattn_pick_step_groups_len(int engine, const spattn_config* cfg, int sp, int64_t local_len) {
+  try {
+    return seqpar::pick_step_groups(make_engine(engine), make_cfg(cfg), sp, local_len);
+  } catch (...) {
+    return 1;
+  }
+}
 
 extern "C" int spattn_pad_batch(const int64_t* tokens, const int64_t* labels,
                                 const int64_t* position_ids, const int64_t* segment_ids,

@@ -52,10 +52,22 @@ bool group_ok(Engine e, const AttentionConfig& c, int sp, int ng) {
 
 }  // namespace
 
-int pick_step_groups(Engine e, const AttentionConfig& c, int sp) {
-  for (int ng : {8, 4, 2})
-    if (group_ok(e, c, sp, ng)) return ng;
-  return 1;
+int pick_step_groups(Engine e, const AttentionConfig& c, int sp, int64_t local_len) {
+  // A ring rank's off-diagonal step block has local_len / 2 keys against local_len queries; its
+  // backward launch should keep >= ~6 waves on 148 SMs even after the query-range split (at
+  // most 4 pieces, engine.cpp split_query_ranges), or the step's kernels idle in their last
+  // wave: at c4 SP=8 one kv head per group gives 64 key tiles x 4 = 256 CTAs, four heads 1024.
+  const int Hkv = c.kv_heads > 0 ? c.kv_heads : c.heads;
+  const bool ring = e == Engine::ring && sp > 1 && local_len > 0;
+  int fallback = 1;
+  for (int ng : {8, 4, 2}) {
+    if (!group_ok(e, c, sp, ng)) continue;
+    if (!ring) return ng;
+    fallback = ng;  // smallest allowed so far
+    const int64_t ctas = 4 * ((local_len / 2 + 127) / 128) * (Hkv / ng);
+    if (ctas >= 6 * 148) return ng;
+  }
+  return ring ? 1 : fallback;
 }
 
 void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig& cfg,
@@ -64,7 +76,7 @@ void run_attention_step_host(RankCtx& ctx, Engine engine, const AttentionConfig&
                              void* hdk, void* hdv, const Documents* docs, int groups) {
   const int H = cfg.heads, Hkv = cfg.kv_heads > 0 ? cfg.kv_heads : cfg.heads, d = cfg.head_dim;
   const int sp = layout.sp;
-  const int ng = groups > 0 ? groups : pick_step_groups(engine, cfg, sp);
+  const int ng = groups > 0 ? groups : pick_step_groups(engine, cfg, sp, layout.local_len());
   if (!group_ok(engine, cfg, sp, ng))
     throw ConfigError("host step: " + std::to_string(ng) + " head groups do not split heads=" +
                       std::to_string(H) + ", kv_heads=" + std::to_string(Hkv) + " for engine " +
