@@ -203,6 +203,61 @@ def test_block_merge_equals_whole(P):
     np.testing.assert_allclose(accs[1][1], accs[0][1], atol=1e-4)
 
 
+@pytest.mark.parametrize("d", [64, 128])
+def test_block_backward_query_split_matches(P, d, monkeypatch):
+    """A fully admitted block (every query sees every key: a ring step's off-diagonal block) on
+    an fp32-accumulating backward launch of few CTAs is cut along the query range
+    (engine.cpp split_query_ranges); its dq / dk / dv equal the uncut launch's up to fp32
+    summation order, and the reference gradients of that block."""
+    import ctypes
+
+    from paper_2505_22296_b200 import _lib as C
+
+    lq, lk, H, Hkv = 1000, 384, 4, 2
+    rng = np.random.default_rng(17)
+    bf = lambda *s: O.bf16_round(rng.uniform(-2, 2, s))  # noqa: E731
+    q, k, v = bf(1, lq, H, d), bf(1, lk, Hkv, d), bf(1, lk, Hkv, d)
+    R = rng.uniform(-1, 1, (1, lq, H, d))
+    qpos = np.arange(lk, lk + lq, dtype=np.int64)  # queries after every key: all admitted
+    kpos = np.arange(lk, dtype=np.int64)
+    s = torch.cuda.current_stream().cuda_stream
+    qt, kt, vt = to_dev(q), to_dev(k), to_dev(v)
+    # forward of the block (merge into an empty accumulator), then its backward
+    acc_o = torch.zeros(1, lq, H, d, device="cuda")
+    acc_l = torch.full((1, lq, H), float("-inf"), device="cuda")
+    C.check(C.lib().spattn_block_fwd(s, 1, H, Hkv, d, qt.data_ptr(), qpos.ctypes.data_as(C._i64p), lq,
+                                     kt.data_ptr(), vt.data_ptr(), kpos.ctypes.data_as(C._i64p), lk, 1,
+                                     1 / np.sqrt(d), acc_o.data_ptr(), acc_l.data_ptr(), None))
+    out = acc_o.bfloat16()
+    dout = to_dev(R).bfloat16()
+    res = []
+    for split in (True, False):
+        if split:
+            monkeypatch.delenv("SPATTN_BWD_NO_SPLIT", raising=False)
+        else:
+            monkeypatch.setenv("SPATTN_BWD_NO_SPLIT", "1")
+        dq = torch.zeros(1, lq, H, d, device="cuda")
+        dk = torch.zeros(1, lk, Hkv, d, device="cuda")
+        dv = torch.zeros(1, lk, Hkv, d, device="cuda")
+        C.check(C.lib().spattn_block_bwd(s, 1, H, Hkv, d, qt.data_ptr(), qpos.ctypes.data_as(C._i64p), lq,
+                                         kt.data_ptr(), vt.data_ptr(), kpos.ctypes.data_as(C._i64p), lk, 1,
+                                         1 / np.sqrt(d), out.data_ptr(), acc_l.data_ptr(), dout.data_ptr(),
+                                         dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), None))
+        torch.cuda.synchronize()
+        res.append([x.double().cpu().numpy() for x in (dq, dk, dv)])
+    for a, b, name in zip(res[0], res[1], ("dq", "dk", "dv")):
+        np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-5 * max(1.0, np.abs(b).max()), err_msg=name)
+    # against torch fp32 on the same bf16 inputs (full attention of the block)
+    qf, kf, vf = (torch.from_numpy(x).float().cuda().requires_grad_(True) for x in (q, k, v))
+    rep = H // Hkv
+    sc = torch.einsum("blhd,bmhd->bhlm", qf, kf.repeat_interleave(rep, 2)) / d ** 0.5
+    o = torch.einsum("bhlm,bmhd->blhd", sc.softmax(-1), vf.repeat_interleave(rep, 2))
+    o.backward(dout.float())
+    for got, want, name in zip(res[0], (qf.grad, kf.grad, vf.grad), ("dq", "dk", "dv")):
+        w = want.double().cpu().numpy()
+        assert np.abs(got - w).max() <= 2e-2 * max(1.0, np.abs(w).max()), name
+
+
 def test_flop_counters_match_reference_pairs(P):
     # the reference charges 4d fwd + 10d bwd per admitted pair (attention.cpp:113, :215)
     L, H, d = 256, 4, 64
